@@ -1,0 +1,742 @@
+// far_oracle.cpp — plain, slow, single-threaded CPU ORACLE of FAR (arXiv 2507.13601).
+//
+// TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+// cpu_baseline / --impl reference legs may load this library.  It shares no code
+// with the CUDA path.  Every function follows PAPER.md step by step (citations
+// "P:<line>" = /root/reference/PAPER.md line) under the readings of SURVEY.md §8(c)
+// / DESIGN.md "Readings".  Library primitives used as steps: std::sort,
+// std::priority_queue.  All arithmetic in int64.
+//
+// Parity pins: see tests/test_oracle_*.py (partition counts, SPEC traces, bounds,
+// brute force, validator, golden phase-3 examples).  The multi-batch stream fold
+// (O8) lives in far_oracle_stream.cpp.
+
+#include "far_oracle.h"
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <deque>
+#include <functional>
+#include <limits>
+#include <queue>
+#include <vector>
+
+namespace {
+
+using i64 = int64_t;
+
+// ---------------------------------------------------------------------------
+// L0: MIG model.  P:71-87 (slices, instances, partitions), Fig. 3 repartition
+// trees (image stripped; reconstructed from P:386, P:726, P:783 — the odd-size
+// split gives the first child one extra slice — and P:84-85, the 3-in-4 node).
+// SURVEY.md §8c O1 fixes node ids.
+// ---------------------------------------------------------------------------
+struct TreeNode {
+  int lo, hi;                 // slice interval [lo, hi)
+  std::vector<int> hosted;    // hosted task sizes, in priority order
+  std::vector<int> children;  // child node ids
+  int parent;
+  int size() const { return hi - lo; }
+};
+
+struct Model {
+  int slices = 0;
+  std::vector<int> sizes;     // C_G
+  std::vector<TreeNode> node; // node 0 = root
+  bool ok = false;
+};
+
+Model make_model(int profile) {
+  Model m;
+  if (profile == 0) {  // A30: 4 -> {2,2} -> 4 leaves
+    m.slices = 4;
+    m.sizes = {1, 2, 4};
+    m.node = {
+        {0, 4, {4}, {1, 2}, -1}, {0, 2, {2}, {3, 4}, 0}, {2, 4, {2}, {5, 6}, 0},
+        {0, 1, {1}, {}, 1},      {1, 2, {1}, {}, 1},     {2, 3, {1}, {}, 2}, {3, 4, {1}, {}, 2},
+    };
+    m.ok = true;
+  } else if (profile == 1 || profile == 2) {  // A100/H100: same tree (Q29)
+    m.slices = 7;
+    m.sizes = {1, 2, 3, 4, 7};
+    m.node = {
+        {0, 7, {7}, {1, 2}, -1},
+        {0, 4, {4, 3}, {3, 4}, 0},  // {S0..S3}: size-4 tasks first, then size-3 tasks
+        {4, 7, {3}, {5, 6}, 0},     // {S4..S6}
+        {0, 2, {2}, {7, 8}, 1},  {2, 4, {2}, {9, 10}, 1}, {4, 6, {2}, {11, 12}, 2},
+        {6, 7, {1}, {}, 2},
+        {0, 1, {1}, {}, 3},  {1, 2, {1}, {}, 3}, {2, 3, {1}, {}, 4}, {3, 4, {1}, {}, 4},
+        {4, 5, {1}, {}, 5},  {5, 6, {1}, {}, 5},
+    };
+    m.ok = true;
+  }
+  return m;
+}
+
+int size_index(const Model& m, int s) {
+  for (size_t c = 0; c < m.sizes.size(); ++c)
+    if (m.sizes[c] == s) return (int)c;
+  return -1;
+}
+
+struct Costs {
+  std::vector<i64> create, destroy;  // per size index (Table 2)
+  i64 cr(const Model& m, int node) const { return create[size_index(m, m.node[node].size())]; }
+  i64 de(const Model& m, int node) const { return destroy[size_index(m, m.node[node].size())]; }
+};
+
+struct Problem {
+  Model m;
+  Costs c;
+  int n = 0;
+  std::vector<std::vector<i64>> t;  // t[i][c] = t_i(sizes[c])
+  i64 time(int i, int size) const { return t[i][size_index(m, size)]; }
+};
+
+// Input checks shared by every entry point.
+int load_problem(int profile, const int32_t* costs, const int32_t* times, int n, bool zero, Problem& P) {
+  P.m = make_model(profile);
+  if (!P.m.ok) return -2;
+  if (n < 0 || (n > 0 && !times)) return -1;
+  if (n > 1024) return -4;
+  const int nc = (int)P.m.sizes.size();
+  P.n = n;
+  P.c.create.assign(nc, 0);
+  P.c.destroy.assign(nc, 0);
+  if (costs && !zero) {
+    for (int c = 0; c < nc; ++c) {
+      P.c.create[c] = costs[c];
+      P.c.destroy[c] = costs[nc + c];
+      if (costs[c] < 0 || costs[nc + c] < 0) return -3;
+    }
+  }
+  P.t.assign(n, std::vector<i64>(nc, 0));
+  i64 bound = 0;
+  for (int i = 0; i < n; ++i) {
+    i64 mx = 0;
+    for (int c = 0; c < nc; ++c) {
+      P.t[i][c] = times[(size_t)i * nc + c];
+      if (P.t[i][c] < 1) return -3;
+      mx = std::max(mx, P.t[i][c]);
+    }
+    bound += mx;
+  }
+  for (size_t v = 0; v < P.m.node.size(); ++v) bound += P.c.cr(P.m, (int)v) + P.c.de(P.m, (int)v);
+  if (bound >= (i64(1) << 30)) return -3;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Phase 1: Turek family of allocations.  Allocations hold size VALUES.
+// ---------------------------------------------------------------------------
+std::vector<std::vector<int>> allocation_family(const Problem& P) {
+  const Model& m = P.m;
+  std::vector<std::vector<int>> fam;
+  if (P.n == 0) return fam;
+  // First allocation: a_i = argmin_{s in C_G} s * t_i(s); ties -> smallest s (Q3).
+  std::vector<int> a(P.n);
+  for (int i = 0; i < P.n; ++i) {
+    int best = -1;
+    i64 bw = 0;
+    for (int s : m.sizes) {
+      i64 w = (i64)s * P.time(i, s);
+      if (best < 0 || w < bw) { best = s; bw = w; }
+    }
+    a[i] = best;
+  }
+  fam.push_back(a);
+  // a^{k+1} from a^k: grow the longest task (ties -> lowest index, Q2)
+  // to argmin_{s > a_j} s * t_j(s) (ties -> smallest s, Q3); stop when it cannot grow (Q4).
+  for (;;) {
+    int j = 0;
+    for (int i = 1; i < P.n; ++i)
+      if (P.time(i, a[i]) > P.time(j, a[j])) j = i;
+    if (a[j] == m.sizes.back()) break;
+    int best = -1;
+    i64 bw = 0;
+    for (int s : m.sizes) {
+      if (s <= a[j]) continue;
+      i64 w = (i64)s * P.time(j, s);
+      if (best < 0 || w < bw) { best = s; bw = w; }
+    }
+    a[j] = best;
+    fam.push_back(a);
+  }
+  return fam;
+}
+
+// ---------------------------------------------------------------------------
+// Schedule representation: the output tree of Alg. 1 — per node an
+// ordered task list — plus per-task start times and the reconfiguration events.
+// ---------------------------------------------------------------------------
+struct Sched {
+  std::vector<std::vector<int>> list;  // per node: task ids in execution order
+  std::vector<int> node, size_used;    // per task
+  std::vector<i64> start;              // per task
+  std::vector<orc_event> events;
+  i64 makespan = 0;
+  i64 pops = 0;
+};
+
+i64 dur(const Problem& P, const Sched& S, int j) { return P.time(j, S.size_used[j]); }
+
+// ---------------------------------------------------------------------------
+// Phase 2: Alg. 1 "Schedule an allocation by repartitioning", and the
+// line-26 replay of Alg. 2 (O7), which is the same event loop taking each node's
+// tasks from its (refined) list instead of from the per-size LPT groups.
+//   mode ALLOC : alloc given; groups by size, LPT (lines 1-2)
+//   mode LISTS : lists given (per node, in order) with size_used per task
+// ---------------------------------------------------------------------------
+Sched run_event_loop(const Problem& P, const std::vector<int>* alloc,
+                     const std::vector<std::vector<int>>* lists, const std::vector<int>* size_used_in) {
+  const Model& m = P.m;
+  const int N = (int)m.node.size();
+  Sched S;
+  S.list.assign(N, {});
+  S.node.assign(P.n, -1);
+  S.size_used.assign(P.n, 0);
+  S.start.assign(P.n, 0);
+
+  // Lines 1-2: group the tasks by allotted size, order each group by decreasing
+  // time (LPT); ties -> lower task index (Q9).
+  std::vector<std::vector<int>> group(m.sizes.size());
+  std::vector<size_t> gptr(m.sizes.size(), 0);
+  std::vector<size_t> lptr(N, 0);
+  if (alloc) {
+    for (int i = 0; i < P.n; ++i) group[size_index(m, (*alloc)[i])].push_back(i);
+    for (size_t c = 0; c < group.size(); ++c) {
+      const int s = m.sizes[c];
+      std::sort(group[c].begin(), group[c].end(), [&](int x, int y) {
+        if (P.time(x, s) != P.time(y, s)) return P.time(x, s) > P.time(y, s);
+        return x < y;
+      });
+    }
+  }
+  int unscheduled = P.n;
+
+  std::vector<i64> end(N, 0);
+  std::vector<bool> has_tasks(N, false);
+  i64 reconfig_end = 0;  // line 3
+  // Min-heap of instances ordered by end time (line 4); ties -> lower first slice (Q8).
+  using Key = std::pair<i64, int>;  // (end, lo) ; node recovered from lo via map below
+  auto cmp = [](const std::pair<Key, int>& a, const std::pair<Key, int>& b) { return a.first > b.first; };
+  std::priority_queue<std::pair<Key, int>, std::vector<std::pair<Key, int>>, decltype(cmp)> heap(cmp);
+  heap.push({{0, m.node[0].lo}, 0});  // root, R.end = 0, R.tasks = []
+
+  while (!heap.empty()) {  // line 5
+    const int v = heap.top().second;  // line 6: pop the first instance to end
+    heap.pop();
+    S.pops++;
+    const int vs = m.node[v].size();
+    // Line 7: are there unscheduled tasks assigned to |I| (a hosted size of I)?
+    int take = -1, take_size = 0;
+    if (alloc) {
+      for (int h : m.node[v].hosted) {
+        int c = size_index(m, h);
+        if (gptr[c] < group[c].size()) { take = group[c][gptr[c]]; take_size = h; gptr[c]++; break; }
+      }
+    } else if (lptr[v] < (*lists)[v].size()) {
+      take = (*lists)[v][lptr[v]++];
+      take_size = (*size_used_in)[take];
+    }
+    if (take >= 0) {
+      if (!has_tasks[v]) {  // lines 8-11: give time for I's creation
+        i64 cs = std::max(reconfig_end, end[v]);
+        reconfig_end = cs + P.c.cr(m, v);
+        S.events.push_back({0, v, cs, P.c.cr(m, v)});
+        end[v] = reconfig_end;
+        has_tasks[v] = true;
+      }
+      // lines 12-15: longest unscheduled task T_j, executed right after in I
+      S.node[take] = v;
+      S.size_used[take] = take_size;
+      S.start[take] = end[v];
+      S.list[v].push_back(take);
+      end[v] += P.time(take, take_size);
+      S.makespan = std::max(S.makespan, end[v]);
+      unscheduled--;
+      heap.push({{end[v], m.node[v].lo}, v});  // line 16
+    } else if (unscheduled > 0) {             // line 17: repartitioning
+      if (has_tasks[v]) {                     // lines 18-20: give time to destroy I
+        i64 ds = std::max(reconfig_end, end[v]);
+        reconfig_end = ds + P.c.de(m, v);
+        S.events.push_back({1, v, ds, P.c.de(m, v)});
+      }
+      for (int ch : m.node[v].children) {  // lines 21-24
+        end[ch] = end[v];
+        has_tasks[ch] = false;
+        heap.push({{end[ch], m.node[ch].lo}, ch});
+      }
+      (void)vs;
+    }
+    // else: drop the instance (no tasks remain anywhere)
+  }
+  return S;
+}
+
+Sched schedule_allocation(const Problem& P, const std::vector<int>& alloc) {
+  return run_event_loop(P, &alloc, nullptr, nullptr);
+}
+
+Sched replay(const Problem& P, const Sched& S) {  // Alg. 2 line 26 (O7)
+  return run_event_loop(P, nullptr, &S.list, &S.size_used);
+}
+
+// ---------------------------------------------------------------------------
+// Phase 3: Alg. 2 "Schedule refinement", moves and
+// swaps with the readings Q14-Q19 of SURVEY.md §8c.
+// ---------------------------------------------------------------------------
+struct RefineStats { int moves = 0, swaps = 0, iterations = 0; i64 evals = 0; };
+
+void insert_ordered(const Problem& P, const Sched& S, std::vector<int>& lst, int j) {
+  // "Insert T in I^a.tasks ordered by T.time": decreasing time, ties -> index (Q18)
+  auto before = [&](int x, int y) {
+    if (dur(P, S, x) != dur(P, S, y)) return dur(P, S, x) > dur(P, S, y);
+    return x < y;
+  };
+  auto it = lst.begin();
+  while (it != lst.end() && before(*it, j)) ++it;
+  lst.insert(it, j);
+}
+
+RefineStats refine(const Problem& P, Sched& S, int max_iterations, int ppm) {
+  const Model& m = P.m;
+  const int N = (int)m.node.size();
+  RefineStats st;
+  // slice ends from the phase-2 times (Q14)
+  std::vector<i64> send(m.slices, 0);
+  for (int j = 0; j < P.n; ++j) {
+    const TreeNode& nd = m.node[S.node[j]];
+    for (int s = nd.lo; s < nd.hi; ++s) send[s] = std::max(send[s], S.start[j] + dur(P, S, j));
+  }
+  auto end_of = [&](int u) {  // end(I) = max_{s in I} s.end
+    i64 e = 0;
+    for (int s = m.node[u].lo; s < m.node[u].hi; ++s) e = std::max(e, send[s]);
+    return e;
+  };
+  auto add_on = [&](int u, i64 d) {
+    for (int s = m.node[u].lo; s < m.node[u].hi; ++s) send[s] += d;
+  };
+  i64 omega = *std::max_element(send.begin(), send.end());  // line 3
+  std::vector<int> leaf_of(m.slices, -1);
+  for (int v = 0; v < N; ++v)
+    if (m.node[v].children.empty()) leaf_of[m.node[v].lo] = v;
+
+  bool stop = false;
+  while (!stop && st.iterations < max_iterations) {  // line 4 (+ iteration cap, Q19)
+    st.iterations++;
+    const i64 omega_prev = omega;
+    // line 5: push the leaves whose slices reach omega (ascending slice order, Q15)
+    std::deque<int> Q;
+    std::vector<bool> opened(N, false);
+    for (int s = 0; s < m.slices; ++s)
+      if (send[s] == omega) { Q.push_back(leaf_of[s]); opened[leaf_of[s]] = true; }
+    while (!Q.empty()) {  // line 6
+      const int I = Q.front();  // line 7
+      Q.pop_front();
+      if (I == 0) { stop = true; break; }  // lines 8-10: root opened
+      // line 11: alternative I^a, same size, != I, minimum end (ties -> lower slice, Q16)
+      int A = -1;
+      i64 eA = 0;
+      for (int u = 0; u < N; ++u) {
+        if (u == I || m.node[u].size() != m.node[I].size()) continue;
+        i64 e = end_of(u);
+        if (A < 0 || e < eA || (e == eA && m.node[u].lo < m.node[A].lo)) { A = u; eA = e; }
+      }
+      bool done = false;
+      if (A >= 0) {
+        const i64 marg = omega - eA;  // omega - end(I^a)
+        // line 12: task T with T.time < marg closest to marg/2 -> argmin(|2t - marg|, index) (Q17)
+        st.evals += (i64)S.list[I].size();
+        int T = -1;
+        i64 bestd = 0;
+        for (int j : S.list[I]) {
+          i64 t = dur(P, S, j);
+          if (!(t < marg)) continue;
+          i64 d = std::llabs(2 * t - marg);
+          if (T < 0 || d < bestd || (d == bestd && j < T)) { T = j; bestd = d; }
+        }
+        if (T >= 0) {  // lines 13-16: move
+          const i64 t = dur(P, S, T);
+          S.list[I].erase(std::find(S.list[I].begin(), S.list[I].end(), T));
+          S.node[T] = A;
+          insert_ordered(P, S, S.list[A], T);
+          add_on(I, -t);
+          add_on(A, +t);
+          st.moves++;
+          done = true;
+        } else {  // lines 17-22: swap
+          st.evals += (i64)S.list[I].size() * (i64)S.list[A].size();
+          int K = -1, J = -1;
+          i64 bd = 0;
+          for (int k : S.list[I])
+            for (int j : S.list[A]) {
+              i64 delta = dur(P, S, k) - dur(P, S, j);
+              if (!(0 < delta && delta < marg)) continue;
+              i64 d = std::llabs(2 * delta - marg);
+              if (K < 0 || d < bd || (d == bd && (k < K || (k == K && j < J)))) { K = k; J = j; bd = d; }
+            }
+          if (K >= 0) {
+            const i64 delta = dur(P, S, K) - dur(P, S, J);
+            S.list[I].erase(std::find(S.list[I].begin(), S.list[I].end(), K));
+            S.list[A].erase(std::find(S.list[A].begin(), S.list[A].end(), J));
+            S.node[K] = A;
+            S.node[J] = I;
+            insert_ordered(P, S, S.list[A], K);
+            insert_ordered(P, S, S.list[I], J);
+            add_on(I, -delta);
+            add_on(A, +delta);
+            st.swaps++;
+            done = true;
+          }
+        }
+      }
+      if (!done) {  // lines 23-24: open the parent once
+        const int par = m.node[I].parent;
+        if (par >= 0 && !opened[par]) { opened[par] = true; Q.push_back(par); }
+      }
+    }
+    omega = *std::max_element(send.begin(), send.end());  // line 25
+    // optional minimum-improvement stop: integer ppm
+    if (ppm > 0 && (omega_prev - omega) * 1000000 < (i64)ppm * omega_prev) break;
+  }
+  return st;
+}
+
+void write_slots(const Sched& S, int n, orc_slot* slots) {
+  if (!slots) return;
+  for (int j = 0; j < n; ++j) slots[j] = {S.node[j], S.size_used[j], S.start[j]};
+}
+void write_events(const Sched& S, orc_event* ev, int32_t* nev) {
+  if (nev) *nev = (int32_t)S.events.size();
+  if (ev)
+    for (size_t k = 0; k < S.events.size(); ++k) ev[k] = S.events[k];
+}
+
+// Phase 3 + line-26 replay + keep-best guard (Q14), on schedule S whose phase-2
+// makespan is ms2.  Returns the final schedule.
+Sched refine_and_replay(const Problem& P, const Sched& S2, i64 ms2, int max_it, int ppm, uint32_t flags,
+                        orc_result* res) {
+  Sched S = S2;
+  RefineStats st = refine(P, S, max_it, ppm);
+  Sched R = replay(P, S);
+  res->moves = st.moves;
+  res->swaps = st.swaps;
+  res->evals = st.evals;
+  res->iterations = st.iterations;
+  res->reverted = 0;
+  if (!(flags & ORC_NO_GUARD) && R.makespan > ms2) {
+    res->reverted = 1;
+    return S2;
+  }
+  return R;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C interface
+// ===========================================================================
+extern "C" {
+
+int orc_num_sizes(int profile) { Model m = make_model(profile); return m.ok ? (int)m.sizes.size() : -2; }
+int orc_num_nodes(int profile) { Model m = make_model(profile); return m.ok ? (int)m.node.size() : -2; }
+int orc_num_slices(int profile) { Model m = make_model(profile); return m.ok ? m.slices : -2; }
+
+int orc_nodes(int profile, int32_t* lo, int32_t* hi, int32_t* parent) {
+  Model m = make_model(profile);
+  if (!m.ok) return -2;
+  for (size_t v = 0; v < m.node.size(); ++v) {
+    lo[v] = m.node[v].lo;
+    hi[v] = m.node[v].hi;
+    parent[v] = m.node[v].parent;
+  }
+  return (int)m.node.size();
+}
+
+// Valid partitions: every way of cutting the tree — a node is used
+// whole, or (A100/H100 {S0..S3}) as the 3-slice instance {S0,S1,S2} with S3
+// unusable, or split into its children.  Each partition is listed as the
+// instances (start, size) it creates.
+int orc_partitions(int profile, int32_t* out, int32_t* counts, int maxparts, int maxinst) {
+  Model m = make_model(profile);
+  if (!m.ok) return -2;
+  std::function<std::vector<std::vector<std::pair<int, int>>>(int)> cuts = [&](int v) {
+    std::vector<std::vector<std::pair<int, int>>> r;
+    const TreeNode& nd = m.node[v];
+    for (int h : nd.hosted) r.push_back({{nd.lo, h}});  // whole node (or 3-in-4)
+    if (!nd.children.empty()) {
+      std::vector<std::vector<std::pair<int, int>>> acc = {{}};
+      for (int ch : nd.children) {
+        std::vector<std::vector<std::pair<int, int>>> nxt;
+        for (auto& a : acc)
+          for (auto& b : cuts(ch)) {
+            auto x = a;
+            x.insert(x.end(), b.begin(), b.end());
+            nxt.push_back(x);
+          }
+        acc = nxt;
+      }
+      r.insert(r.end(), acc.begin(), acc.end());
+    }
+    return r;
+  };
+  auto all = cuts(0);
+  int k = 0;
+  for (auto& p : all) {
+    if (k < maxparts && (int)p.size() <= maxinst) {
+      counts[k] = (int32_t)p.size();
+      for (size_t q = 0; q < p.size(); ++q) {
+        out[(size_t)k * 2 * maxinst + 2 * q] = p[q].first;
+        out[(size_t)k * 2 * maxinst + 2 * q + 1] = p[q].second;
+      }
+    }
+    ++k;
+  }
+  return k;
+}
+
+int orc_family(int profile, const int32_t* times, int n, int32_t* out, int maxK) {
+  Problem P;
+  int rc = load_problem(profile, nullptr, times, n, true, P);
+  if (rc) return rc;
+  auto fam = allocation_family(P);
+  for (size_t k = 0; k < fam.size() && (int)k < maxK; ++k)
+    for (int i = 0; i < n; ++i) out[k * n + i] = fam[k][i];
+  return (int)fam.size();
+}
+
+int orc_schedule_allocation(int profile, const int32_t* costs, const int32_t* times, int n, const int32_t* alloc,
+                            orc_slot* slots, orc_event* ev, int32_t* nev, int64_t* makespan, int64_t* pops) {
+  Problem P;
+  int rc = load_problem(profile, costs, times, n, false, P);
+  if (rc) return rc;
+  std::vector<int> a(alloc, alloc + n);
+  for (int s : a)
+    if (size_index(P.m, s) < 0) return -1;
+  Sched S = schedule_allocation(P, a);
+  write_slots(S, n, slots);
+  write_events(S, ev, nev);
+  if (makespan) *makespan = S.makespan;
+  if (pops) *pops = S.pops;
+  return 0;
+}
+
+int orc_far(int profile, const int32_t* costs, const int32_t* times, int n, int32_t max_iterations,
+            int32_t ppm, uint32_t flags, orc_slot* slots, orc_result* res, orc_event* ev, int32_t* nev) {
+  Problem P;
+  int rc = load_problem(profile, costs, times, n, (flags & ORC_ZERO_RECONFIG) != 0, P);
+  if (rc) return rc;
+  orc_result r{};
+  // Phase 1 + phase 2 on every member; k* = argmin (makespan_k, k)  (Q13)
+  auto fam = allocation_family(P);
+  r.family_size = (int)fam.size();
+  Sched best;
+  int kbest = -1;
+  for (size_t k = 0; k < fam.size(); ++k) {
+    Sched S = schedule_allocation(P, fam[k]);
+    r.events += S.pops;
+    if (kbest < 0 || S.makespan < best.makespan) { best = S; kbest = (int)k; }
+  }
+  if (n == 0) best = Sched{}, best.list.assign(P.m.node.size(), {});
+  r.alloc_index = kbest < 0 ? 0 : kbest;
+  r.makespan_phase2 = best.makespan;
+  Sched fin = best;
+  if (!(flags & ORC_NO_REFINE) && n > 0) fin = refine_and_replay(P, best, best.makespan, max_iterations, ppm, flags, &r);
+  r.makespan = fin.makespan;
+  write_slots(fin, n, slots);
+  write_events(fin, ev, nev);
+  if (res) *res = r;
+  return 0;
+}
+
+int orc_refine(int profile, const int32_t* costs, const int32_t* times, int n, int32_t max_iterations, int32_t ppm,
+               uint32_t flags, orc_slot* slots, orc_result* res, orc_event* ev, int32_t* nev) {
+  Problem P;
+  int rc = load_problem(profile, costs, times, n, (flags & ORC_ZERO_RECONFIG) != 0, P);
+  if (rc) return rc;
+  if (!slots || !res) return -1;
+  const int N = (int)P.m.node.size();
+  // Rebuild the tree from the slots: node lists ordered by start time (then index).
+  Sched S;
+  S.list.assign(N, {});
+  S.node.resize(n);
+  S.size_used.resize(n);
+  S.start.resize(n);
+  std::vector<int> order(n);
+  for (int j = 0; j < n; ++j) {
+    if (slots[j].node < 0 || slots[j].node >= N) return -1;
+    bool hosted = false;
+    for (int h : P.m.node[slots[j].node].hosted) hosted |= (h == slots[j].size_used);
+    if (!hosted) return -1;
+    S.node[j] = slots[j].node;
+    S.size_used[j] = slots[j].size_used;
+    S.start[j] = slots[j].start;
+    order[j] = j;
+  }
+  std::sort(order.begin(), order.end(), [&](int x, int y) {
+    return S.start[x] != S.start[y] ? S.start[x] < S.start[y] : x < y;
+  });
+  for (int j : order) S.list[S.node[j]].push_back(j);
+  for (int j = 0; j < n; ++j) S.makespan = std::max(S.makespan, S.start[j] + dur(P, S, j));
+  const i64 ms2 = res->makespan_phase2;
+  orc_result r = *res;
+  Sched fin = S;
+  if (n > 0) fin = refine_and_replay(P, S, ms2, max_iterations, ppm, flags, &r);
+  r.makespan = fin.makespan;
+  write_slots(fin, n, slots);
+  write_events(fin, ev, nev);
+  *res = r;
+  return 0;
+}
+
+// Zero-reconfiguration optimum: each task picks a node hosting
+// some size; for a fixed choice, running ancestors before descendants is optimal
+// and the makespan is the max over slices of the summed loads of the nodes that
+// cover the slice (nodes covering one slice form a root-leaf chain).
+int64_t orc_bruteforce(int profile, const int32_t* times, int n) {
+  Problem P;
+  int rc = load_problem(profile, nullptr, times, n, true, P);
+  if (rc) return rc;
+  const Model& m = P.m;
+  std::vector<std::pair<int, int>> choice;  // (node, size)
+  for (size_t v = 0; v < m.node.size(); ++v)
+    for (int h : m.node[v].hosted) choice.push_back({(int)v, h});
+  std::vector<i64> slice_load(m.slices, 0);
+  i64 best = std::numeric_limits<i64>::max();
+  // order tasks by decreasing minimum time for better pruning
+  std::vector<int> ord(n);
+  for (int i = 0; i < n; ++i) ord[i] = i;
+  std::function<void(int)> rec = [&](int d) {
+    i64 cur = *std::max_element(slice_load.begin(), slice_load.end());
+    if (cur >= best) return;
+    if (d == n) { best = cur; return; }
+    const int i = ord[d];
+    for (auto& ch : choice) {
+      const TreeNode& nd = m.node[ch.first];
+      i64 t = P.time(i, ch.second);
+      for (int s = nd.lo; s < nd.hi; ++s) slice_load[s] += t;
+      rec(d + 1);
+      for (int s = nd.lo; s < nd.hi; ++s) slice_load[s] -= t;
+    }
+  };
+  if (n == 0) return 0;
+  rec(0);
+  return best;
+}
+
+// Constraints 1-3 of P:214-230 plus lifecycle consistency of the explicit
+// reconfiguration events.  Returns the number of violations.
+int orc_validate(int profile, const int32_t* costs, const int32_t* times, int n, const orc_slot* slots,
+                 const orc_event* ev, int32_t nev) {
+  Problem P;
+  int rc = load_problem(profile, costs, times, n, costs == nullptr, P);
+  if (rc) return 1000000 - rc;
+  const Model& m = P.m;
+  const int N = (int)m.node.size();
+  int bad = 0;
+  auto overlap = [&](int u, int v) { return m.node[u].lo < m.node[v].hi && m.node[v].lo < m.node[u].hi; };
+  std::vector<i64> b(n), f(n);
+  for (int j = 0; j < n; ++j) {
+    int v = slots[j].node;
+    if (v < 0 || v >= N) { bad++; continue; }
+    bool hosted = false;
+    for (int h : m.node[v].hosted) hosted |= (h == slots[j].size_used);
+    if (!hosted) { bad++; continue; }
+    b[j] = slots[j].start;
+    f[j] = b[j] + P.time(j, slots[j].size_used);
+    if (b[j] < 0) bad++;
+  }
+  if (bad) return bad;
+  // (1) tasks whose instances share a slice do not run at the same time
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j)
+      if (overlap(slots[i].node, slots[j].node) && b[i] < f[j] && b[j] < f[i]) bad++;
+  // (2) at every task start the running instances are pairwise disjoint tree nodes
+  //     (the tree's disjoint node sets are exactly the valid partitions' subsets)
+  for (int k = 0; k < n; ++k) {
+    std::vector<int> run;
+    for (int j = 0; j < n; ++j)
+      if (b[j] <= b[k] && b[k] < f[j]) run.push_back(slots[j].node);
+    for (size_t x = 0; x < run.size(); ++x)
+      for (size_t y = x + 1; y < run.size(); ++y)
+        if (run[x] != run[y] && overlap(run[x], run[y])) bad++;
+  }
+  // (3) sequential reconfiguration: events pairwise disjoint, correctly sized; every
+  //     node with tasks is created before its first task; lifecycles of nodes with
+  //     overlapping slices are disjoint (destroy before the next create).
+  std::vector<i64> first(N, std::numeric_limits<i64>::max()), last(N, std::numeric_limits<i64>::min());
+  std::vector<bool> used(N, false);
+  for (int j = 0; j < n; ++j) {
+    int v = slots[j].node;
+    used[v] = true;
+    first[v] = std::min(first[v], b[j]);
+    last[v] = std::max(last[v], f[j]);
+  }
+  std::vector<i64> cstart(N, 0), cend(N, 0), dstart(N, std::numeric_limits<i64>::max()),
+      dend(N, std::numeric_limits<i64>::max());
+  std::vector<int> ncreate(N, 0), ndestroy(N, 0);
+  for (int e = 0; e < nev; ++e) {
+    const orc_event& E = ev[e];
+    if (E.node < 0 || E.node >= N) { bad++; continue; }
+    i64 want = E.kind == 0 ? P.c.cr(m, E.node) : P.c.de(m, E.node);
+    if (E.dur != want || E.start < 0) bad++;
+    if (E.kind == 0) { ncreate[E.node]++; cstart[E.node] = E.start; cend[E.node] = E.start + E.dur; }
+    else { ndestroy[E.node]++; dstart[E.node] = E.start; dend[E.node] = E.start + E.dur; }
+    for (int g = e + 1; g < nev; ++g)
+      if (E.start < ev[g].start + ev[g].dur && ev[g].start < E.start + E.dur) bad++;
+  }
+  for (int v = 0; v < N; ++v) {
+    if (!used[v]) { if (ncreate[v] || ndestroy[v]) bad++; continue; }
+    if (ncreate[v] != 1 || ndestroy[v] > 1) { bad++; continue; }
+    if (cend[v] > first[v]) bad++;
+    if (ndestroy[v] && dstart[v] < last[v]) bad++;
+  }
+  for (int u = 0; u < N; ++u)
+    for (int v = u + 1; v < N; ++v) {
+      if (!used[u] || !used[v] || !overlap(u, v)) continue;
+      // lifecycle [cstart, dend) ; the earlier one must be destroyed before the later is created
+      bool u_first = cstart[u] < cstart[v];
+      int a = u_first ? u : v, c = u_first ? v : u;
+      if (ndestroy[a] == 0 || dend[a] > cstart[c]) bad++;
+    }
+  return bad;
+}
+
+int orc_lower_bound(int profile, const int32_t* times, int n, int64_t* sum_min_work, int64_t* max_min_time) {
+  Problem P;
+  int rc = load_problem(profile, nullptr, times, n, true, P);
+  if (rc) return rc;
+  i64 W = 0, H = 0;
+  for (int i = 0; i < n; ++i) {
+    i64 w = std::numeric_limits<i64>::max(), h = std::numeric_limits<i64>::max();
+    for (int s : P.m.sizes) {
+      w = std::min(w, (i64)s * P.time(i, s));
+      h = std::min(h, P.time(i, s));
+    }
+    W += w;
+    H = std::max(H, h);
+  }
+  *sum_min_work = W;
+  *max_min_time = H;
+  return 0;
+}
+
+int orc_far_many(int profile, const int32_t* costs, const int32_t* times, int64_t I, int n, int32_t max_iterations,
+                 int32_t ppm, uint32_t flags, int64_t* makespans, orc_result* res) {
+  const int nc = orc_num_sizes(profile);
+  if (nc < 0) return nc;
+  int worst = 0;
+  for (int64_t i = 0; i < I; ++i) {
+    orc_result r{};
+    int rc = orc_far(profile, costs, times + (size_t)i * n * nc, n, max_iterations, ppm, flags, nullptr, &r, nullptr,
+                     nullptr);
+    if (rc) { worst = rc; r.makespan = -1; }
+    if (makespans) makespans[i] = r.makespan;
+    if (res) res[i] = r;
+  }
+  return worst;
+}
+
+}  // extern "C"

@@ -1,0 +1,233 @@
+"""Oracle pins for phases 1-3: worked examples, the paper's bounds, brute force,
+feasibility (constraints 1-3) and invariants.  None of these re-types the
+oracle's own formulas; each checks something PAPER.md (or mathematics) fixes."""
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from paper_2507_13601_b200 import inputs
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_traces.json")))
+SLICES = {"A30": 4, "A100": 7, "H100": 7}
+
+
+def _t(x, profile):
+    return np.array(x, dtype=np.int32).reshape(-1, len(inputs.SIZES[profile]))
+
+
+# ----------------------------------------------------------------- worked examples
+@pytest.mark.parametrize("case", GOLD["schedule_allocation"], ids=lambda c: c["cite"][:24])
+def test_alg1_traces(O, case):
+    r = O.schedule_allocation(case["profile"], case["costs"], _t(case["times"], case["profile"]), case["alloc"])
+    assert r["makespan"] == case["makespan"]
+    assert r["slots"]["start"].tolist() == case["starts"]
+    if "events" in case:
+        assert [list(map(int, e)) for e in r["events"]] == case["events"]
+
+
+@pytest.mark.parametrize("case", GOLD["family"], ids=lambda c: c["cite"][:12])
+def test_family_examples(O, case):
+    fam = O.family(case["profile"], _t(case["times"], case["profile"]))
+    assert fam.tolist() == case["family"]
+
+
+def test_far_example(O):
+    case = GOLD["far"][0]
+    t = _t(case["times"], case["profile"])
+    fam = O.family(case["profile"], t)
+    ms = [O.schedule_allocation(case["profile"], None, t, a)["makespan"] for a in fam]
+    assert ms == case["member_makespans"]
+    r = O.far(case["profile"], None, t)["result"]
+    assert r["makespan"] == case["makespan"] and r["alloc_index"] == case["alloc_index"]
+    assert O.bruteforce(case["profile"], t) == case["optimum"]
+
+
+@pytest.mark.parametrize("case", GOLD["refine"], ids=["move", "swap"])
+def test_refine_examples(O, case):
+    t = _t(case["times"], case["profile"])
+    p2 = O.schedule_allocation(case["profile"], None, t, case["alloc"])
+    assert p2["makespan"] == case["phase2_makespan"]
+    r = O.refine(case["profile"], None, t, p2["slots"], p2["makespan"])
+    res = r["result"]
+    assert (res["makespan"], res["moves"], res["swaps"]) == (case["makespan"], case["moves"], case["swaps"])
+    assert r["slots"]["node"].tolist() == case["nodes"]
+    # Fig. 6: > 1.5x ; Fig. 7: almost 1.25x
+    ratio = Fraction(case["phase2_makespan"], case["makespan"])
+    assert ratio >= Fraction(3, 2) if case["moves"] else Fraction(6, 5) <= ratio < Fraction(5, 4)
+    assert O.validate(case["profile"], None, t, r["slots"], r["events"]) == 0
+
+
+def test_empty_and_single(O):
+    for profile in ("A30", "A100"):
+        nc = len(inputs.SIZES[profile])
+        r = O.far(profile, inputs.reconfig_costs(profile), np.zeros((0, nc), np.int32))
+        assert r["result"]["makespan"] == 0 and r["result"]["family_size"] == 0
+        # single task, zero reconfiguration, property 1: FAR = t(max size) = min_s t(s)
+        for t in inputs.synthetic(profile, 1, 50, 11):
+            r = O.far(profile, None, t)["result"]
+            assert r["makespan"] == t.min() == t[0, -1]
+
+
+# ----------------------------------------------------------------- phase 1 invariants
+@pytest.mark.parametrize("profile", ["A30", "A100"])
+def test_family_invariants(O, profile):
+    sizes = inputs.SIZES[profile]
+    tabs = [inputs.synthetic(profile, 12, 40, 1), inputs.uniform_random(profile, 12, 40, 2),
+            inputs.small_ties(profile, 12, 40, 3)]
+    for tab in tabs:
+        for t in tab:
+            fam = O.family(profile, t)
+            n = t.shape[0]
+            assert 1 <= len(fam) <= 1 + n * (len(sizes) - 1)
+            col = {s: j for j, s in enumerate(sizes)}
+            a1 = fam[0]
+            for i in range(n):  # P:341 argmin work, smallest s on ties
+                w = [s * int(t[i, col[s]]) for s in sizes]
+                assert a1[i] == sizes[int(np.argmin(w))]
+            for k in range(len(fam) - 1):
+                d = np.nonzero(fam[k + 1] != fam[k])[0]
+                assert len(d) == 1
+                j = d[0]
+                cur = np.array([t[i, col[fam[k][i]]] for i in range(n)])
+                assert cur[j] == cur.max() and j == int(np.argmax(cur))
+                assert fam[k + 1][j] > fam[k][j]
+            last = fam[-1]
+            cur = np.array([t[i, col[last[i]]] for i in range(n)])
+            assert last[int(np.argmax(cur))] == sizes[-1]
+
+
+def test_work_monotone_gives_all_ones(O):
+    # if s*t(s) is non-decreasing for every task, a^1 = 1 slice everywhere
+    t = np.array([[10, 6, 4], [7, 5, 2], [3, 3, 3]], np.int32)
+    assert O.family("A30", t)[0].tolist() == [1, 1, 1]
+
+
+# ----------------------------------------------------------------- §5 bounds (zero reconfiguration)
+def _w_h(t, alloc, sizes):
+    col = {s: j for j, s in enumerate(sizes)}
+    W = sum(int(a) * int(t[i, col[int(a)]]) for i, a in enumerate(alloc))
+    H = max(int(t[i, col[int(a)]]) for i, a in enumerate(alloc))
+    return W, H
+
+
+@pytest.mark.parametrize("profile", ["A30", "A100"])
+def test_per_allocation_bounds(O, profile):
+    """P:847 (A30): w <= W/4 + 3h/4.  P:898 (A100): w <= max(W/6+5h/6, W/4, W/5+3h/5).
+    Checked on every family member and on random allocations, exact integer arithmetic."""
+    sizes = inputs.SIZES[profile]
+    rng = np.random.default_rng(5)
+    tabs = [inputs.synthetic(profile, n, 60, 20 + n) for n in (3, 8, 17)] + \
+           [inputs.uniform_random(profile, n, 60, 30 + n) for n in (4, 9)]
+    checked = 0
+    for tab in tabs:
+        for t in tab:
+            allocs = list(O.family(profile, t)) + [rng.choice(sizes, t.shape[0]) for _ in range(3)]
+            for a in allocs:
+                w = O.schedule_allocation(profile, None, t, a)["makespan"]
+                W, H = _w_h(t, a, sizes)
+                if profile == "A30":
+                    assert 4 * w <= W + 3 * H
+                else:
+                    assert 60 * w <= max(10 * W + 50 * H, 15 * W, 12 * W + 36 * H)
+                checked += 1
+    assert checked > 1000
+
+
+@pytest.mark.parametrize("profile,factor", [("A30", Fraction(7, 4)), ("A100", Fraction(2))])
+def test_approximation_factor_vs_bruteforce(O, profile, factor):
+    """Theorem 1 + §5: with zero reconfiguration and property 1,
+    w_FAR <= 7/4 w* (A30), <= 2 w* (A100).  Also LB <= w* <= w_FAR."""
+    ns = (2, 3, 4, 5, 6) if profile == "A30" else (2, 3, 4, 5)
+    for n in ns:
+        for t in inputs.synthetic(profile, n, 40, 100 + n):
+            w_far = O.far(profile, None, t)["result"]["makespan"]
+            w_opt = O.bruteforce(profile, t)
+            W, H = O.lower_bound(profile, t)
+            assert W <= SLICES[profile] * w_opt and H <= w_opt <= w_far
+            assert w_far <= factor * w_opt
+
+
+def test_bruteforce_closed_forms(O):
+    # identical 1-slice-only tasks (flat times): w* = ceil(n / slices) * t
+    for profile in ("A30", "A100"):
+        nc = len(inputs.SIZES[profile])
+        for n in range(1, 6):
+            t = np.full((n, nc), 9, np.int32)
+            assert O.bruteforce(profile, t) == -(-n // SLICES[profile]) * 9
+    # one task: min over sizes
+    t = np.array([[8, 5, 7]], np.int32)
+    assert O.bruteforce("A30", t) == 5
+
+
+# ----------------------------------------------------------------- feasibility and guards
+@pytest.mark.parametrize("profile", ["A30", "A100", "H100"])
+def test_far_feasible_and_bounded(O, profile):
+    costs = inputs.reconfig_costs(profile)
+    tabs = [inputs.synthetic(profile, n, 25, 40 + n) for n in (1, 5, 10, 23)] + \
+           [inputs.uniform_random(profile, 11, 25, 9), inputs.small_ties(profile, 9, 25, 8)]
+    if profile != "A30":
+        tabs.append(inputs.rodinia_like(25, 1))
+    for tab in tabs:
+        for t in tab:
+            r = O.far(profile, costs, t)
+            res = r["result"]
+            assert O.validate(profile, costs, t, r["slots"], r["events"]) == 0
+            assert res["makespan"] <= res["makespan_phase2"]          # guard: refinement never worse
+            W, H = O.lower_bound(profile, t)
+            assert SLICES[profile] * res["makespan"] >= W and res["makespan"] >= H
+            nr = O.far(profile, costs, t, flags=O.NO_REFINE)
+            assert O.validate(profile, costs, t, nr["slots"], nr["events"]) == 0
+            assert nr["result"]["makespan"] == res["makespan_phase2"]
+            z = O.far(profile, costs, t, max_iterations=0)
+            assert (z["slots"] == nr["slots"]).all() and z["result"]["makespan"] == res["makespan_phase2"]
+            assert r["slots"]["start"].tolist() == O.far(profile, costs, t)["slots"]["start"].tolist()
+
+
+def test_refine_fixpoint_and_balanced(O):
+    # replay of the phase-2 tree reproduces phase 2 exactly (O7 fixpoint): refine with 0 iterations
+    for t in inputs.synthetic("A100", 14, 30, 77):
+        costs = inputs.reconfig_costs("A100")
+        p2 = O.far("A100", costs, t, flags=O.NO_REFINE)
+        r = O.refine("A100", costs, t, p2["slots"], p2["result"]["makespan"], max_iterations=0)
+        assert (r["slots"] == p2["slots"]).all()
+    # balanced schedule (all slice ends equal) -> 0 moves, 0 swaps
+    t = np.full((4, 3), 5, np.int32)
+    r = O.far("A30", None, t)["result"]
+    assert r["makespan"] == 5 and r["moves"] == 0 and r["swaps"] == 0
+
+
+def test_validator_rejects(O):
+    """Negative pins for the validator."""
+    t = np.array([[2, 2, 2], [2, 2, 2]], np.int32)
+    slot = np.zeros(2, O.SLOT_DT)
+    ev_dt = [("kind", "<i4"), ("node", "<i4"), ("start", "<i8"), ("dur", "<i8")]
+    # two tasks on S0 at [0,2) and [1,3) -> constraint 1
+    slot["node"] = [3, 3]; slot["size_used"] = [1, 1]; slot["start"] = [0, 1]
+    ev = np.array([(0, 3, 0, 0)], ev_dt)
+    assert O.validate("A30", None, t, slot, ev) > 0
+    # node 1 ({S0,S1}) and leaf 4 (S1) concurrently -> constraints 1/2
+    slot["node"] = [1, 4]; slot["size_used"] = [2, 1]; slot["start"] = [0, 1]
+    ev = np.array([(0, 1, 0, 0), (0, 4, 0, 0)], ev_dt)
+    assert O.validate("A30", None, t, slot, ev) > 0
+    # missing destroy of node 1 before leaf 3 is created -> constraint 3 / lifecycle
+    costs = np.array([[1, 1, 1], [1, 1, 1]], np.int32)
+    slot["node"] = [1, 3]; slot["size_used"] = [2, 1]; slot["start"] = [1, 5]
+    ev = np.array([(0, 1, 0, 1), (0, 3, 3, 1)], ev_dt)
+    assert O.validate("A30", costs, t, slot, ev) > 0
+    ev = np.array([(0, 1, 0, 1), (1, 1, 3, 1), (0, 3, 4, 1)], ev_dt)
+    assert O.validate("A30", costs, t, slot, ev) == 0
+    # overlapping reconfiguration events -> constraint 3
+    ev = np.array([(0, 1, 0, 1), (1, 1, 3, 1), (0, 3, 3, 1)], ev_dt)
+    assert O.validate("A30", costs, t, slot, ev) > 0
+
+
+def test_input_errors(O):
+    with pytest.raises(O.OracleError):
+        O.far("A30", None, np.array([[1, 0, 1]], np.int32))        # t < 1
+    with pytest.raises(O.OracleError):
+        O.far("A30", None, np.full((3, 3), 1 << 29, np.int32))     # makespan bound
+    with pytest.raises(O.OracleError):
+        O.far(7, None, np.ones((1, 3), np.int32))                  # unknown profile
