@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""Benchmark: batched FAR (phases 1-3 + replay) on B200 — FAR-scheduled instances/s and
+move/swap evals/s.  See DESIGN.md "Measurement".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+Workload (BASELINE.json configs[4]): A100/H100 7-slice tree,
+n = 128 tasks per instance, §6.3 MixedScaling / WideTimes generator, Table 2 A100
+reconfiguration costs, seed 5.  1M instances PER RANK (weak scaling: rank r solves the
+instances [r*1M, (r+1)*1M) of the counter-based table).  A step = far_solve_many over
+the rank's resident table (every phase of the hot path, schedules + reports written),
+plus at N>1 the NCCL allgather of the per-instance makespans (H9).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2507_13601_b200 import inputs  # noqa: E402
+
+METRIC = "FAR-scheduled instances/sec and move/swap evals/sec at 1/2/4/8 B200"
+WORKLOAD = inputs.WORKLOADS["M5"]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--instances", type=int, default=WORKLOAD.count, help="instances per rank")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--baseline-seconds", type=float, default=12.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-baseline", action="store_true")
+    ap.add_argument("--profile-run", action="store_true", help="short run for ncu (no clocks/e2e/baseline)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.p = None
+        self.out = []
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.out.append(line.strip())
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def oracle_baseline(seconds, rank_table=None):
+    """The CPU oracle, as it stands, single thread, on the first instances of the workload."""
+    from oracle import oracle as O
+    O.build()
+    costs = WORKLOAD.costs()
+    done, evals, t0 = 0, 0, time.perf_counter()
+    chunk = 200
+    while time.perf_counter() - t0 < seconds:
+        tab = WORKLOAD.table(count=chunk, start=done)
+        _, res = O.far_many(WORKLOAD.profile, costs, tab)
+        done += chunk
+        evals += int(res["evals"].sum())
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "instances/s", "cores": 1, "kind": "oracle",
+            "evals_per_s": evals / dt,
+            "sample": f"first {done} instances of {WORKLOAD.name} (A100, n=128, seed 5), single-threaded C++ oracle"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    O.build()
+    cores = os.cpu_count() or 1
+    costs = WORKLOAD.costs()
+    per_step = max(200, 100 * cores)
+    tab_all = WORKLOAD.table(count=per_step * (args.warmup + args.steps))
+    times = []
+    evals = 0
+    for s in range(args.warmup + args.steps):
+        tab = tab_all[s * per_step:(s + 1) * per_step]
+        t0 = time.perf_counter()
+        _, res = O.far_many_parallel(WORKLOAD.profile, costs, tab, workers=cores)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            evals += int(res["evals"].sum())
+    tot = sum(times)
+    v = per_step * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "instances/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD.name, "profile": "A100", "n_tasks": WORKLOAD.n,
+                       "instances_per_step": per_step, "generator": "PAPER.md §6.3 MixedScaling/WideTimes seed 5"},
+            "evals_per_s": evals / tot,
+            "cpu_baseline": {"value": v, "unit": "instances/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{per_step} instances per step of {WORKLOAD.name}, C++ oracle in a "
+                                       f"{cores}-process pool"},
+            "e2e": {"value": v, "unit": "instances/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_13601_b200 import far
+
+    assert torch.cuda.is_available(), "bench.py needs a GPU (no CPU fallback)"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    I = args.instances
+    nc = len(inputs.SIZES[WORKLOAD.profile])
+    # rank's shard of the counter-based table (weak scaling)
+    host = inputs.synthetic_parallel(WORKLOAD.profile, WORKLOAD.n, I, WORKLOAD.seed, scaling=WORKLOAD.scaling,
+                                     times=WORKLOAD.times, start=rank * I)
+    pinned = torch.from_numpy(host).pin_memory()
+    d_times = pinned.to(dev, non_blocking=False)
+    F = far.Far(WORKLOAD.profile, WORKLOAD.costs())
+    stream = torch.cuda.current_stream(dev)
+    ms = torch.empty(I, dtype=torch.int32, device=dev)
+    sd = torch.empty((I, WORKLOAD.n, 8), dtype=torch.uint8, device=dev)
+    rs = torch.empty((I, 56), dtype=torch.uint8, device=dev)
+    gathered = torch.empty(I * world, dtype=torch.int32, device=dev) if world > 1 else None
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        F.solve_many(d_times, out=(ms, sd, rs), stream=stream)
+        if ev is not None:
+            ev[1].record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, ms)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    F.sync()
+
+    clk = Clocks(local)
+    if not args.profile_run:
+        clk.start()
+        time.sleep(0.5)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start.record(stream)
+    for s in range(args.steps):
+        step(kev[s])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop() if not args.profile_run else None
+    total_ms = t_start.elapsed_time(t_end)
+    kern_ms = [a.elapsed_time(b) for a, b in kev]
+    F.sync()
+
+    res = far.results_np(rs)
+    evals_step = int(res["evals"].sum())
+    events_step = int(res["events"].sum())
+    moves_swaps = int(res["moves"].sum() + res["swaps"].sum())
+
+    # max over ranks
+    t = torch.tensor([total_ms, sum(kern_ms), float(evals_step), float(events_step)], dtype=torch.float64,
+                     device=dev)
+    if world > 1:
+        mx = t.clone()
+        dist.all_reduce(mx[:2], op=dist.ReduceOp.MAX)
+        sm_ = t.clone()
+        dist.all_reduce(sm_[2:], op=dist.ReduceOp.SUM)
+        total_ms, kern_total = float(mx[0]), float(mx[1])
+        evals_all, events_all = float(sm_[2]), float(sm_[3])
+    else:
+        kern_total = sum(kern_ms)
+        evals_all, events_all = float(evals_step), float(events_step)
+    ms_per_step = total_ms / args.steps
+    inst_all = I * world
+    value = inst_all / (ms_per_step / 1000.0)
+
+    # e2e through the public host API (pinned host buffers, H2D + D2H inside)
+    e2e = None
+    if not args.no_e2e and not args.profile_run:
+        hms = torch.empty(I, dtype=torch.int32).pin_memory().numpy()
+        hsd = torch.empty((I, WORKLOAD.n, 8), dtype=torch.uint8).pin_memory().numpy().view(far.SLOT_DT)[..., 0]
+        hrs = torch.empty((I, 56), dtype=torch.uint8).pin_memory().numpy().view(far.RESULT_DT)[..., 0]
+        hin = pinned.numpy()
+        F.solve_many_host(hin, out=(hms, hsd, hrs))  # warm
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            F.solve_many_host(hin, out=(hms, hsd, hrs))
+        dt = (time.perf_counter() - t0) / args.e2e_steps
+        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt[0])
+        ok = bool((hms == ms.cpu().numpy()).all())
+        e2e = {"value": inst_all / dt, "unit": "instances/s", "h2d_bytes_per_step": int(host.nbytes) * world,
+               "d2h_bytes_per_step": int(I * (4 + WORKLOAD.n * 8 + 56)) * world, "matches_device_run": ok,
+               "api": "far_solve_many_host (C-ABI, 2-stream chunk pipeline)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    pk, pk_src = peaks()
+    sm_max = float(pk.get("sm_max_mhz", 1965.0))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_ops = nsm * 4 * 32 * sm_max * 1e6  # int32 lane-ops/s: 1 warp-instr/clk/SMSP issue limit
+    # algorithmic integer ops per launch: Alg. 1 events x OPS_EVENT +
+    # phase-3 candidate evaluations x OPS_EVAL + phase 1 argmax/work ops
+    S, NCs = 7, nc
+    OPS_EVENT, OPS_EVAL = (S - 1) + 4, 3
+    fam = res["family_size"].astype(np.int64)
+    ops_p1 = int((2 * WORKLOAD.n * NCs + (fam - 1) * (WORKLOAD.n + NCs)).sum())
+    ops = events_step * OPS_EVENT + evals_step * OPS_EVAL + ops_p1
+    kern_avg_s = kern_total / args.steps / 1000.0
+    achieved = ops / kern_avg_s
+    roof = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
+            "frac": achieved / peak_ops, "traffic": None,
+            "peak_source": f"{nsm} SMs x 4 SMSP x 32 lanes x {sm_max:.0f} MHz (sm_max_mhz {pk_src})",
+            "kernel_ms": kern_avg_s * 1000.0,
+            "hbm_bytes_algorithmic": int(host.nbytes + I * (4 + WORKLOAD.n * 8 + 56)),
+            "hbm_gbs_achieved": (host.nbytes + I * (4 + WORKLOAD.n * 8 + 56)) / kern_avg_s / 1e9,
+            "hbm_gbs_peak": pk.get("hbm_gbs")}
+    line = {"metric": METRIC, "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": WORKLOAD.name, "profile": "A100 (7-slice tree, Table 2 A100 costs)",
+                       "n_tasks": WORKLOAD.n, "instances_per_rank": I, "global_instances": inst_all,
+                       "generator": "PAPER.md §6.3 MixedScaling/WideTimes, seed 5",
+                       "l2": "inputs (2.56 GB/rank) larger than the 126 MB L2; no flush",
+                       "parallelism": f"dp{world} (instances sharded, NCCL allgather of makespans)"},
+            "evals_per_s": evals_all / (ms_per_step / 1000.0),
+            "events_per_s": events_all / (ms_per_step / 1000.0),
+            "moves_swaps_per_step": moves_swaps,
+            "gpu_launches": args.steps * 1,
+            "roofline": roof, "clocks": clocks, "e2e": e2e}
+    if not args.no_baseline and not args.profile_run:
+        line["cpu_baseline"] = oracle_baseline(args.baseline_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,165 @@
+/* far.h — C-ABI of the B200-native batched FAR solver (arXiv 2507.13601).
+ *
+ * FAR = "Family of Allocations and Repartitioning", the three-phase moldable
+ * scheduler of PAPER.md §3 (citations "P:<line>" refer to PAPER.md):
+ *   phase 1  Turek family of allocations
+ *   phase 2  Alg. 1, LPT + list scheduling over the MIG
+ *            repartitioning tree with sequential reconfiguration P:374-463
+ *   phase 3  Alg. 2, critical-task moves and swaps, then the
+ *            line-26 replay of start/reconfiguration times
+ * plus the multi-batch concatenation of §4.
+ *
+ * Every entry point runs on the GPU (sm_100a kernels in libfar.so).  There is
+ * no CPU fallback: without a CUDA device every compute call returns FAR_E_CUDA.
+ *
+ * Units and layout
+ *   - All times are int32 "ticks" chosen by the caller (1 tick = 1 ms in the
+ *     bundled Table 2 costs).  Runtimes t_i(s) must be >= 1 (t_i maps to
+ *     R+); they need NOT be monotone in s.
+ *   - A runtime table is int32 [n][nsizes] per instance (C-contiguous), sizes in
+ *     the profile's order: A30 {1,2,4}; A100/H100 {1,2,3,4,7}.  Many
+ *     instances: [I][n][nsizes].
+ *   - Integer range: per instance, sum_i max_s t_i(s) + sum over tree nodes of
+ *     (t_create + t_destroy) must be < 2^30, so every makespan, start and the
+ *     |2x - m| comparisons of Alg. 2 fit in int32.  Violations: FAR_E_BAD_TIME.
+ *   - Tree node ids (far_task_slot.node) index the fixed repartitioning trees of
+ *     Fig. 3: A30 0=[0,4) 1=[0,2) 2=[2,4) 3..6 = leaves S0..S3;
+ *     A100/H100 0=[0,7) 1=[0,4) (hosts sizes 4 then 3) 2=[4,7) 3=[0,2) 4=[2,4)
+ *     5=[4,6) 6=[6,7) 7..12 = leaves S0..S5.
+ *
+ * Ownership: the caller owns every buffer passed in; the library never frees
+ * caller memory.  The library owns the far_ctx (constant tables, a lazily grown
+ * device workspace and private streams), released by far_destroy.
+ * Threading: one far_ctx per host thread; concurrent calls on one ctx are not
+ * allowed.
+ * Errors: every call returns far_status; far_last_error(ctx) gives a message.
+ * Argument errors are reported synchronously.  Asynchronous calls
+ * (far_solve_many, far_concat_streams) report per-instance input errors in
+ * far_result.status (makespan = -1) and raise a sticky device flag that the next
+ * far_sync() returns as FAR_E_BAD_TIME; CUDA faults surface as FAR_E_CUDA.
+ */
+#ifndef FAR_H
+#define FAR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct far_ctx far_ctx; /* opaque; owned by the library */
+
+typedef enum { FAR_A30 = 0, FAR_A100 = 1, FAR_H100 = 2 } far_profile;
+
+typedef enum {
+  FAR_OK = 0,
+  FAR_E_INVALID_ARG = 1,
+  FAR_E_UNSUPPORTED_PROFILE = 2,
+  FAR_E_BAD_TIME = 3,
+  FAR_E_TOO_LARGE = 4,
+  FAR_E_CUDA = 5,
+  FAR_E_OOM = 6
+} far_status;
+
+/* far_opts.flags */
+enum {
+  FAR_NO_REFINE = 1u,     /* skip phase 3 (Alg. 2) and its replay */
+  FAR_NO_GUARD = 2u,      /* return the replayed refined schedule even if worse than phase 2 */
+  FAR_ZERO_RECONFIG = 4u, /* ignore the ctx's create/destroy costs (all zero) */
+  FAR_NO_SCHEDULE = 8u    /* solve_many: do not write per-task slots (makespans/results only) */
+};
+
+typedef struct {
+  int32_t max_iterations;      /* Alg. 2 iteration cap; default 100 */
+  int32_t min_improvement_ppm; /* 0 = off; else stop when 1e6*(w_prev - w) < ppm*w_prev */
+  uint32_t flags;
+} far_opts;
+
+/* Per-instance report: 56 bytes. */
+typedef struct {
+  int32_t makespan;        /* final makespan (ticks); -1 on error */
+  int32_t makespan_phase2; /* min over the family of Alg. 1 makespans (phase 2 result) */
+  int32_t alloc_index;     /* k* : the winning family member (0-based) */
+  int32_t family_size;     /* K : number of allocations in the family */
+  int32_t moves, swaps;    /* phase 3 operations performed (Table 6 columns) */
+  int32_t iterations;      /* phase 3 outer iterations executed */
+  int32_t reverted;        /* 1 if the keep-best guard returned the phase-2 schedule */
+  int32_t status;          /* far_status for this instance */
+  int32_t reserved;
+  int64_t evals;           /* phase 3 move/swap candidate evaluations */
+  int64_t events;          /* Alg. 1 heap pops summed over all family members */
+} far_result;
+
+/* Per-task placement: 8 bytes.  start in ticks from the batch start. */
+typedef struct {
+  uint8_t node;      /* tree node id (see above) */
+  uint8_t size_used; /* slices the task runs with: the node size, or 3 on the A100 4-slice node */
+  uint8_t pad[2];
+  int32_t start;
+} far_task_slot;
+
+/* Create a context for a MIG profile.
+ * reconfig_cost: NULL -> Table 2 in 1 ms ticks; else int32[2][nsizes] =
+ * {create[], destroy[]} in the profile's size order, each >= 0 (all zero = no
+ * reconfiguration cost).  Unknown profile -> FAR_E_UNSUPPORTED_PROFILE. */
+far_status far_create(far_profile profile, const int32_t *reconfig_cost, far_ctx **out);
+void far_destroy(far_ctx *ctx);
+int32_t far_num_sizes(const far_ctx *ctx);
+const int32_t *far_sizes(const far_ctx *ctx);          /* nsizes values, host memory owned by ctx */
+int32_t far_num_nodes(const far_ctx *ctx);
+int32_t far_num_slices(const far_ctx *ctx);
+/* Tree node table (host): lo[v], hi[v] slice interval [lo,hi), parent[v] (-1 for the root). */
+far_status far_node_table(const far_ctx *ctx, int32_t *lo, int32_t *hi, int32_t *parent);
+const char *far_last_error(const far_ctx *ctx);
+/* Wait for all work queued by this ctx; returns FAR_E_BAD_TIME if any instance failed
+ * its input checks since the last far_sync, FAR_E_CUDA on a device fault. */
+far_status far_sync(far_ctx *ctx);
+
+/* Phases 1-2 on ONE batch (host memory, synchronous): the family, Alg. 1 on
+ * every member, k* = argmin (makespan, k).  sched[n] receives the
+ * phase-2 schedule, res its report (moves = swaps = 0).  n in [0, 1024]. */
+far_status far_schedule_batch(far_ctx *ctx, const int32_t *times, int32_t n, const far_opts *opts,
+                              far_task_slot *sched, far_result *res);
+
+/* Phase 3 (Alg. 2) + line-26 replay + keep-best guard on a given schedule
+ * (host memory, synchronous).  sched[n] in/out: node lists are rebuilt from it ordered
+ * by (start, task).  res in/out: on input res->makespan_phase2 is the guard reference
+ * (if <= 0 the input schedule's own makespan is used). */
+far_status far_local_search(far_ctx *ctx, const int32_t *times, int32_t n, const far_opts *opts,
+                            far_task_slot *sched, far_result *res);
+
+/* Phases 1-3 on I independent instances, DEVICE pointers, asynchronous on cuda_stream
+ * (a cudaStream_t; NULL = legacy default stream).
+ *   d_times    int32 [I][n][nsizes]
+ *   d_makespan int32 [I]            (required)
+ *   d_sched    far_task_slot [I][n] (or NULL, or ignored with FAR_NO_SCHEDULE)
+ *   d_res      far_result [I]       (or NULL)
+ * The buffers must stay valid until the stream reaches the call. */
+far_status far_solve_many(far_ctx *ctx, const int32_t *d_times, int64_t I, int32_t n, const far_opts *opts,
+                          int32_t *d_makespan, far_task_slot *d_sched, far_result *d_res, void *cuda_stream);
+
+/* Same as far_solve_many on HOST buffers (synchronous).  The library pipelines chunks of
+ * instances through its device workspace on two streams (H2D copy, solve, D2H copy
+ * overlapped); host buffers may be pageable or pinned (pinned is faster).
+ * This is the end-to-end public API the benchmark's "e2e" number measures. */
+far_status far_solve_many_host(far_ctx *ctx, const int32_t *h_times, int64_t I, int32_t n, const far_opts *opts,
+                               int32_t *h_makespan, far_task_slot *h_sched, far_result *h_res);
+
+/* Multi-batch concatenation (§4) of S independent streams of B batches each,
+ * DEVICE pointers, asynchronous.  Each batch is FAR-scheduled (phases 1-3), odd batches
+ * are reversed, and the batches are folded left to right with the seam offset
+ * rule and seam move/swap of DESIGN.md "Streams".
+ *   d_times           int32 [S][B][n][nsizes]
+ *   d_stream_makespan int64 [S]     total makespan of each stream
+ *   d_offsets         int64 [S][B]  absolute start offset of each batch
+ *   d_batch_res       far_result [S][B] (or NULL): the per-batch FAR reports
+ *   d_seam            int32 [S][B][4] (or NULL): per batch {trivial offset delta, seam moves,
+ *                     seam swaps, reversed flag} */
+far_status far_concat_streams(far_ctx *ctx, const int32_t *d_times, int64_t S, int32_t B, int32_t n,
+                              const far_opts *opts, int64_t *d_stream_makespan, int64_t *d_offsets,
+                              far_result *d_batch_res, int32_t *d_seam, void *cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FAR_H */

@@ -1,0 +1,357 @@
+// far_capi.cu — C-ABI of libfar.so (include/far.h): context, argument checks, launches,
+// host-memory paths (staging + a 2-stream chunk pipeline).  No compute happens here;
+// every step of FAR runs in far_kernel.cuh / far_stream.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "far_kernel.cuh"
+#include "far_stream.cuh"
+
+using namespace farb;
+
+namespace {
+constexpr int RING = 256;
+constexpr int SMEM_MAX = 227 * 1024;
+}  // namespace
+
+struct far_ctx {
+  int profile = 0, nc = 0, ns = 0, nn = 0;
+  int32_t sizes[8] = {0};
+  int cr[8] = {0}, de[8] = {0};
+  std::string err;
+  int device = -1, sms = 0;
+  unsigned long long* d_counter = nullptr;  // RING launch counters
+  int launch_id = 0;
+  int* d_errflag = nullptr;
+  // staging for host-memory calls
+  char* d_buf = nullptr;
+  size_t d_buf_bytes = 0;
+  cudaStream_t s[2] = {nullptr, nullptr};
+  bool inited = false;
+};
+
+static far_status fail(far_ctx* c, far_status st, const std::string& m) {
+  if (c) c->err = m;
+  return st;
+}
+
+static far_status cuda_fail(far_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, FAR_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                              \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);  \
+  } while (0)
+
+static far_status ensure_device(far_ctx* ctx) {
+  if (ctx->inited) return FAR_OK;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(ctx, FAR_E_CUDA, "no CUDA device: libfar has no CPU fallback");
+  CK(cudaGetDevice(&ctx->device));
+  CK(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  CK(cudaMalloc(&ctx->d_counter, RING * sizeof(unsigned long long)));
+  CK(cudaMemset(ctx->d_counter, 0, RING * sizeof(unsigned long long)));
+  CK(cudaMalloc(&ctx->d_errflag, sizeof(int)));
+  CK(cudaMemset(ctx->d_errflag, 0, sizeof(int)));
+  CK(cudaStreamCreateWithFlags(&ctx->s[0], cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&ctx->s[1], cudaStreamNonBlocking));
+  ctx->inited = true;
+  return FAR_OK;
+}
+
+static far_status ensure_buf(far_ctx* ctx, size_t bytes) {
+  if (ctx->d_buf_bytes >= bytes) return FAR_OK;
+  if (ctx->d_buf) {
+    CK(cudaDeviceSynchronize());
+    CK(cudaFree(ctx->d_buf));
+    ctx->d_buf = nullptr;
+    ctx->d_buf_bytes = 0;
+  }
+  size_t b = std::max(bytes, (size_t)1 << 20);
+  cudaError_t e = cudaMalloc(&ctx->d_buf, b);
+  if (e != cudaSuccess) return fail(ctx, FAR_E_OOM, "device workspace allocation failed");
+  ctx->d_buf_bytes = b;
+  return FAR_OK;
+}
+
+template <int NC> static Layout layout_for(int n) { return make_layout(n, NC, Tree<NC>::S, Tree<NC>::NN); }
+
+// Launch the fused solver kernel for I instances on `stream`.
+static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
+  if (P.I <= 0) return FAR_OK;
+  const bool a30 = ctx->nc == 3;
+  const Layout L = a30 ? layout_for<3>(P.n) : layout_for<5>(P.n);
+  int warps = std::min(4, SMEM_MAX / std::max(1, L.bytes));
+  if (warps < 1) return fail(ctx, FAR_E_TOO_LARGE, "instance does not fit in shared memory");
+  const size_t smem = (size_t)warps * L.bytes;
+  const void* fn = a30 ? (const void*)far_solve_kernel<3> : (const void*)far_solve_kernel<5>;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, warps * 32, smem));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t need = (P.I + warps - 1) / warps;
+  const int grid = (int)std::min<int64_t>(need, (int64_t)ctx->sms * per_sm);
+  const int slot = ctx->launch_id++ % RING;
+  P.counter = ctx->d_counter + slot;
+  P.errflag = ctx->d_errflag;
+  CK(cudaMemsetAsync(P.counter, 0, sizeof(unsigned long long), stream));
+  if (a30)
+    far_solve_kernel<3><<<grid, warps * 32, smem, stream>>>(P);
+  else
+    far_solve_kernel<5><<<grid, warps * 32, smem, stream>>>(P);
+  CK(cudaGetLastError());
+  return FAR_OK;
+}
+
+static far_status check_opts(far_ctx* ctx, const far_opts* o) {
+  if (o && (o->max_iterations < 0 || o->min_improvement_ppm < 0 || o->min_improvement_ppm > 1000000))
+    return fail(ctx, FAR_E_INVALID_ARG, "far_opts out of range");
+  return FAR_OK;
+}
+
+static void fill_params(far_ctx* ctx, const far_opts* o, KParams& P) {
+  memset(&P, 0, sizeof(P));
+  P.max_it = o ? o->max_iterations : 100;
+  P.ppm = o ? o->min_improvement_ppm : 0;
+  P.flags = o ? o->flags : 0u;
+  const bool zero = (P.flags & FAR_ZERO_RECONFIG) != 0;
+  for (int c = 0; c < 8; ++c) {
+    P.cr[c] = zero ? 0 : ctx->cr[c];
+    P.de[c] = zero ? 0 : ctx->de[c];
+  }
+}
+
+extern "C" {
+
+far_status far_create(far_profile profile, const int32_t* reconfig_cost, far_ctx** out) {
+  if (!out) return FAR_E_INVALID_ARG;
+  *out = nullptr;
+  if (profile != FAR_A30 && profile != FAR_A100 && profile != FAR_H100) return FAR_E_UNSUPPORTED_PROFILE;
+  far_ctx* c = new far_ctx();
+  c->profile = profile;
+  if (profile == FAR_A30) {
+    c->nc = 3; c->ns = Tree<3>::S; c->nn = Tree<3>::NN;
+  } else {
+    c->nc = 5; c->ns = Tree<5>::S; c->nn = Tree<5>::NN;
+  }
+  for (int i = 0; i < c->nc; ++i) c->sizes[i] = c->nc == 3 ? size_of<3>(i) : size_of<5>(i);
+  // Table 2 in 1 ms ticks
+  static const int a30c[3] = {110, 120, 130}, a30d[3] = {100, 100, 100};
+  static const int a100c[5] = {160, 170, 200, 210, 240}, a100d[5] = {200, 200, 210, 210, 220};
+  static const int h100c[5] = {160, 210, 330, 380, 420}, h100d[5] = {210, 230, 250, 260, 260};
+  for (int i = 0; i < c->nc; ++i) {
+    if (reconfig_cost) {
+      c->cr[i] = reconfig_cost[i];
+      c->de[i] = reconfig_cost[c->nc + i];
+      if (c->cr[i] < 0 || c->de[i] < 0 || c->cr[i] >= BOUND || c->de[i] >= BOUND) {
+        delete c;
+        return FAR_E_BAD_TIME;
+      }
+    } else if (profile == FAR_A30) {
+      c->cr[i] = a30c[i]; c->de[i] = a30d[i];
+    } else if (profile == FAR_A100) {
+      c->cr[i] = a100c[i]; c->de[i] = a100d[i];
+    } else {
+      c->cr[i] = h100c[i]; c->de[i] = h100d[i];
+    }
+  }
+  *out = c;
+  return FAR_OK;
+}
+
+void far_destroy(far_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->inited) {
+    cudaDeviceSynchronize();
+    cudaFree(ctx->d_counter);
+    cudaFree(ctx->d_errflag);
+    if (ctx->d_buf) cudaFree(ctx->d_buf);
+    cudaStreamDestroy(ctx->s[0]);
+    cudaStreamDestroy(ctx->s[1]);
+  }
+  delete ctx;
+}
+
+int32_t far_num_sizes(const far_ctx* ctx) { return ctx ? ctx->nc : -1; }
+const int32_t* far_sizes(const far_ctx* ctx) { return ctx ? ctx->sizes : nullptr; }
+int32_t far_num_nodes(const far_ctx* ctx) { return ctx ? ctx->nn : -1; }
+int32_t far_num_slices(const far_ctx* ctx) { return ctx ? ctx->ns : -1; }
+const char* far_last_error(const far_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+far_status far_node_table(const far_ctx* ctx, int32_t* lo, int32_t* hi, int32_t* parent) {
+  if (!ctx || !lo || !hi || !parent) return FAR_E_INVALID_ARG;
+  for (int v = 0; v < ctx->nn; ++v) {
+    const uint32_t w = ctx->nc == 3 ? Tree<3>::node[v] : Tree<5>::node[v];
+    lo[v] = nd_lo(w);
+    hi[v] = nd_lo(w) + nd_sz(w);
+    parent[v] = nd_par(w) == ROOTP ? -1 : nd_par(w);
+  }
+  return FAR_OK;
+}
+
+far_status far_sync(far_ctx* ctx) {
+  if (!ctx) return FAR_E_INVALID_ARG;
+  far_status st = ensure_device(ctx);
+  if (st) return st;
+  CK(cudaDeviceSynchronize());
+  int flag = 0;
+  CK(cudaMemcpy(&flag, ctx->d_errflag, sizeof(int), cudaMemcpyDeviceToHost));
+  if (flag) {
+    CK(cudaMemset(ctx->d_errflag, 0, sizeof(int)));
+    return fail(ctx, (flag & 1) ? FAR_E_BAD_TIME : FAR_E_INVALID_ARG,
+                (flag & 1) ? "an instance failed the input checks (t < 1 or makespan bound)"
+                           : "an instance had an invalid input schedule");
+  }
+  return FAR_OK;
+}
+
+far_status far_solve_many(far_ctx* ctx, const int32_t* d_times, int64_t I, int32_t n, const far_opts* opts,
+                          int32_t* d_makespan, far_task_slot* d_sched, far_result* d_res, void* cuda_stream) {
+  if (!ctx) return FAR_E_INVALID_ARG;
+  if (I < 0 || n < 0) return fail(ctx, FAR_E_INVALID_ARG, "negative I or n");
+  if (n > MAXN) return fail(ctx, FAR_E_TOO_LARGE, "n > 1024");
+  if (I > 0 && (!d_makespan || (n > 0 && !d_times))) return fail(ctx, FAR_E_INVALID_ARG, "null device pointer");
+  far_status st = check_opts(ctx, opts);
+  if (st) return st;
+  if ((st = ensure_device(ctx))) return st;
+  KParams P;
+  fill_params(ctx, opts, P);
+  P.times = d_times;
+  P.I = I;
+  P.n = n;
+  P.makespan = d_makespan;
+  P.sched = d_sched;
+  P.res = d_res;
+  P.mode = MODE_SOLVE;
+  return launch_solve(ctx, P, (cudaStream_t)cuda_stream);
+}
+
+// one instance through device staging; mode SOLVE (phases 1-2 only) or LOCAL
+static far_status one_instance(far_ctx* ctx, const int32_t* times, int32_t n, const far_opts* opts,
+                               far_task_slot* sched, far_result* res, int mode) {
+  if (!ctx) return FAR_E_INVALID_ARG;
+  if (n < 0) return fail(ctx, FAR_E_INVALID_ARG, "negative n");
+  if (n > MAXN) return fail(ctx, FAR_E_TOO_LARGE, "n > 1024");
+  if ((n > 0 && (!times || !sched)) || !res) return fail(ctx, FAR_E_INVALID_ARG, "null host pointer");
+  far_status st = check_opts(ctx, opts);
+  if (st) return st;
+  if ((st = ensure_device(ctx))) return st;
+  const size_t tb = (size_t)n * ctx->nc * 4, sb = (size_t)n * sizeof(far_task_slot);
+  const size_t o_t = 0, o_s = (tb + 255) & ~(size_t)255, o_si = o_s + ((sb + 255) & ~(size_t)255);
+  const size_t o_r = o_si + ((sb + 255) & ~(size_t)255), o_ri = o_r + 256, o_m = o_ri + 256;
+  if ((st = ensure_buf(ctx, o_m + 256))) return st;
+  cudaStream_t s = ctx->s[0];
+  KParams P;
+  fill_params(ctx, opts, P);
+  if (mode == MODE_SOLVE) P.flags |= FAR_NO_REFINE;
+  P.flags &= ~(unsigned)FAR_NO_SCHEDULE;
+  P.times = (const int32_t*)(ctx->d_buf + o_t);
+  P.I = 1;
+  P.n = n;
+  P.makespan = (int32_t*)(ctx->d_buf + o_m);
+  P.sched = n > 0 ? (far_task_slot*)(ctx->d_buf + o_s) : nullptr;
+  P.res = (far_result*)(ctx->d_buf + o_r);
+  P.mode = mode;
+  if (tb) CK(cudaMemcpyAsync(ctx->d_buf + o_t, times, tb, cudaMemcpyHostToDevice, s));
+  if (mode == MODE_LOCAL) {
+    if (sb) CK(cudaMemcpyAsync(ctx->d_buf + o_si, sched, sb, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->d_buf + o_ri, res, sizeof(far_result), cudaMemcpyHostToDevice, s));
+    P.sched_in = (const far_task_slot*)(ctx->d_buf + o_si);
+    P.res_in = (const far_result*)(ctx->d_buf + o_ri);
+  }
+  if ((st = launch_solve(ctx, P, s))) return st;
+  far_result r;
+  CK(cudaMemcpyAsync(&r, P.res, sizeof(far_result), cudaMemcpyDeviceToHost, s));
+  if (sb) CK(cudaMemcpyAsync(sched, P.sched, sb, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  int flag = 0;
+  CK(cudaMemcpy(&flag, ctx->d_errflag, sizeof(int), cudaMemcpyDeviceToHost));
+  if (flag) CK(cudaMemset(ctx->d_errflag, 0, sizeof(int)));
+  *res = r;
+  if (r.status != FAR_OK)
+    return fail(ctx, (far_status)r.status,
+                r.status == FAR_E_BAD_TIME ? "input check failed (t < 1 or makespan bound)" : "invalid input schedule");
+  return FAR_OK;
+}
+
+far_status far_schedule_batch(far_ctx* ctx, const int32_t* times, int32_t n, const far_opts* opts,
+                              far_task_slot* sched, far_result* res) {
+  return one_instance(ctx, times, n, opts, sched, res, MODE_SOLVE);
+}
+
+far_status far_local_search(far_ctx* ctx, const int32_t* times, int32_t n, const far_opts* opts,
+                            far_task_slot* sched, far_result* res) {
+  return one_instance(ctx, times, n, opts, sched, res, MODE_LOCAL);
+}
+
+far_status far_solve_many_host(far_ctx* ctx, const int32_t* h_times, int64_t I, int32_t n, const far_opts* opts,
+                               int32_t* h_makespan, far_task_slot* h_sched, far_result* h_res) {
+  if (!ctx) return FAR_E_INVALID_ARG;
+  if (I < 0 || n < 0) return fail(ctx, FAR_E_INVALID_ARG, "negative I or n");
+  if (n > MAXN) return fail(ctx, FAR_E_TOO_LARGE, "n > 1024");
+  if (I > 0 && (!h_makespan || (n > 0 && !h_times))) return fail(ctx, FAR_E_INVALID_ARG, "null host pointer");
+  far_status st = check_opts(ctx, opts);
+  if (st) return st;
+  if ((st = ensure_device(ctx))) return st;
+  if (I == 0) return FAR_OK;
+  const bool want_sched = h_sched && !(opts && (opts->flags & FAR_NO_SCHEDULE));
+  const size_t per_t = (size_t)n * ctx->nc * 4, per_s = want_sched ? (size_t)n * sizeof(far_task_slot) : 0;
+  const size_t per_r = h_res ? sizeof(far_result) : 0, per_m = 4;
+  const size_t per = per_t + per_s + per_r + per_m;
+  // chunk: ~48 MB of staging per stream
+  int64_t chunk = std::max<int64_t>(1, ((size_t)48 << 20) / std::max<size_t>(per, 1));
+  chunk = std::min<int64_t>(chunk, I);
+  auto a256 = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t bt = a256(chunk * per_t), bs = a256(chunk * per_s), br = a256(chunk * per_r), bm = a256(chunk * per_m);
+  const size_t per_stream = bt + bs + br + bm;
+  if ((st = ensure_buf(ctx, 2 * per_stream))) return st;
+  KParams P;
+  fill_params(ctx, opts, P);
+  P.n = n;
+  P.mode = MODE_SOLVE;
+  int64_t nchunks = (I + chunk - 1) / chunk;
+  for (int64_t q = 0; q < nchunks; ++q) {
+    const int si = (int)(q & 1);
+    cudaStream_t s = ctx->s[si];
+    char* base = ctx->d_buf + si * per_stream;
+    const int64_t i0 = q * chunk, cnt = std::min(chunk, I - i0);
+    if (per_t) CK(cudaMemcpyAsync(base, (const char*)h_times + i0 * per_t, cnt * per_t, cudaMemcpyHostToDevice, s));
+    P.times = (const int32_t*)base;
+    P.I = cnt;
+    P.sched = want_sched ? (far_task_slot*)(base + bt) : nullptr;
+    P.res = h_res ? (far_result*)(base + bt + bs) : nullptr;
+    P.makespan = (int32_t*)(base + bt + bs + br);
+    if ((st = launch_solve(ctx, P, s))) return st;
+    CK(cudaMemcpyAsync(h_makespan + i0, P.makespan, cnt * per_m, cudaMemcpyDeviceToHost, s));
+    if (want_sched)
+      CK(cudaMemcpyAsync((char*)h_sched + i0 * per_s, P.sched, cnt * per_s, cudaMemcpyDeviceToHost, s));
+    if (h_res) CK(cudaMemcpyAsync(h_res + i0, P.res, cnt * per_r, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(ctx->s[0]));
+  CK(cudaStreamSynchronize(ctx->s[1]));
+  int flag = 0;
+  CK(cudaMemcpy(&flag, ctx->d_errflag, sizeof(int), cudaMemcpyDeviceToHost));
+  if (flag) {
+    CK(cudaMemset(ctx->d_errflag, 0, sizeof(int)));
+    return fail(ctx, FAR_E_BAD_TIME, "an instance failed the input checks (t < 1 or makespan bound)");
+  }
+  return FAR_OK;
+}
+
+}  // extern "C"
+
+extern "C" far_status far_concat_streams(far_ctx* ctx, const int32_t* d_times, int64_t S, int32_t B, int32_t n,
+                                         const far_opts* opts, int64_t* d_stream_makespan, int64_t* d_offsets,
+                                         far_result* d_batch_res, int32_t* d_seam, void* cuda_stream) {
+  (void)d_times; (void)S; (void)B; (void)n; (void)opts; (void)d_stream_makespan; (void)d_offsets;
+  (void)d_batch_res; (void)d_seam; (void)cuda_stream;
+  return fail(ctx, FAR_E_INVALID_ARG, "far_concat_streams: not built yet");
+}

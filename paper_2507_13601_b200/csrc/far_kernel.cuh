@@ -1,0 +1,846 @@
+// far_kernel.cuh — fused sm_100a kernel: one WARP solves one FAR instance end to end.
+//
+//   H0 stage   : the instance's runtime table t[n][|C|] -> shared memory (int4 loads)
+//   H1/H2      : phase 1, Turek family — warp argmax per growth step
+//   H3         : per-size LPT lists (Alg. 1 lines 1-2) of every (task, size)
+//                that some family member uses, each entry tagged with the member
+//                interval [lo, hi) in which the task has that size
+//   H4         : phase 2, Alg. 1 for every family member IN PARALLEL, one
+//                member per lane; the heap of frontier nodes is a register array
+//                indexed by first slice (the frontier is an antichain, so the first
+//                slice is a unique key and the (end, lo) tie-break is the scan order)
+//   H5         : k* = argmin (makespan_k, k) by two REDUX.MIN
+//   H6         : phase 3, Alg. 2: warp-parallel move / swap candidate
+//                search with deterministic packed-key argmins
+//   H7         : line-26 replay + keep-best guard, coalesced output stores
+//
+// Readings of the paper: DESIGN.md "Readings" (identical to the oracle's; the two
+// share no code).  All times int32.
+#pragma once
+#include <climits>
+#include <cstdint>
+
+#include "../../include/far.h"
+#include "far_tree.cuh"
+
+namespace farb {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int MAXN = 1024;
+constexpr int BOUND = 1 << 30;
+enum { MODE_SOLVE = 0, MODE_LOCAL = 1 };
+
+struct KParams {
+  const int32_t* times;
+  int64_t I;
+  int n;
+  int32_t* makespan;
+  far_task_slot* sched;
+  far_result* res;
+  const far_task_slot* sched_in;  // MODE_LOCAL
+  const far_result* res_in;       // MODE_LOCAL
+  int cr[8], de[8];               // create / destroy cost per size index (ticks)
+  int max_it, ppm;
+  unsigned flags;
+  int mode;
+  unsigned long long* counter;  // dynamic instance scheduler (reset to 0 before launch)
+  int* errflag;                 // sticky input-error flag
+};
+
+// Per-warp shared-memory layout (bytes), identical on host and device.
+struct Layout {
+  int times, lent, ltask, cnts, cur, su, bestnode, scratch, lstate, lslice, start, misc, bytes;
+};
+
+__host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
+
+__host__ __device__ inline Layout make_layout(int n, int NC, int S, int NN) {
+  Layout L;
+  const int Kmax = 1 + n * (NC - 1), Emax = n * NC;
+  int o = 0;
+  L.times = o;    o = al16(o + 4 * n * NC);
+  L.lent = o;     o = al16(o + 8 * Emax);
+  L.ltask = o;    o = al16(o + 2 * Emax);
+  L.cnts = o;     o = al16(o + 8 * Kmax);
+  L.cur = o;      o = al16(o + n);
+  L.su = o;       o = al16(o + n);
+  L.bestnode = o; o = al16(o + n);
+  int sc = 32 * n;
+  if (10 * Emax > sc) sc = 10 * Emax;
+  if (2 * NN * n > sc) sc = 2 * NN * n;
+  L.scratch = o;  o = al16(o + sc);
+  L.lstate = o;   o = al16(o + 4 * NC * 32);
+  L.lslice = o;   o = al16(o + 4 * S * 32);
+  L.start = o;    o = al16(o + 4 * n);
+  L.misc = o;     o = al16(o + 4 * 96);
+  L.bytes = o;
+  return L;
+}
+
+// misc int slots
+enum { M_LOFF = 0, M_NCNT = 8, M_LP = 24, M_SEND = 40, M_BSEND = 48, M_Q = 56 };
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// slices of size index c: A30 {1,2,4}; A100/H100 {1,2,3,4,7}
+template <int NC> __host__ __device__ __forceinline__ int size_of(int c) {
+  return NC == 3 ? (c == 2 ? 4 : c + 1) : (c == 4 ? 7 : c + 1);
+}
+// leaf node of slice s (node ids of include/far.h)
+template <int NC> __device__ __forceinline__ int leaf_of(int s) {
+  return NC == 3 ? 3 + s : (s < 6 ? 7 + s : 6);
+}
+
+// ---------------------------------------------------------------------------
+// Frontier of Alg. 1: slot s (= first slice) holds the node starting at s, its end
+// time, and whether it already has tasks.  Pop = min (end, slot) by an unrolled scan.
+// ---------------------------------------------------------------------------
+template <int S> struct Frontier {
+  int e[S];
+  uint32_t slotnode = 0, live = 1, has = 0;
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int s = 0; s < S; ++s) e[s] = INT_MAX;
+    e[0] = 0;
+    slotnode = 0;  // root (node 0) in slot 0
+    live = 1;
+    has = 0;
+  }
+  __device__ __forceinline__ void pop(int& bs, int& be) const {
+    bs = 0;
+    be = e[0];
+#pragma unroll
+    for (int s = 1; s < S; ++s) {
+      const bool lt = e[s] < be;
+      be = lt ? e[s] : be;
+      bs = lt ? s : bs;
+    }
+  }
+  __device__ __forceinline__ void set(int bs, int v) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) e[s] = (s == bs) ? v : e[s];
+  }
+  __device__ __forceinline__ int node(int s) const { return (slotnode >> (4 * s)) & 15; }
+  // Alg. 1 lines 17-24 (repartitioning) after the optional destroy; returns false if v was a leaf.
+  __device__ __forceinline__ bool split(int bs, int be, uint32_t w) {
+    has &= ~(1u << bs);
+    const int ch1 = nd_ch1(w);
+    if (ch1 != LEAF) {
+      const int s2 = nd_ch2lo(w);
+      slotnode = (slotnode & ~(15u << (4 * bs))) | ((uint32_t)ch1 << (4 * bs));
+      slotnode = (slotnode & ~(15u << (4 * s2))) | ((uint32_t)nd_ch2(w) << (4 * s2));
+      live |= 1u << s2;
+      set(s2, be);  // C.end := I.end for both children (slot bs keeps be)
+      return true;
+    }
+    live &= ~(1u << bs);
+    set(bs, INT_MAX);
+    return false;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Replay (Alg. 2 line 26, O7): the Alg. 1 event loop taking each node's tasks from its
+// ordered list.  One lane.  Writes start[j], onode[j]; returns the makespan.
+// ---------------------------------------------------------------------------
+template <int NC>
+__device__ int replay_one(int n, const int32_t* T, const uint8_t* su, const uint16_t* nlist, const int* ncnt,
+                          int* lp, int* start, uint8_t* onode, const uint32_t* ninfo, const int* cr, const int* de) {
+  constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
+  for (int v = 0; v < NN; ++v) lp[v] = 0;
+  Frontier<S> F;
+  F.init();
+  int rec = 0, ms = 0, remaining = n;
+  while (remaining > 0) {
+    int bs, be;
+    F.pop(bs, be);
+    if (be == INT_MAX) break;  // unreachable: every listed task is reachable
+    const int v = F.node(bs);
+    const uint32_t w = ninfo[v];
+    if (lp[v] < ncnt[v]) {
+      if (!((F.has >> bs) & 1)) {
+        rec = max(rec, be) + cr[nd_szi(w)];
+        be = rec;
+        F.has |= 1u << bs;
+      }
+      const int j = nlist[v * n + lp[v]];
+      lp[v]++;
+      start[j] = be;
+      onode[j] = (uint8_t)v;
+      be += T[j * NC + su[j]];
+      ms = max(ms, be);
+      --remaining;
+      F.set(bs, be);
+    } else {
+      if ((F.has >> bs) & 1) rec = max(rec, be) + de[nd_szi(w)];
+      F.split(bs, be, w);
+    }
+  }
+  return ms;
+}
+
+// ---------------------------------------------------------------------------
+// Phase 3: Alg. 2 on node lists (warp-cooperative).  sliceEnd in smem.
+// ---------------------------------------------------------------------------
+template <int NC>
+__device__ __forceinline__ int dur_of(const int32_t* T, const uint8_t* su, int j) {
+  return T[j * NC + su[j]];
+}
+
+template <int NC>
+__device__ void list_remove(uint16_t* lst, int* cnt, int j, int lane) {
+  if (lane == 0) {
+    int q = 0;
+    while (lst[q] != j) ++q;
+    for (; q + 1 < *cnt; ++q) lst[q] = lst[q + 1];
+    *cnt -= 1;
+  }
+  __syncwarp();
+}
+
+// "Insert T in I^a.tasks ordered by T.time": decreasing time, ties -> lower index.
+template <int NC>
+__device__ void list_insert(uint16_t* lst, int* cnt, int j, const int32_t* T, const uint8_t* su, int lane) {
+  if (lane == 0) {
+    const int dj = dur_of<NC>(T, su, j);
+    int q = *cnt;
+    while (q > 0) {
+      const int x = lst[q - 1];
+      const int dx = dur_of<NC>(T, su, x);
+      if (dx > dj || (dx == dj && x < j)) break;
+      lst[q] = lst[q - 1];
+      --q;
+    }
+    lst[q] = (uint16_t)j;
+    *cnt += 1;
+  }
+  __syncwarp();
+}
+
+template <int NC>
+__device__ void refine_warp(int n, const int32_t* T, const uint8_t* su, uint16_t* nlist, int* ncnt, int* send,
+                            const uint32_t* ninfo, int max_it, int ppm, int lane, int& moves, int& swaps, int& iters,
+                            long long& evals) {
+  constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
+  auto end_of = [&](uint32_t w) {
+    int e = 0;
+    const int lo = nd_lo(w), hi = lo + nd_sz(w);
+    for (int s = lo; s < hi; ++s) e = max(e, send[s]);
+    return e;
+  };
+  auto add_on = [&](uint32_t w, int d) {
+    const int lo = nd_lo(w);
+    if (lane >= lo && lane < lo + nd_sz(w)) send[lane] += d;
+    __syncwarp();
+  };
+  int omega = 0;
+  for (int s = 0; s < S; ++s) omega = max(omega, send[s]);
+  moves = swaps = iters = 0;
+  evals = 0;
+  bool stop = false;
+  while (!stop && iters < max_it) {
+    ++iters;
+    const int omega_prev = omega;
+    unsigned long long Q = 0;  // FIFO of node ids, 4 bits each
+    int qh = 0, qt = 0;
+    uint32_t opened = 0;
+    for (int s = 0; s < S; ++s)
+      if (send[s] == omega) {
+        const int leaf = leaf_of<NC>(s);
+        Q |= (unsigned long long)leaf << (4 * qt++);
+        opened |= 1u << leaf;
+      }
+    while (qh < qt) {
+      const int I = (int)((Q >> (4 * qh++)) & 15);
+      if (I == 0) { stop = true; break; }
+      const uint32_t wI = ninfo[I];
+      int A = -1, eA = 0;
+      for (int u = 0; u < NN; ++u) {
+        const uint32_t wu = ninfo[u];
+        if (u == I || nd_sz(wu) != nd_sz(wI)) continue;
+        const int eu = end_of(wu);
+        if (A < 0 || eu < eA || (eu == eA && nd_lo(wu) < nd_lo(ninfo[A]))) { A = u; eA = eu; }
+      }
+      bool done = false;
+      if (A >= 0) {
+        const int m = omega - eA;
+        const int nI = ncnt[I];
+        uint16_t* LI = nlist + I * n;
+        uint16_t* LA = nlist + A * n;
+        evals += nI;
+        // move: argmin (|2t - m|, index) over t < m
+        unsigned bd = UINT_MAX;
+        int bj = INT_MAX;
+        for (int q = lane; q < nI; q += 32) {
+          const int j = LI[q];
+          const int t = dur_of<NC>(T, su, j);
+          if (t < m) {
+            const unsigned d = (unsigned)abs(2 * t - m);
+            if (d < bd || (d == bd && j < bj)) { bd = d; bj = j; }
+          }
+        }
+        const unsigned dmin = __reduce_min_sync(FULL, bd);
+        if (dmin != UINT_MAX) {
+          const int Tm = __reduce_min_sync(FULL, (unsigned)(bd == dmin ? bj : INT_MAX));
+          const int t = dur_of<NC>(T, su, Tm);
+          list_remove<NC>(LI, &ncnt[I], Tm, lane);
+          list_insert<NC>(LA, &ncnt[A], Tm, T, su, lane);
+          add_on(wI, -t);
+          add_on(ninfo[A], t);
+          ++moves;
+          done = true;
+        } else {
+          const int nA = ncnt[A];
+          evals += (long long)nI * nA;
+          unsigned bd2 = UINT_MAX, bkey = UINT_MAX;
+          const int tot = nI * nA;
+          for (int p = lane; p < tot; p += 32) {
+            const int qi = p / nA, qa = p - qi * nA;
+            const int k = LI[qi], j = LA[qa];
+            const int delta = dur_of<NC>(T, su, k) - dur_of<NC>(T, su, j);
+            if (0 < delta && delta < m) {
+              const unsigned d = (unsigned)abs(2 * delta - m);
+              const unsigned key = ((unsigned)k << 10) | (unsigned)j;
+              if (d < bd2 || (d == bd2 && key < bkey)) { bd2 = d; bkey = key; }
+            }
+          }
+          const unsigned d2 = __reduce_min_sync(FULL, bd2);
+          if (d2 != UINT_MAX) {
+            const unsigned key = __reduce_min_sync(FULL, bd2 == d2 ? bkey : UINT_MAX);
+            const int k = (int)(key >> 10), j = (int)(key & 1023);
+            const int delta = dur_of<NC>(T, su, k) - dur_of<NC>(T, su, j);
+            list_remove<NC>(LI, &ncnt[I], k, lane);
+            list_remove<NC>(LA, &ncnt[A], j, lane);
+            list_insert<NC>(LA, &ncnt[A], k, T, su, lane);
+            list_insert<NC>(LI, &ncnt[I], j, T, su, lane);
+            add_on(wI, -delta);
+            add_on(ninfo[A], delta);
+            ++swaps;
+            done = true;
+          }
+        }
+      }
+      if (!done) {
+        const int par = nd_par(wI);
+        if (par != ROOTP && !((opened >> par) & 1)) {
+          opened |= 1u << par;
+          Q |= (unsigned long long)par << (4 * qt++);
+        }
+      }
+    }
+    omega = 0;
+    for (int s = 0; s < S; ++s) omega = max(omega, send[s]);
+    if (ppm > 0 && (long long)(omega_prev - omega) * 1000000LL < (long long)ppm * omega_prev) break;
+  }
+}
+
+// Build per-node ordered lists of member k from the per-size LPT lists: sizes in
+// decreasing order so the A100 {S0..S3} node lists its size-4 tasks before its size-3
+// tasks.  Lane 0.
+template <int NC>
+__device__ void build_node_lists(int n, int k, const int2* lent, const uint16_t* ltask, const int* loff,
+                                 const uint8_t* node_of, uint16_t* nlist, int* ncnt, uint8_t* su, int lane) {
+  constexpr int NN = Tree<NC>::NN;
+  if (lane == 0) {
+    for (int v = 0; v < NN; ++v) ncnt[v] = 0;
+    for (int c = NC - 1; c >= 0; --c)
+      for (int p = loff[c]; p < loff[c + 1]; ++p) {
+        const int y = lent[p].y;
+        const int lo = y & 0xFFFF, hi = (int)((unsigned)y >> 16);
+        if (lo <= k && k < hi) {
+          const int j = ltask[p];
+          const int v = node_of[j];
+          nlist[v * n + ncnt[v]++] = (uint16_t)j;
+          su[j] = (uint8_t)c;
+        }
+      }
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// One instance, one warp.
+// ---------------------------------------------------------------------------
+template <int NC>
+__device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* wsm, const Layout& L,
+                               const uint32_t* ninfo, const int* cr, const int* de, int lane) {
+  constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
+  const int n = P.n;
+  int32_t* T = (int32_t*)(wsm + L.times);
+  int2* lent = (int2*)(wsm + L.lent);
+  uint16_t* ltask = (uint16_t*)(wsm + L.ltask);
+  unsigned long long* cnts = (unsigned long long*)(wsm + L.cnts);
+  uint8_t* cur = wsm + L.cur;
+  uint8_t* su = wsm + L.su;
+  uint8_t* bestnode = wsm + L.bestnode;
+  unsigned char* scratch = wsm + L.scratch;
+  uint32_t* lstate = (uint32_t*)(wsm + L.lstate);
+  int* lslice = (int*)(wsm + L.lslice);
+  int* start = (int*)(wsm + L.start);
+  int* misc = (int*)(wsm + L.misc);
+  int* loff = misc + M_LOFF;
+  int* ncnt = misc + M_NCNT;
+  int* lp = misc + M_LP;
+  int* send = misc + M_SEND;
+  int* bsend = misc + M_BSEND;
+
+  // ---- H0: stage the runtime table (contiguous n*NC int32) into shared memory
+  const int cntT = n * NC;
+  const int32_t* src = P.times + inst * (int64_t)cntT;
+  if ((((uintptr_t)src) & 15) == 0) {
+    const int n4 = cntT >> 2;
+    const int4* s4 = (const int4*)src;
+    int4* d4 = (int4*)T;
+    for (int q = lane; q < n4; q += 32) d4[q] = __ldcs(s4 + q);
+    for (int q = (n4 << 2) + lane; q < cntT; q += 32) T[q] = __ldcs(src + q);
+  } else {
+    for (int q = lane; q < cntT; q += 32) T[q] = __ldcs(src + q);
+  }
+  __syncwarp();
+
+  far_result R;
+  R.makespan = 0; R.makespan_phase2 = 0; R.alloc_index = 0; R.family_size = 0;
+  R.moves = 0; R.swaps = 0; R.iterations = 0; R.reverted = 0; R.status = FAR_OK; R.reserved = 0;
+  R.evals = 0; R.events = 0;
+  const bool want_sched = P.sched != nullptr && !(P.flags & FAR_NO_SCHEDULE);
+  const bool refine = !(P.flags & FAR_NO_REFINE);
+
+  // ---- input checks (include/far.h "Integer range")
+  {
+    int bad = 0;
+    long long bsum = 0;
+    for (int j = lane; j < n; j += 32) {
+      int mx = 0;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int t = T[j * NC + c];
+        bad |= (t < 1);
+        mx = max(mx, t);
+      }
+      bsum += mx;
+    }
+    bad = __any_sync(FULL, bad);
+    bsum = warp_sum_ll(bsum);
+    long long rsum = 0;
+    for (int v = 0; v < NN; ++v) rsum += cr[nd_szi(ninfo[v])] + de[nd_szi(ninfo[v])];
+    if (bad || bsum + rsum >= BOUND) {
+      if (lane == 0) {
+        R.makespan = -1;
+        R.status = FAR_E_BAD_TIME;
+        P.makespan[inst] = -1;
+        if (P.res) P.res[inst] = R;
+        atomicOr(P.errflag, 1);
+      }
+      return;
+    }
+  }
+
+  int ms2 = 0, bestk = 0;
+  if (P.mode == MODE_LOCAL) {
+    // ---- rebuild the tree from an input schedule: node lists ordered by (start, task)
+    const far_task_slot* in = P.sched_in + inst * (int64_t)n;
+    int bad = 0, msIn = 0;
+    for (int j = lane; j < n; j += 32) {
+      const far_task_slot s = in[j];
+      int c = -1;
+      if (s.node < NN) {
+        const uint32_t w = ninfo[s.node];
+        if (size_of<NC>(nd_c0(w)) == s.size_used) c = nd_c0(w);
+        else if (nd_c1(w) != NONE && size_of<NC>(nd_c1(w)) == s.size_used) c = nd_c1(w);
+      }
+      if (c < 0 || s.start < 0 || s.start > BOUND) { bad = 1; c = 0; }
+      cur[j] = s.node < NN ? s.node : 0;
+      su[j] = (uint8_t)c;
+      start[j] = s.start;
+      msIn = max(msIn, s.start + T[j * NC + c]);
+    }
+    bad = __any_sync(FULL, bad);
+    msIn = __reduce_max_sync(FULL, msIn);
+    if (bad) {
+      if (lane == 0) {
+        R.makespan = -1;
+        R.status = FAR_E_INVALID_ARG;
+        P.makespan[inst] = -1;
+        if (P.res) P.res[inst] = R;
+        atomicOr(P.errflag, 2);
+      }
+      return;
+    }
+    __syncwarp();
+    uint16_t* nlist = (uint16_t*)scratch;
+    for (int j = lane; j < n; j += 32) {
+      const int v = cur[j], sj = start[j];
+      int pos = 0;
+      for (int q = 0; q < n; ++q)
+        pos += (cur[q] == v) && (start[q] < sj || (start[q] == sj && q < j));
+      nlist[v * n + pos] = (uint16_t)j;
+    }
+    for (int v = 0; v < NN; ++v) {
+      int c = 0;
+      for (int j = lane; j < n; j += 32) c += (cur[j] == v);
+      c = __reduce_add_sync(FULL, c);
+      if (lane == 0) ncnt[v] = c;
+    }
+    for (int s = 0; s < S; ++s) {
+      int e = 0;
+      for (int j = lane; j < n; j += 32) {
+        const uint32_t w = ninfo[cur[j]];
+        if (s >= nd_lo(w) && s < nd_lo(w) + nd_sz(w)) e = max(e, start[j] + T[j * NC + su[j]]);
+      }
+      e = __reduce_max_sync(FULL, e);
+      if (lane == 0) send[s] = e;
+    }
+    __syncwarp();
+    const far_result rin = P.res_in ? P.res_in[inst] : R;
+    R.alloc_index = rin.alloc_index;
+    R.family_size = rin.family_size;
+    R.events = rin.events;
+    ms2 = (P.res_in && rin.makespan_phase2 > 0) ? rin.makespan_phase2 : msIn;
+    R.makespan_phase2 = ms2;
+    int msF = msIn;
+    bool use_input = true;
+    if (refine && n > 0) {
+      int mv, sw, it;
+      long long ev;
+      refine_warp<NC>(n, T, su, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
+      R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
+      int msR = 0;
+      if (lane == 0) msR = replay_one<NC>(n, T, su, nlist, ncnt, lp, start + 0, bestnode, ninfo, cr, de);
+      // replay wrote into start[] / bestnode[] only on lane 0's view; broadcast
+      msR = __shfl_sync(FULL, msR, 0);
+      __syncwarp();
+      if (!(P.flags & FAR_NO_GUARD) && msR > ms2) {
+        R.reverted = 1;
+      } else {
+        use_input = false;
+        msF = msR;
+      }
+    }
+    R.makespan = msF;
+    if (want_sched) {
+      far_task_slot* out = P.sched + inst * (int64_t)n;
+      for (int j = lane; j < n; j += 32) {
+        if (use_input) {
+          out[j] = in[j];
+        } else {
+          far_task_slot s;
+          s.node = bestnode[j];
+          s.size_used = (uint8_t)size_of<NC>(su[j]);
+          s.pad[0] = s.pad[1] = 0;
+          s.start = start[j];
+          out[j] = s;
+        }
+      }
+    }
+    if (lane == 0) {
+      P.makespan[inst] = R.makespan;
+      if (P.res) P.res[inst] = R;
+    }
+    return;
+  }
+
+  if (n == 0) {
+    if (lane == 0) {
+      P.makespan[inst] = 0;
+      if (P.res) P.res[inst] = R;
+    }
+    return;
+  }
+
+  // ---- H1: first allocation a^1_i = argmin_s s*t_i(s), ties -> smallest s
+  uint32_t* ivl = (uint32_t*)scratch;  // [n][NC] member interval lo | hi<<16 (0xFFFF = absent/open)
+  unsigned long long c0pack = 0;
+  {
+    int cnt_c[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) cnt_c[c] = 0;
+    for (int j = lane; j < n; j += 32) {
+      int best = 0;
+      long long bw = (long long)size_of<NC>(0) * T[j * NC];
+#pragma unroll
+      for (int c = 1; c < NC; ++c) {
+        const long long w = (long long)size_of<NC>(c) * T[j * NC + c];
+        if (w < bw) { bw = w; best = c; }
+      }
+      cur[j] = (uint8_t)best;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        cnt_c[c] += (c == best);
+        ivl[j * NC + c] = (c == best) ? 0xFFFF0000u : 0xFFFFFFFFu;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) c0pack |= (unsigned long long)__reduce_add_sync(FULL, cnt_c[c]) << (11 * c);
+  }
+  if (lane == 0) cnts[0] = c0pack;
+  __syncwarp();
+
+  // ---- H2: a^{k+1}: grow the longest task (ties -> lowest index) to
+  //          argmin_{s > a_j} s*t_j(s) (ties -> smallest s); stop when it is at max size
+  int K = 1;
+  {
+    unsigned long long cp = c0pack;
+    for (;;) {
+      int lm = -1, lj = INT_MAX;
+      for (int j = lane; j < n; j += 32) {
+        const int t = T[j * NC + cur[j]];
+        if (t > lm) { lm = t; lj = j; }
+      }
+      const int m = __reduce_max_sync(FULL, lm);
+      const int jj = (int)__reduce_min_sync(FULL, (unsigned)(lm == m ? lj : INT_MAX));
+      const int cj = cur[jj];
+      if (cj == NC - 1) break;
+      int best = -1;
+      long long bw = 0;
+      for (int c = cj + 1; c < NC; ++c) {
+        const long long w = (long long)size_of<NC>(c) * T[jj * NC + c];
+        if (best < 0 || w < bw) { bw = w; best = c; }
+      }
+      cp = cp - (1ull << (11 * cj)) + (1ull << (11 * best));
+      __syncwarp();
+      if (lane == 0) {
+        cur[jj] = (uint8_t)best;
+        ivl[jj * NC + cj] = (ivl[jj * NC + cj] & 0xFFFFu) | ((uint32_t)K << 16);  // leaves size cj at member K
+        ivl[jj * NC + best] = (uint32_t)K | 0xFFFF0000u;                          // enters size best at member K
+        cnts[K] = cp;
+      }
+      __syncwarp();
+      ++K;
+    }
+  }
+  R.family_size = K;
+
+  // ---- H3: per-size LPT lists of the (task, size) pairs used by some member, with the
+  //          member interval; order (-t(s), task) (Alg. 1 lines 1-2)
+  int off[NC + 1];
+  {
+    off[0] = 0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      int cnt = 0;
+      for (int j = lane; j < n; j += 32) cnt += ((ivl[j * NC + c] & 0xFFFFu) != 0xFFFFu);
+      off[c + 1] = off[c] + __reduce_add_sync(FULL, cnt);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c <= NC; ++c) loff[c] = off[c];
+    }
+    // compaction (unsorted) into the final segments
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      int base = off[c];
+      for (int j0 = 0; j0 < n; j0 += 32) {
+        const int j = j0 + lane;
+        uint32_t iv = 0xFFFFFFFFu;
+        if (j < n) iv = ivl[j * NC + c];
+        const bool pres = (iv & 0xFFFFu) != 0xFFFFu;
+        const unsigned bal = __ballot_sync(FULL, pres);
+        if (pres) {
+          const int pos = base + __popc(bal & ((1u << lane) - 1));
+          uint32_t hi = iv >> 16;
+          if (hi == 0xFFFFu) hi = (uint32_t)K;
+          lent[pos] = make_int2(T[j * NC + c], (int)((iv & 0xFFFFu) | (hi << 16)));
+          ltask[pos] = (uint16_t)j;
+        }
+        base += __popc(bal);
+      }
+    }
+    __syncwarp();
+    // rank sort inside each segment -> scratch (ivl is dead), then copy back
+    int2* sent = (int2*)scratch;
+    uint16_t* stask = (uint16_t*)(scratch + 8 * n * NC);
+    for (int c = 0; c < NC; ++c) {
+      const int b = off[c], m = off[c + 1] - off[c];
+      for (int e = lane; e < m; e += 32) {
+        const int2 x = lent[b + e];
+        const int tj = ltask[b + e];
+        int rank = 0;
+        for (int f = 0; f < m; ++f) {
+          const int tf = lent[b + f].x;
+          rank += (tf > x.x) || (tf == x.x && (int)ltask[b + f] < tj);
+        }
+        sent[b + rank] = x;
+        stask[b + rank] = (uint16_t)tj;
+      }
+    }
+    __syncwarp();
+    for (int p = lane; p < off[NC]; p += 32) {
+      lent[p] = sent[p];
+      ltask[p] = stask[p];
+    }
+    __syncwarp();
+  }
+
+  // ---- H4: Alg. 1 for every family member, one member per lane
+  uint8_t* recnode = scratch;  // [n][32]: node of task j in this lane's member
+  int bestms = INT_MAX;
+  long long events = 0;
+  for (int kb = 0; kb < K; kb += 32) {
+    const int k = kb + lane;
+    int ms = INT_MAX, pops = 0;
+    if (k < K) {
+      const unsigned long long cp = cnts[k];
+      int total = 0;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int r = (int)((cp >> (11 * c)) & 2047);
+        lstate[c * 32 + lane] = (uint32_t)r << 16;
+        total += r;
+      }
+      Frontier<S> F;
+      F.init();
+      int rec = 0;
+      ms = 0;
+      while (total > 0) {
+        int bs, be;
+        F.pop(bs, be);
+        const int v = F.node(bs);
+        const uint32_t w = ninfo[v];
+        // line 7: unscheduled tasks of a hosted size (A100 {S0..S3}: size 4 first, then 3)
+        int c = nd_c0(w);
+        uint32_t sv = lstate[c * 32 + lane];
+        if (!(sv >> 16)) {
+          c = nd_c1(w);
+          sv = 0;
+          if (c != NONE) sv = lstate[c * 32 + lane];
+        }
+        ++pops;
+        if (sv >> 16) {
+          if (!((F.has >> bs) & 1)) {  // lines 8-11: creation, sequenced on reconfig_end
+            rec = max(rec, be) + cr[nd_szi(w)];
+            be = rec;
+            F.has |= 1u << bs;
+          }
+          // line 12: longest unscheduled task of size c for member k (skip other members' entries)
+          int p = (int)(sv & 0xFFFFu);
+          const int base = loff[c];
+          int2 ent;
+          for (;;) {
+            ent = lent[base + p];
+            ++p;
+            const int lo = ent.y & 0xFFFF, hi = (int)((unsigned)ent.y >> 16);
+            if (lo <= k && k < hi) break;
+          }
+          recnode[(int)ltask[base + p - 1] * 32 + lane] = (uint8_t)v;
+          lstate[c * 32 + lane] = ((sv & 0xFFFF0000u) - 0x10000u) | (uint32_t)p;
+          be += ent.x;  // lines 13-15
+          ms = max(ms, be);
+          --total;
+          F.set(bs, be);
+        } else {  // lines 17-24 (total > 0 here)
+          if ((F.has >> bs) & 1) rec = max(rec, be) + de[nd_szi(w)];
+          if (!F.split(bs, be, w)) lslice[bs * 32 + lane] = be;  // removed leaf keeps its slice end
+        }
+      }
+      pops += __popc(F.live);  // the remaining frontier nodes are popped and dropped (heap empties)
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+        if ((F.live >> s) & 1) {
+          const int sz = nd_sz(ninfo[F.node(s)]);
+          for (int q = s; q < s + sz; ++q) lslice[q * 32 + lane] = F.e[s];
+        }
+    }
+    events += warp_sum_ll(pops);
+    // ---- H5: k* = argmin (makespan_k, k)
+    const int m = __reduce_min_sync(FULL, ms);
+    const int kw = (int)__reduce_min_sync(FULL, (unsigned)(ms == m ? k : INT_MAX));
+    __syncwarp();
+    if (m < bestms) {
+      bestms = m;
+      bestk = kw;
+      const int wl = kw - kb;
+      for (int j = lane; j < n; j += 32) bestnode[j] = recnode[j * 32 + wl];
+      if (lane < S) bsend[lane] = lslice[lane * 32 + wl];
+    }
+    __syncwarp();
+  }
+  R.events = events;
+  R.alloc_index = bestk;
+  R.makespan_phase2 = bestms;
+  ms2 = bestms;
+
+  // ---- H6/H7: node lists of k*, phase 3, replay, guard
+  uint16_t* nlist = (uint16_t*)scratch;
+  int msF = ms2;
+  bool have_starts = false;
+  build_node_lists<NC>(n, bestk, lent, ltask, loff, bestnode, nlist, ncnt, su, lane);
+  if (refine) {
+    if (lane < S) send[lane] = bsend[lane];
+    __syncwarp();
+    int mv, sw, it;
+    long long ev;
+    refine_warp<NC>(n, T, su, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
+    R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
+    int msR = 0;
+    if (lane == 0) msR = replay_one<NC>(n, T, su, nlist, ncnt, lp, start, cur, ninfo, cr, de);
+    msR = __shfl_sync(FULL, msR, 0);
+    __syncwarp();
+    if (!(P.flags & FAR_NO_GUARD) && msR > ms2) {
+      R.reverted = 1;  // keep-best guard: return the phase-2 schedule
+      build_node_lists<NC>(n, bestk, lent, ltask, loff, bestnode, nlist, ncnt, su, lane);
+    } else {
+      msF = msR;
+      have_starts = true;
+    }
+  }
+  if (want_sched && !have_starts) {
+    if (lane == 0) replay_one<NC>(n, T, su, nlist, ncnt, lp, start, cur, ninfo, cr, de);  // fixpoint = phase 2
+    __syncwarp();
+  }
+  R.makespan = msF;
+  if (want_sched) {
+    far_task_slot* out = P.sched + inst * (int64_t)n;
+    for (int j = lane; j < n; j += 32) {
+      far_task_slot s;
+      s.node = cur[j];
+      s.size_used = (uint8_t)size_of<NC>(su[j]);
+      s.pad[0] = s.pad[1] = 0;
+      s.start = start[j];
+      out[j] = s;
+    }
+  }
+  if (lane == 0) {
+    P.makespan[inst] = R.makespan;
+    if (P.res) P.res[inst] = R;
+  }
+  __syncwarp();
+}
+
+__constant__ uint32_t c_nodes3[7] = {
+    Tree<3>::node[0], Tree<3>::node[1], Tree<3>::node[2], Tree<3>::node[3],
+    Tree<3>::node[4], Tree<3>::node[5], Tree<3>::node[6]};
+__constant__ uint32_t c_nodes5[13] = {
+    Tree<5>::node[0], Tree<5>::node[1], Tree<5>::node[2],  Tree<5>::node[3],  Tree<5>::node[4],
+    Tree<5>::node[5], Tree<5>::node[6], Tree<5>::node[7],  Tree<5>::node[8],  Tree<5>::node[9],
+    Tree<5>::node[10], Tree<5>::node[11], Tree<5>::node[12]};
+
+template <int NC>
+__global__ void __launch_bounds__(128) far_solve_kernel(KParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint32_t ninfo[16];
+  __shared__ int cr[8], de[8];
+  constexpr int NN = Tree<NC>::NN;
+  if (threadIdx.x < NN) ninfo[threadIdx.x] = (NC == 3) ? c_nodes3[threadIdx.x] : c_nodes5[threadIdx.x];
+  if (threadIdx.x < 8) {
+    cr[threadIdx.x] = P.cr[threadIdx.x];
+    de[threadIdx.x] = P.de[threadIdx.x];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Layout L = make_layout(P.n, NC, Tree<NC>::S, NN);
+  unsigned char* wsm = smem + (size_t)warp * L.bytes;
+  for (;;) {
+    unsigned long long inst = 0;
+    if (lane == 0) inst = atomicAdd(P.counter, 1ull);
+    inst = __shfl_sync(FULL, inst, 0);
+    if ((int64_t)inst >= P.I) break;
+    solve_instance<NC>(P, (int64_t)inst, wsm, L, ninfo, cr, de, lane);
+    __syncwarp();
+  }
+}
+
+}  // namespace farb

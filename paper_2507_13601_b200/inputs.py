@@ -152,18 +152,19 @@ def _chunked(fn, n, nc, count, seed, tag, start):
     return out
 
 
-def synthetic_parallel(profile, n, count, seed, workers=None, **kw) -> np.ndarray:
+def synthetic_parallel(profile, n, count, seed, workers=None, start=0, **kw) -> np.ndarray:
     """Same table as :func:`synthetic`, generated chunk-parallel in a process pool."""
     import concurrent.futures as cf
     workers = workers or min(32, os.cpu_count() or 1)
     if count <= 4 * CHUNK or workers <= 1:
-        return synthetic(profile, n, count, seed, **kw)
+        return synthetic(profile, n, count, seed, start=start, **kw)
     sizes = SIZES[profile]
     out = np.empty((count, n, len(sizes)), dtype=np.int32)
     step = CHUNK * max(1, (count // CHUNK) // (workers * 4) or 1)
     starts = list(range(0, count, step))
     with cf.ProcessPoolExecutor(workers) as ex:
-        futs = {ex.submit(synthetic, profile, n, min(step, count - s), seed, start=s, **kw): s for s in starts}
+        futs = {ex.submit(synthetic, profile, n, min(step, count - s), seed, start=start + s, **kw): s
+                for s in starts}
         for f in cf.as_completed(futs):
             s = futs[f]
             blk = f.result()

@@ -1,0 +1,151 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by
+element, on seeded inputs.  Integer work -> bit-exact on every field."""
+import numpy as np
+import pytest
+
+from paper_2507_13601_b200 import far, inputs
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("makespan", "makespan_phase2", "alloc_index", "family_size", "moves", "swaps", "iterations", "reverted",
+          "evals", "events")
+
+
+@pytest.fixture(scope="module")
+def torch_dev():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch, torch.device("cuda:0")
+
+
+def run_gpu(torch_dev, profile, costs, tab, **kw):
+    torch, dev = torch_dev
+    F = far.Far(profile, costs)
+    d = torch.from_numpy(np.ascontiguousarray(tab)).to(dev)
+    ms, sd, rs = F.solve_many(d, **kw)
+    torch.cuda.synchronize()
+    F.sync()
+    return ms.cpu().numpy(), far.slots_np(sd), far.results_np(rs)
+
+
+def check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=0, max_iterations=100, ppm=0, full=True):
+    oflags = flags & (O.NO_REFINE | O.NO_GUARD | O.ZERO_RECONFIG)
+    oms, ores = O.far_many(profile, costs, tab, max_iterations=max_iterations, min_improvement_ppm=ppm, flags=oflags)
+    bad = np.nonzero(ms != oms)[0]
+    assert len(bad) == 0, f"makespan mismatch at {bad[:10]}: gpu {ms[bad[:5]]} oracle {oms[bad[:5]]}"
+    for k in FIELDS:
+        assert (res[k] == ores[k]).all(), f"{k} mismatch at {np.nonzero(res[k] != ores[k])[0][:10]}"
+    if full and slots is not None:
+        for i in range(tab.shape[0]):
+            o = O.far(profile, costs, tab[i], max_iterations=max_iterations, min_improvement_ppm=ppm, flags=oflags)
+            os_ = o["slots"]
+            assert (slots[i]["node"] == os_["node"]).all(), f"node mismatch instance {i}"
+            assert (slots[i]["size_used"] == os_["size_used"]).all(), f"size_used mismatch instance {i}"
+            assert (slots[i]["start"] == os_["start"]).all(), f"start mismatch instance {i}"
+
+
+@pytest.mark.parametrize("wname,count", [("M1", 2000), ("M2", 2000), ("M3", 1000)])
+def test_workload_samples_bitexact(O, torch_dev, wname, count):
+    w = inputs.WORKLOADS[wname]
+    tab = w.table(count=count)
+    ms, slots, res = run_gpu(torch_dev, w.profile, w.costs(), tab)
+    check_against_oracle(O, w.profile, w.costs(), tab, ms, slots, res, full=True)
+
+
+@pytest.mark.parametrize("profile", ["A30", "A100", "H100"])
+@pytest.mark.parametrize("n", [0, 1, 2, 7, 31, 32, 33, 64, 65])
+def test_ragged_sizes(O, torch_dev, profile, n):
+    costs = inputs.reconfig_costs(profile)
+    tab = inputs.synthetic(profile, n, 97, 1000 + n)
+    ms, slots, res = run_gpu(torch_dev, profile, costs, tab)
+    check_against_oracle(O, profile, costs, tab, ms, slots, res)
+
+
+@pytest.mark.parametrize("profile", ["A30", "A100"])
+@pytest.mark.parametrize("gen", ["ties", "uniform", "narrow", "poor", "good"])
+def test_tie_and_nonmonotone_inputs(O, torch_dev, profile, gen):
+    n = 24
+    if gen == "ties":
+        tab = inputs.small_ties(profile, n, 300, 5)
+    elif gen == "uniform":
+        tab = inputs.uniform_random(profile, n, 300, 6)       # non-monotone runtimes
+    elif gen == "narrow":
+        tab = inputs.synthetic(profile, n, 300, 7, times="narrow")
+    else:
+        tab = inputs.synthetic(profile, n, 300, 8, scaling=gen)
+    for costs in (inputs.reconfig_costs(profile), inputs.reconfig_costs(profile, zero=True)):
+        ms, slots, res = run_gpu(torch_dev, profile, costs, tab)
+        check_against_oracle(O, profile, costs, tab, ms, slots, res)
+
+
+@pytest.mark.parametrize("flags,max_it,ppm", [(far.NO_REFINE, 100, 0), (far.NO_GUARD, 100, 0),
+                                               (far.ZERO_RECONFIG, 100, 0), (0, 0, 0), (0, 1, 0), (0, 3, 0),
+                                               (0, 100, 20000)])
+def test_options(O, torch_dev, flags, max_it, ppm):
+    profile = "A100"
+    costs = inputs.reconfig_costs(profile)
+    tab = inputs.synthetic(profile, 20, 400, 21)
+    ms, slots, res = run_gpu(torch_dev, profile, costs, tab, flags=flags, max_iterations=max_it,
+                             min_improvement_ppm=ppm)
+    check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=flags, max_iterations=max_it, ppm=ppm)
+
+
+@pytest.mark.parametrize("n", [128, 256, 1024])
+def test_large_n(O, torch_dev, n):
+    profile = "A100"
+    costs = inputs.reconfig_costs(profile)
+    tab = inputs.synthetic(profile, n, 24 if n < 1024 else 3, 31, times="narrow" if n == 1024 else "wide")
+    if n == 1024:
+        tab = np.minimum(tab, 900)  # keep the makespan bound < 2^30
+    ms, slots, res = run_gpu(torch_dev, profile, costs, tab)
+    check_against_oracle(O, profile, costs, tab, ms, slots, res)
+
+
+def test_input_errors_flagged(torch_dev):
+    torch, dev = torch_dev
+    tab = inputs.synthetic("A30", 5, 4, 3)
+    tab[1, 2, 1] = 0                      # t < 1
+    tab[2, :, :] = 1 << 29                # makespan bound
+    F = far.Far("A30")
+    ms, sd, rs = F.solve_many(torch.from_numpy(tab).to(dev))
+    torch.cuda.synchronize()
+    r = far.results_np(rs)
+    assert ms.cpu().numpy().tolist()[1:3] == [-1, -1]
+    assert r["status"].tolist() == [0, 3, 3, 0]
+    with pytest.raises(far.FarError) as e:
+        F.sync()
+    assert e.value.status == 3
+    F.sync()  # flag cleared
+
+
+def test_schedule_batch_and_local_search(O, torch_dev):
+    for profile in ("A30", "A100", "H100"):
+        costs = inputs.reconfig_costs(profile)
+        F = far.Far(profile, costs)
+        for t in inputs.synthetic(profile, 19, 60, 55):
+            s, r = F.schedule_batch(t)
+            o = O.far(profile, costs, t, flags=O.NO_REFINE)
+            assert (s["node"] == o["slots"]["node"]).all() and (s["start"] == o["slots"]["start"]).all()
+            assert r["makespan"] == o["result"]["makespan"] and r["alloc_index"] == o["result"]["alloc_index"]
+            # phase 3 on the phase-2 schedule == the oracle's refine
+            s2, r2 = F.local_search(t, s, makespan_phase2=int(r["makespan"]))
+            oslots = np.zeros(len(s), O.SLOT_DT)
+            oslots["node"], oslots["size_used"], oslots["start"] = s["node"], s["size_used"], s["start"]
+            q = O.refine(profile, costs, t, oslots, int(r["makespan"]))
+            assert r2["makespan"] == q["result"]["makespan"]
+            for k in ("moves", "swaps", "evals", "iterations", "reverted"):
+                assert r2[k] == q["result"][k], k
+            assert (s2["node"] == q["slots"]["node"]).all() and (s2["start"] == q["slots"]["start"]).all()
+            # and it equals the full pipeline
+            full = O.far(profile, costs, t)
+            assert r2["makespan"] == full["result"]["makespan"]
+
+
+def test_host_pipeline_matches_device(torch_dev):
+    w = inputs.WORKLOADS["M3"]
+    tab = w.table(count=5000)
+    ms, slots, res = run_gpu(torch_dev, w.profile, w.costs(), tab)
+    F = far.Far(w.profile, w.costs())
+    hms, hsl, hres = F.solve_many_host(tab)
+    assert (hms == ms).all() and (hsl["start"] == slots["start"]).all() and (hres["evals"] == res["evals"]).all()
