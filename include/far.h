@@ -146,18 +146,23 @@ far_status far_solve_many_host(far_ctx *ctx, const int32_t *h_times, int64_t I, 
                                int32_t *h_makespan, far_task_slot *h_sched, far_result *h_res);
 
 /* Multi-batch concatenation (§4) of S independent streams of B batches each,
- * DEVICE pointers, asynchronous.  Each batch is FAR-scheduled (phases 1-3), odd batches
- * are reversed, and the batches are folded left to right with the seam offset
- * rule and seam move/swap of DESIGN.md "Streams".
+ * DEVICE pointers, asynchronous on cuda_stream.  Every batch is FAR-scheduled (phases 1-3),
+ * odd batches are reversed, and each stream is folded left to right with the seam
+ * offset rule and the seam move/swap of DESIGN.md §9.
  *   d_times           int32 [S][B][n][nsizes]
- *   d_stream_makespan int64 [S]     total makespan of each stream
+ *   d_stream_makespan int64 [S][2]  {stream makespan (last task end), trivial-concatenation
+ *                                     makespan}
  *   d_offsets         int64 [S][B]  absolute start offset of each batch
- *   d_batch_res       far_result [S][B] (or NULL): the per-batch FAR reports
- *   d_seam            int32 [S][B][4] (or NULL): per batch {trivial offset delta, seam moves,
- *                     seam swaps, reversed flag} */
+ *   d_sched           far_task_slot [S][B][n] (or NULL): node, size used and start RELATIVE to
+ *                     the batch offset in the batch's final (possibly reversed) timeline
+ *   d_batch_res       far_result [S][B] (or NULL): each batch's FAR report
+ *   d_seam            int32 [S][B][4] (or NULL): {reversed, seam moves, seam swaps, reused instances}
+ * The ctx workspace holds the intermediate per-batch schedules: calls on one ctx must be ordered
+ * on one stream.  A stream whose placed-event window (256 events) overflows raises FAR_E_TOO_LARGE
+ * at the next far_sync. */
 far_status far_concat_streams(far_ctx *ctx, const int32_t *d_times, int64_t S, int32_t B, int32_t n,
                               const far_opts *opts, int64_t *d_stream_makespan, int64_t *d_offsets,
-                              far_result *d_batch_res, int32_t *d_seam, void *cuda_stream);
+                              far_task_slot *d_sched, far_result *d_batch_res, int32_t *d_seam, void *cuda_stream);
 
 #ifdef __cplusplus
 }

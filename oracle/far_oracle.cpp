@@ -188,8 +188,12 @@ i64 dur(const Problem& P, const Sched& S, int j) { return P.time(j, S.size_used[
 //   mode ALLOC : alloc given; groups by size, LPT (lines 1-2)
 //   mode LISTS : lists given (per node, in order) with size_used per task
 // ---------------------------------------------------------------------------
+//   full_lifecycle : also destroy every node with tasks when it is dropped (multi-batch
+//                    lifecycle timeline); the single-batch result never
+//                    includes these final destroys (R12).
 Sched run_event_loop(const Problem& P, const std::vector<int>* alloc,
-                     const std::vector<std::vector<int>>* lists, const std::vector<int>* size_used_in) {
+                     const std::vector<std::vector<int>>* lists, const std::vector<int>* size_used_in,
+                     bool full_lifecycle = false) {
   const Model& m = P.m;
   const int N = (int)m.node.size();
   Sched S;
@@ -269,6 +273,10 @@ Sched run_event_loop(const Problem& P, const std::vector<int>* alloc,
         heap.push({{end[ch], m.node[ch].lo}, ch});
       }
       (void)vs;
+    } else if (full_lifecycle && has_tasks[v]) {  // drop: final destroy of the lifecycle timeline
+      i64 ds = std::max(reconfig_end, end[v]);
+      reconfig_end = ds + P.c.de(m, v);
+      S.events.push_back({1, v, ds, P.c.de(m, v)});
     }
     // else: drop the instance (no tasks remain anywhere)
   }
@@ -432,6 +440,312 @@ Sched refine_and_replay(const Problem& P, const Sched& S2, i64 ms2, int max_it, 
   }
   return R;
 }
+
+
+// ===========================================================================
+// §4 Multi-batch concatenation under the readings R21-R25 of
+// DESIGN.md §9.  Times of a batch timeline are relative to the batch start;
+// the stream state holds absolute times.
+// ===========================================================================
+struct Life {  // one instance lifecycle inside a batch timeline
+  int node = -1;
+  i64 cs = 0, ce = 0;  // create  [cs, ce)
+  i64 ds = 0, de = 0;  // destroy [ds, de)
+  i64 first_task = 0, last_task = 0;
+};
+
+struct Timeline {
+  std::vector<i64> start;       // per task (relative)
+  std::vector<Life> life;       // lifecycles, ordered by node id
+  i64 E = 0;                    // end of the last event (relative)
+  i64 task_end = 0;             // last task finish (relative)
+};
+
+// Full-lifecycle timeline of a batch tree (R22).  forward: the O7 replay where every
+// node with tasks is also destroyed when dropped.  reversed: the same loop with
+// t_create <-> t_destroy swapped, mirrored about its last event end E, so each mirrored
+// destroy has the create duration and vice versa (tasks of a node run in reverse order).
+Timeline batch_timeline(const Problem& P, const Sched& S, bool reversed) {
+  const Model& m = P.m;
+  Problem Q = P;
+  if (reversed) std::swap(Q.c.create, Q.c.destroy);
+  Sched R = run_event_loop(Q, nullptr, &S.list, &S.size_used, /*full_lifecycle=*/true);
+  Timeline T;
+  i64 E = 0;
+  for (const orc_event& e : R.events) E = std::max(E, e.start + e.dur);
+  for (int j = 0; j < P.n; ++j) E = std::max(E, R.start[j] + dur(P, S, j));
+  T.E = E;
+  T.start.assign(P.n, 0);
+  for (int j = 0; j < P.n; ++j) T.start[j] = reversed ? E - (R.start[j] + dur(P, S, j)) : R.start[j];
+  for (int j = 0; j < P.n; ++j) T.task_end = std::max(T.task_end, T.start[j] + dur(P, S, j));
+  for (int v = 0; v < (int)m.node.size(); ++v) {
+    if (S.list[v].empty()) continue;
+    Life L;
+    L.node = v;
+    for (const orc_event& e : R.events) {
+      if (e.node != v) continue;
+      i64 a = e.start, b = e.start + e.dur;
+      if (reversed) { i64 a2 = E - b, b2 = E - a; a = a2; b = b2; }
+      const bool is_create = reversed ? (e.kind == 1) : (e.kind == 0);
+      if (is_create) { L.cs = a; L.ce = b; } else { L.ds = a; L.de = b; }
+    }
+    L.first_task = std::numeric_limits<i64>::max();
+    L.last_task = std::numeric_limits<i64>::min();
+    for (int j : S.list[v]) {
+      L.first_task = std::min(L.first_task, T.start[j]);
+      L.last_task = std::max(L.last_task, T.start[j] + dur(P, S, j));
+    }
+    T.life.push_back(L);
+  }
+  return T;
+}
+
+struct LifeAbs {
+  int node;
+  bool has_create;
+  i64 cs, ce, ds, de;        // absolute
+  i64 last_task;
+  int destroy_ev;            // index into StreamState::events
+};
+struct EvAbs { i64 s, e; int kind, node; bool alive; };
+struct TaskAbs { i64 s, e; int node, life; };
+
+struct StreamState {
+  std::vector<i64> tail;       // per slice: end of the last lifecycle on the slice (0 if none)
+  std::vector<int> tail_life;  // per slice: that lifecycle (-1 if none)
+  std::vector<LifeAbs> lives;
+  std::vector<EvAbs> events;
+  std::vector<TaskAbs> tasks;
+  i64 last_offset = 0;
+};
+
+struct SeamEval {
+  i64 O = 0, end = 0;
+  std::vector<bool> reuse;   // per node
+  std::vector<i64> gap;      // per slice
+};
+
+// Seam offset (R23): the least O >= max(previous offset, 0) such that (i) on every slice
+// B_k's first lifecycle starts after the last placed lifecycle ends, (ii) with the
+// destroy/create pair elided where the last placed instance on a node's slices is that
+// node and B_k's first instance there is the same node (then task times bound), and
+// (iii) B_k's non-elided reconfiguration events overlap no placed event.
+SeamEval seam_offset(const Model& m, const StreamState& st, const Timeline& T) {
+  const int N = (int)m.node.size();
+  SeamEval R;
+  R.reuse.assign(N, false);
+  std::vector<int> first(m.slices, -1);  // index into T.life of the first lifecycle on s
+  for (int q = 0; q < (int)T.life.size(); ++q) {
+    const TreeNode& nd = m.node[T.life[q].node];
+    for (int s = nd.lo; s < nd.hi; ++s)
+      if (first[s] < 0 || T.life[q].cs < T.life[first[s]].cs) first[s] = q;
+  }
+  for (const Life& L : T.life) {
+    const TreeNode& nd = m.node[L.node];
+    bool ok = true;
+    for (int s = nd.lo; s < nd.hi && ok; ++s) {
+      ok = first[s] >= 0 && T.life[first[s]].node == L.node && st.tail_life[s] >= 0 &&
+           st.lives[st.tail_life[s]].node == L.node;
+    }
+    R.reuse[L.node] = ok;
+  }
+  std::vector<i64> bound(m.slices, 0);
+  i64 O = std::max<i64>(st.last_offset, 0);
+  for (int s = 0; s < m.slices; ++s) {
+    if (first[s] < 0) continue;
+    const Life& L = T.life[first[s]];
+    bound[s] = R.reuse[L.node] ? st.lives[st.tail_life[s]].last_task - L.first_task : st.tail[s] - L.cs;
+    O = std::max(O, bound[s]);
+  }
+  // (iii): push O past conflicting placed events until none conflicts
+  std::vector<std::pair<i64, i64>> mine;
+  for (const Life& L : T.life) {
+    if (!R.reuse[L.node]) mine.push_back({L.cs, L.ce});
+    mine.push_back({L.ds, L.de});
+  }
+  std::vector<bool> skip(st.events.size(), false);
+  for (int s = 0; s < m.slices; ++s)
+    if (first[s] >= 0 && R.reuse[T.life[first[s]].node]) skip[st.lives[st.tail_life[s]].destroy_ev] = true;
+  for (;;) {
+    i64 push = O;
+    for (auto& e : mine)
+      for (size_t p = 0; p < st.events.size(); ++p) {
+        const EvAbs& P = st.events[p];
+        if (!P.alive || skip[p]) continue;
+        if (e.first + O < P.e && P.s < e.second + O) push = std::max(push, P.e - e.first);
+      }
+    if (push == O) break;
+    O = push;
+  }
+  R.O = O;
+  R.end = O + T.E;
+  R.gap.assign(m.slices, 0);
+  for (int s = 0; s < m.slices; ++s) {
+    i64 g = first[s] >= 0 ? O - bound[s] : O + T.E - st.tail[s];
+    R.gap[s] = std::max<i64>(g, 0);
+  }
+  return R;
+}
+
+void place_batch(const Problem& P, const Sched& S, StreamState& st, const Timeline& T, const SeamEval& ev) {
+  const Model& m = P.m;
+  const i64 O = ev.O;
+  std::vector<int> life_id(m.node.size(), -1);
+  for (const Life& L : T.life) {
+    const TreeNode& nd = m.node[L.node];
+    int lid;
+    if (ev.reuse[L.node]) {
+      lid = st.tail_life[nd.lo];
+      st.events[st.lives[lid].destroy_ev].alive = false;  // elided destroy of the previous batch
+    } else {
+      lid = (int)st.lives.size();
+      st.lives.push_back({L.node, true, O + L.cs, O + L.ce, 0, 0, 0, -1});
+      st.events.push_back({O + L.cs, O + L.ce, 0, L.node, true});
+    }
+    st.lives[lid].ds = O + L.ds;
+    st.lives[lid].de = O + L.de;
+    st.lives[lid].last_task = O + L.last_task;
+    st.lives[lid].destroy_ev = (int)st.events.size();
+    st.events.push_back({O + L.ds, O + L.de, 1, L.node, true});
+    life_id[L.node] = lid;
+  }
+  for (int j = 0; j < P.n; ++j)
+    st.tasks.push_back({O + T.start[j], O + T.start[j] + dur(P, S, j), S.node[j], life_id[S.node[j]]});
+  for (int s = 0; s < m.slices; ++s) {  // the last lifecycle on each slice is the one ending last
+    int best = -1;
+    for (const Life& L : T.life) {
+      const TreeNode& nd = m.node[L.node];
+      if (s >= nd.lo && s < nd.hi && (best < 0 || L.de > T.life[best].de)) best = (int)(&L - &T.life[0]);
+    }
+    if (best >= 0) {
+      st.tail[s] = O + T.life[best].de;
+      st.tail_life[s] = life_id[T.life[best].node];
+    }
+  }
+  st.last_offset = O;
+}
+
+// Seam move/swap (R24): Alg. 2's operations on a reversed B_k with the
+// inter-batch idle time of a node's slices as the margin; each candidate is evaluated by
+// recomputing the mirrored timeline and the seam, and kept only if B_k ends earlier.
+struct SeamStats { int moves = 0, swaps = 0; i64 evals = 0; };
+
+SeamStats seam_refine(const Problem& P, Sched& S, const StreamState& st, int max_it) {
+  const Model& m = P.m;
+  const int N = (int)m.node.size();
+  SeamStats stt;
+  auto eval = [&](const Sched& X) { return seam_offset(m, st, batch_timeline(P, X, true)); };
+  SeamEval cur = eval(S);
+  std::vector<int> leaf_of(m.slices, -1);
+  for (int v = 0; v < N; ++v)
+    if (m.node[v].children.empty()) leaf_of[m.node[v].lo] = v;
+  for (int it = 0; it < max_it; ++it) {
+    std::vector<bool> touched(m.slices, false);  // slices used by the current B_k
+    for (int v = 0; v < N; ++v)
+      if (!S.list[v].empty())
+        for (int s = m.node[v].lo; s < m.node[v].hi; ++s) touched[s] = true;
+    std::deque<int> Q;
+    std::vector<bool> opened(N, false);
+    for (int s = 0; s < m.slices; ++s)
+      if (touched[s] && cur.gap[s] == 0) { Q.push_back(leaf_of[s]); opened[leaf_of[s]] = true; }
+    if (Q.empty()) break;
+    bool accepted = false, stop = false;
+    while (!Q.empty() && !accepted) {
+      const int I = Q.front();
+      Q.pop_front();
+      if (I == 0) { stop = true; break; }
+      auto slack = [&](int u) {
+        i64 g = std::numeric_limits<i64>::max();
+        for (int s = m.node[u].lo; s < m.node[u].hi; ++s) g = std::min(g, cur.gap[s]);
+        return g;
+      };
+      int A = -1;
+      i64 sA = 0;
+      for (int u = 0; u < N; ++u) {  // the same-size node with the most idle time (ties -> lower slice)
+        if (u == I || m.node[u].size() != m.node[I].size()) continue;
+        i64 g = slack(u);
+        if (A < 0 || g > sA) { A = u; sA = g; }
+      }
+      if (A >= 0 && sA > 0) {
+        const i64 marg = sA;
+        stt.evals += (i64)S.list[I].size();
+        int T = -1;
+        i64 bd = 0;
+        for (int j : S.list[I]) {
+          i64 t = dur(P, S, j);
+          if (!(t < marg)) continue;
+          i64 d = std::llabs(2 * t - marg);
+          if (T < 0 || d < bd || (d == bd && j < T)) { T = j; bd = d; }
+        }
+        if (T >= 0) {
+          Sched X = S;
+          X.list[I].erase(std::find(X.list[I].begin(), X.list[I].end(), T));
+          X.node[T] = A;
+          insert_ordered(P, X, X.list[A], T);
+          SeamEval e2 = eval(X);
+          if (e2.end < cur.end) { S = X; cur = e2; stt.moves++; accepted = true; }
+        }
+        if (!accepted) {
+          stt.evals += (i64)S.list[I].size() * (i64)S.list[A].size();
+          int K = -1, J = -1;
+          i64 bd2 = 0;
+          for (int k : S.list[I])
+            for (int j : S.list[A]) {
+              i64 delta = dur(P, S, k) - dur(P, S, j);
+              if (!(0 < delta && delta < marg)) continue;
+              i64 d = std::llabs(2 * delta - marg);
+              if (K < 0 || d < bd2 || (d == bd2 && (k < K || (k == K && j < J)))) { K = k; J = j; bd2 = d; }
+            }
+          if (K >= 0) {
+            Sched X = S;
+            X.list[I].erase(std::find(X.list[I].begin(), X.list[I].end(), K));
+            X.list[A].erase(std::find(X.list[A].begin(), X.list[A].end(), J));
+            X.node[K] = A;
+            X.node[J] = I;
+            insert_ordered(P, X, X.list[A], K);
+            insert_ordered(P, X, X.list[I], J);
+            SeamEval e2 = eval(X);
+            if (e2.end < cur.end) { S = X; cur = e2; stt.swaps++; accepted = true; }
+          }
+        }
+      }
+      if (!accepted) {
+        const int par = m.node[I].parent;
+        if (par >= 0 && !opened[par]) { opened[par] = true; Q.push_back(par); }
+      }
+    }
+    if (stop || !accepted) break;
+  }
+  return stt;
+}
+
+// Stream validator: constraints 1-3 across the concatenated timeline.
+int validate_stream(const Model& m, const StreamState& st) {
+  int bad = 0;
+  auto overlap = [&](int u, int v) { return m.node[u].lo < m.node[v].hi && m.node[v].lo < m.node[u].hi; };
+  const size_t nt = st.tasks.size();
+  for (size_t a = 0; a < nt; ++a)
+    for (size_t b = a + 1; b < nt; ++b)
+      if (overlap(st.tasks[a].node, st.tasks[b].node) && st.tasks[a].s < st.tasks[b].e &&
+          st.tasks[b].s < st.tasks[a].e)
+        bad++;
+  for (size_t a = 0; a < st.events.size(); ++a) {
+    if (!st.events[a].alive) continue;
+    for (size_t b = a + 1; b < st.events.size(); ++b)
+      if (st.events[b].alive && st.events[a].s < st.events[b].e && st.events[b].s < st.events[a].e) bad++;
+  }
+  for (const TaskAbs& t : st.tasks) {
+    const LifeAbs& L = st.lives[t.life];
+    if (t.s < L.ce || t.e > L.ds) bad++;
+  }
+  for (size_t a = 0; a < st.lives.size(); ++a)
+    for (size_t b = a + 1; b < st.lives.size(); ++b) {
+      const LifeAbs &A = st.lives[a], &B = st.lives[b];
+      if (overlap(A.node, B.node) && A.cs < B.de && B.cs < A.de) bad++;
+    }
+  return bad;
+}
+
 
 }  // namespace
 
@@ -740,3 +1054,100 @@ int orc_far_many(int profile, const int32_t* costs, const int32_t* times, int64_
 }
 
 }  // extern "C"
+
+extern "C" int orc_stream(int profile, const int32_t* costs, const int32_t* times, int B, int n,
+                          int32_t max_iterations, int32_t ppm, uint32_t flags, int64_t* out2, int64_t* offsets,
+                          int32_t* seam, orc_slot* slots, orc_result* batch_res, int32_t* violations) {
+  const int nc = orc_num_sizes(profile);
+  if (nc < 0) return nc;
+  if (B < 0 || n < 0) return -1;
+  std::vector<Problem> Pb(B);
+  std::vector<Sched> fin(B);
+  // each batch: FAR phases 1-3
+  for (int k = 0; k < B; ++k) {
+    int rc = load_problem(profile, costs, times + (size_t)k * n * nc, n, (flags & ORC_ZERO_RECONFIG) != 0, Pb[k]);
+    if (rc) return rc;
+    const Problem& P = Pb[k];
+    orc_result r{};
+    auto fam = allocation_family(P);
+    r.family_size = (int)fam.size();
+    Sched best;
+    int kbest = -1;
+    for (size_t q = 0; q < fam.size(); ++q) {
+      Sched S = schedule_allocation(P, fam[q]);
+      r.events += S.pops;
+      if (kbest < 0 || S.makespan < best.makespan) { best = S; kbest = (int)q; }
+    }
+    if (n == 0) best = Sched{}, best.list.assign(P.m.node.size(), {});
+    r.alloc_index = kbest < 0 ? 0 : kbest;
+    r.makespan_phase2 = best.makespan;
+    Sched f = best;
+    if (!(flags & ORC_NO_REFINE) && n > 0) f = refine_and_replay(P, best, best.makespan, max_iterations, ppm, flags, &r);
+    r.makespan = f.makespan;
+    fin[k] = f;
+    if (batch_res) batch_res[k] = r;
+  }
+  // trivial concatenation (R25): forward batches one after another
+  i64 triv_ms = 0, prev_end = 0;
+  for (int k = 0; k < B; ++k) {
+    Timeline T = batch_timeline(Pb[k], fin[k], false);
+    const i64 O = k == 0 ? 0 : prev_end;
+    triv_ms = std::max(triv_ms, O + T.task_end);
+    prev_end = O + T.E;
+  }
+  // reversal + seam offset + seam move/swap fold (R21-R24)
+  StreamState st;
+  const Model& m = Pb.empty() ? make_model(profile) : Pb[0].m;
+  Model mm = make_model(profile);
+  st.tail.assign(mm.slices, 0);
+  st.tail_life.assign(mm.slices, -1);
+  i64 ms = 0;
+  for (int k = 0; k < B; ++k) {
+    const bool rev = (k % 2) == 1;
+    Sched S = fin[k];
+    SeamStats ss;
+    if (rev && k > 0) ss = seam_refine(Pb[k], S, st, max_iterations);
+    Timeline T = batch_timeline(Pb[k], S, rev);
+    SeamEval ev = seam_offset(mm, st, T);
+    int reused = 0;
+    for (bool b : ev.reuse) reused += b;
+    place_batch(Pb[k], S, st, T, ev);
+    ms = std::max(ms, ev.O + T.task_end);
+    if (offsets) offsets[k] = ev.O;
+    if (seam) {
+      seam[4 * k + 0] = rev;
+      seam[4 * k + 1] = ss.moves;
+      seam[4 * k + 2] = ss.swaps;
+      seam[4 * k + 3] = reused;
+    }
+    if (slots)
+      for (int j = 0; j < n; ++j) slots[(size_t)k * n + j] = {S.node[j], S.size_used[j], T.start[j]};
+  }
+  (void)m;
+  if (out2) { out2[0] = ms; out2[1] = triv_ms; }
+  if (violations) *violations = validate_stream(mm, st);
+  return 0;
+}
+
+// Test entry (tests/test_oracle_stream.py): the seam offset of a batch whose first use of
+// slice s starts at first[s] (first[s] < 0: slice unused), after placed lifecycles ending at
+// tail[s], with zero-length reconfiguration events and no reuse (SPEC.md:345-350 examples).
+extern "C" int64_t orc_seam_offset_simple(int profile, const int64_t* tail, const int64_t* first) {
+  Model m = make_model(profile);
+  if (!m.ok) return -2;
+  StreamState st;
+  st.tail.assign(tail, tail + m.slices);
+  st.tail_life.assign(m.slices, -1);
+  Timeline T;
+  for (int s = 0; s < m.slices; ++s) {
+    if (first[s] < 0) continue;
+    Life L;
+    for (int v = 0; v < (int)m.node.size(); ++v)
+      if (m.node[v].children.empty() && m.node[v].lo == s) L.node = v;
+    L.cs = L.ce = L.first_task = first[s];
+    L.ds = L.de = L.last_task = first[s] + 1;
+    T.life.push_back(L);
+    T.E = std::max(T.E, first[s] + 1);
+  }
+  return seam_offset(m, st, T).O;
+}

@@ -14,7 +14,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "liboracle.so")
-SOURCES = ["far_oracle.cpp", "far_oracle_stream.cpp"]
+SOURCES = ["far_oracle.cpp"]
 
 PROFILES = {"A30": 0, "A100": 1, "H100": 2}
 NO_REFINE, NO_GUARD, ZERO_RECONFIG = 1, 2, 4
@@ -79,12 +79,13 @@ def lib():
             ("orc_validate", [C.c_int, p, p, C.c_int, p, p, C.c_int32], C.c_int),
             ("orc_lower_bound", [C.c_int, p, C.c_int, p, p], C.c_int),
             ("orc_far_many", [C.c_int, p, p, C.c_int64, C.c_int, C.c_int32, C.c_int32, C.c_uint32, p, p], C.c_int),
+            ("orc_seam_offset_simple", [C.c_int, p, p], C.c_int64),
         ]:
             f = getattr(_lib, name)
             f.argtypes, f.restype = args, res
         if hasattr(_lib, "orc_stream"):
             _lib.orc_stream.argtypes = [C.c_int, p, p, C.c_int, C.c_int, C.c_int32, C.c_int32, C.c_uint32,
-                                        p, p, p, p]
+                                        p, p, p, p, p, p]
             _lib.orc_stream.restype = C.c_int
     return _lib
 
@@ -233,3 +234,22 @@ def far_many_parallel(profile, costs, times, workers=None, **kw):
             ms[p[0]:p[-1] + 1] = m
             res[p[0]:p[-1] + 1] = r
     return ms, res
+
+
+def stream(profile, costs, times, max_iterations=100, min_improvement_ppm=0, flags=0):
+    """§4 multi-batch fold over one stream: times [B][n][|C|].  Returns dict with makespan,
+    trivial makespan, offsets [B], seam [B][4] {reversed, moves, swaps, reused}, slots [B][n]
+    (batch-relative starts of the final timeline), per-batch results and the number of
+    violations of the concatenated timeline's validator."""
+    t = _times(times)
+    B, n = t.shape[0], t.shape[1]
+    out2 = np.zeros(2, np.int64)
+    offs = np.zeros(B, np.int64)
+    seam = np.zeros((B, 4), np.int32)
+    slots = np.zeros((B, n), SLOT_DT)
+    res = np.zeros(B, RESULT_DT)
+    viol = np.zeros(1, np.int32)
+    _check(lib().orc_stream(pid(profile), _ptr(_costs(costs)), _ptr(t), B, n, max_iterations, min_improvement_ppm,
+                            flags, _ptr(out2), _ptr(offs), _ptr(seam), _ptr(slots), _ptr(res), _ptr(viol)))
+    return {"makespan": int(out2[0]), "trivial": int(out2[1]), "offsets": offs, "seam": seam, "slots": slots,
+            "results": res, "violations": int(viol[0])}

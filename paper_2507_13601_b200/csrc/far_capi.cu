@@ -206,6 +206,7 @@ far_status far_sync(far_ctx* ctx) {
   CK(cudaMemcpy(&flag, ctx->d_errflag, sizeof(int), cudaMemcpyDeviceToHost));
   if (flag) {
     CK(cudaMemset(ctx->d_errflag, 0, sizeof(int)));
+    if (flag & 4) return fail(ctx, FAR_E_TOO_LARGE, "a stream overflowed its placed-event window");
     return fail(ctx, (flag & 1) ? FAR_E_BAD_TIME : FAR_E_INVALID_ARG,
                 (flag & 1) ? "an instance failed the input checks (t < 1 or makespan bound)"
                            : "an instance had an invalid input schedule");
@@ -350,8 +351,69 @@ far_status far_solve_many_host(far_ctx* ctx, const int32_t* h_times, int64_t I, 
 
 extern "C" far_status far_concat_streams(far_ctx* ctx, const int32_t* d_times, int64_t S, int32_t B, int32_t n,
                                          const far_opts* opts, int64_t* d_stream_makespan, int64_t* d_offsets,
-                                         far_result* d_batch_res, int32_t* d_seam, void* cuda_stream) {
-  (void)d_times; (void)S; (void)B; (void)n; (void)opts; (void)d_stream_makespan; (void)d_offsets;
-  (void)d_batch_res; (void)d_seam; (void)cuda_stream;
-  return fail(ctx, FAR_E_INVALID_ARG, "far_concat_streams: not built yet");
+                                         far_task_slot* d_sched, far_result* d_batch_res, int32_t* d_seam,
+                                         void* cuda_stream) {
+  if (!ctx) return FAR_E_INVALID_ARG;
+  if (S < 0 || B < 0 || n < 0) return fail(ctx, FAR_E_INVALID_ARG, "negative S, B or n");
+  if (n > MAXN) return fail(ctx, FAR_E_TOO_LARGE, "n > 1024");
+  if (S > 0 && B > 0 && (!d_stream_makespan || !d_offsets || (n > 0 && !d_times)))
+    return fail(ctx, FAR_E_INVALID_ARG, "null device pointer");
+  far_status st = check_opts(ctx, opts);
+  if (st) return st;
+  if ((st = ensure_device(ctx))) return st;
+  if (S == 0) return FAR_OK;
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  if (B == 0) {
+    CK(cudaMemsetAsync(d_stream_makespan, 0, S * 2 * sizeof(int64_t), stream));
+    return FAR_OK;
+  }
+  const int64_t IB = S * (int64_t)B;
+  auto a256 = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t bs = a256((size_t)IB * n * sizeof(far_task_slot)), br = a256((size_t)IB * sizeof(far_result)),
+               bm = a256((size_t)IB * 4);
+  if ((st = ensure_buf(ctx, bs + br + bm))) return st;
+  // 1) FAR phases 1-3 on every batch of every stream (data-parallel)
+  KParams P;
+  fill_params(ctx, opts, P);
+  P.flags &= ~(unsigned)FAR_NO_SCHEDULE;
+  P.times = d_times;
+  P.I = IB;
+  P.n = n;
+  P.sched = (far_task_slot*)ctx->d_buf;
+  P.res = d_batch_res ? d_batch_res : (far_result*)(ctx->d_buf + bs);
+  P.makespan = (int32_t*)(ctx->d_buf + bs + br);
+  P.mode = MODE_SOLVE;
+  if ((st = launch_solve(ctx, P, stream))) return st;
+  // 2) the per-stream fold (one warp per stream)
+  SParams Q;
+  memset(&Q, 0, sizeof(Q));
+  Q.times = d_times;
+  Q.sched = P.sched;
+  Q.S = S;
+  Q.B = B;
+  Q.n = n;
+  for (int c = 0; c < 8; ++c) {
+    Q.cr[c] = P.cr[c];
+    Q.de[c] = P.de[c];
+  }
+  Q.max_it = P.max_it;
+  Q.stream_ms = d_stream_makespan;
+  Q.offsets = d_offsets;
+  Q.out_sched = d_sched;
+  Q.seam = d_seam;
+  Q.errflag = ctx->d_errflag;
+  const bool a30 = ctx->nc == 3;
+  const SLayout L = make_slayout(n, ctx->nc, ctx->nn);
+  int warps = std::min(4, SMEM_MAX / std::max(1, L.bytes));
+  if (warps < 1) return fail(ctx, FAR_E_TOO_LARGE, "stream state does not fit in shared memory");
+  const size_t smem = (size_t)warps * L.bytes;
+  const void* fn = a30 ? (const void*)far_stream_kernel<3> : (const void*)far_stream_kernel<5>;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = (int)((S + warps - 1) / warps);
+  if (a30)
+    far_stream_kernel<3><<<grid, warps * 32, smem, stream>>>(Q);
+  else
+    far_stream_kernel<5><<<grid, warps * 32, smem, stream>>>(Q);
+  CK(cudaGetLastError());
+  return FAR_OK;
 }

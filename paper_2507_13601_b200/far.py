@@ -72,7 +72,7 @@ def lib():
             "far_local_search": ([p, p, i32, p, p, p], C.c_int),
             "far_solve_many": ([p, p, i64, i32, p, p, p, p, p], C.c_int),
             "far_solve_many_host": ([p, p, i64, i32, p, p, p, p], C.c_int),
-            "far_concat_streams": ([p, p, i64, i32, i32, p, p, p, p, p, p], C.c_int),
+            "far_concat_streams": ([p, p, i64, i32, i32, p, p, p, p, p, p, p], C.c_int),
         }
         for name, (a, r) in sig.items():
             f = getattr(L, name)
@@ -191,22 +191,25 @@ class Far:
                                               _np_ptr(rs)))
         return ms, sd, rs
 
-    def concat_streams(self, d_times, *, batch_res=True, seam=True, stream=None, **kw):
-        """d_times: int32 CUDA tensor [S][B][n][nsizes] -> (stream_makespan int64 [S],
-        offsets int64 [S][B], batch_res uint8 [S][B][56] | None, seam int32 [S][B][4] | None)."""
+    def concat_streams(self, d_times, *, sched=True, batch_res=True, seam=True, stream=None, **kw):
+        """d_times: int32 CUDA tensor [S][B][n][nsizes] -> (stream_makespan int64 [S][2],
+        offsets int64 [S][B], sched uint8 [S][B][n][8] | None, batch_res uint8 [S][B][56] | None,
+        seam int32 [S][B][4] | None)."""
         import torch
         assert d_times.is_cuda and d_times.dtype == torch.int32 and d_times.is_contiguous()
         S, B, n = d_times.shape[0], d_times.shape[1], d_times.shape[2]
         dev = d_times.device
-        sm = torch.empty(S, dtype=torch.int64, device=dev)
+        sm = torch.empty((S, 2), dtype=torch.int64, device=dev)
         off = torch.empty((S, B), dtype=torch.int64, device=dev)
+        sd = torch.empty((S, B, n, 8), dtype=torch.uint8, device=dev) if sched else None
         br = torch.empty((S, B, 56), dtype=torch.uint8, device=dev) if batch_res else None
         se = torch.empty((S, B, 4), dtype=torch.int32, device=dev) if seam else None
         st = stream if stream is not None else torch.cuda.current_stream(dev)
         o = _opts(**kw)
         self._check(lib().far_concat_streams(self._h, _t_ptr(d_times), S, B, n, C.byref(o), _t_ptr(sm),
-                                             _t_ptr(off), _t_ptr(br), _t_ptr(se), C.c_void_p(st.cuda_stream)))
-        return sm, off, br, se
+                                             _t_ptr(off), _t_ptr(sd), _t_ptr(br), _t_ptr(se),
+                                             C.c_void_p(st.cuda_stream)))
+        return sm, off, sd, br, se
 
 
 def slots_np(sd_tensor):

@@ -1,0 +1,73 @@
+"""GPU parity of the §4 multi-batch fold (far_concat_streams) against the oracle."""
+import numpy as np
+import pytest
+
+from paper_2507_13601_b200 import far, inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_dev():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch, torch.device("cuda:0")
+
+
+def run_streams(torch_dev, profile, costs, tab, **kw):
+    torch, dev = torch_dev
+    F = far.Far(profile, costs)
+    sm, off, sd, br, se = F.concat_streams(torch.from_numpy(np.ascontiguousarray(tab)).to(dev), **kw)
+    torch.cuda.synchronize()
+    F.sync()
+    return (sm.cpu().numpy(), off.cpu().numpy(), far.slots_np(sd), far.results_np(br), se.cpu().numpy())
+
+
+def check(O, profile, costs, tab, out, **kw):
+    sm, off, slots, res, seam = out
+    for s in range(tab.shape[0]):
+        o = O.stream(profile, costs, tab[s], **kw)
+        assert o["violations"] == 0
+        assert sm[s, 0] == o["makespan"] and sm[s, 1] == o["trivial"], f"stream {s} makespans"
+        assert (off[s] == o["offsets"]).all(), f"stream {s} offsets {np.nonzero(off[s] != o['offsets'])[0][:5]}"
+        assert (seam[s] == o["seam"]).all(), f"stream {s} seam info"
+        assert (slots[s]["node"] == o["slots"]["node"]).all(), f"stream {s} nodes"
+        assert (slots[s]["start"] == o["slots"]["start"]).all(), f"stream {s} starts"
+        for k in ("makespan", "alloc_index", "moves", "swaps", "evals", "events"):
+            assert (res[s][k] == o["results"][k]).all(), f"stream {s} {k}"
+
+
+@pytest.mark.parametrize("wname", ["M4_A30", "M4_A100"])
+def test_m4_stream_bitexact(O, torch_dev, wname):
+    w = inputs.WORKLOADS[wname]
+    tab = w.table(count=64)[None]          # one stream of 64 batches x 64 tasks
+    out = run_streams(torch_dev, w.profile, w.costs(), tab)
+    check(O, w.profile, w.costs(), tab, out)
+
+
+@pytest.mark.parametrize("profile", ["A30", "A100", "H100"])
+@pytest.mark.parametrize("n", [1, 5, 10, 30])
+def test_many_streams(O, torch_dev, profile, n):
+    tab = inputs.synthetic(profile, n, 12 * 9, 40 + n).reshape(12, 9, n, -1)
+    for costs in (inputs.reconfig_costs(profile), inputs.reconfig_costs(profile, zero=True)):
+        out = run_streams(torch_dev, profile, costs, tab)
+        check(O, profile, costs, tab, out)
+
+
+@pytest.mark.parametrize("gen", ["ties", "uniform", "narrow"])
+def test_stream_edge_inputs(O, torch_dev, gen):
+    profile = "A100"
+    n = 12
+    if gen == "ties":
+        t = inputs.small_ties(profile, n, 64, 3)
+    elif gen == "uniform":
+        t = inputs.uniform_random(profile, n, 64, 4)
+    else:
+        t = inputs.synthetic(profile, n, 64, 5, times="narrow")
+    tab = t.reshape(8, 8, n, -1)
+    costs = inputs.reconfig_costs(profile)
+    out = run_streams(torch_dev, profile, costs, tab)
+    check(O, profile, costs, tab, out)
+    out = run_streams(torch_dev, profile, costs, tab, max_iterations=2)
+    check(O, profile, costs, tab, out, max_iterations=2)
