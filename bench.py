@@ -185,7 +185,8 @@ def main():
     nc = len(inputs.SIZES[WORKLOAD.profile])
     # rank's shard of the counter-based table (weak scaling)
     host = inputs.synthetic_parallel(WORKLOAD.profile, WORKLOAD.n, I, WORKLOAD.seed, scaling=WORKLOAD.scaling,
-                                     times=WORKLOAD.times, start=rank * I)
+                                     times=WORKLOAD.times, start=rank * I,
+                                     workers=max(1, min(32, (os.cpu_count() or 1) // world)))
     pinned = torch.from_numpy(host).pin_memory()
     d_times = pinned.to(dev, non_blocking=False)
     F = far.Far(WORKLOAD.profile, WORKLOAD.costs())
