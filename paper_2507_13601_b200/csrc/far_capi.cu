@@ -15,7 +15,7 @@ using namespace farb;
 
 namespace {
 constexpr int RING = 256;
-constexpr int SMEM_MAX = 227 * 1024;
+int SMEM_MAX = 227 * 1024 - 1024;  // set from cudaDevAttrMaxSharedMemoryPerBlockOptin (minus static smem)
 }  // namespace
 
 struct far_ctx {
@@ -32,6 +32,13 @@ struct far_ctx {
   size_t d_buf_bytes = 0;
   cudaStream_t s[2] = {nullptr, nullptr};
   bool inited = false;
+  // overflow bitmasks (instances whose family exceeds the fast layout), ring of 4
+  unsigned* d_ovf[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t ovf_words[4] = {0, 0, 0, 0};
+  // launch-shape cache: (kernel, layout bytes) -> (warps per CTA, CTAs per SM)
+  struct Shape { const void* fn; int bytes, warps, per_sm; };
+  Shape shapes[16];
+  int nshapes = 0;
 };
 
 static far_status fail(far_ctx* c, far_status st, const std::string& m) {
@@ -63,6 +70,13 @@ static far_status ensure_device(far_ctx* ctx) {
   CK(cudaMemset(ctx->d_errflag, 0, sizeof(int)));
   CK(cudaStreamCreateWithFlags(&ctx->s[0], cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&ctx->s[1], cudaStreamNonBlocking));
+  // allow every kernel the full opt-in shared memory; each launch passes its own size
+  int optin = 0;
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  SMEM_MAX = optin - 1024;
+  const void* fns[4] = {(const void*)far_solve_kernel<3>, (const void*)far_solve_kernel<5>,
+                        (const void*)far_stream_kernel<3>, (const void*)far_stream_kernel<5>};
+  for (const void* f : fns) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
   ctx->inited = true;
   return FAR_OK;
 }
@@ -82,32 +96,80 @@ static far_status ensure_buf(far_ctx* ctx, size_t bytes) {
   return FAR_OK;
 }
 
-template <int NC> static Layout layout_for(int n) { return make_layout(n, NC, Tree<NC>::S, Tree<NC>::NN); }
+template <int NC> static Layout layout_for(int n, int kcap) {
+  return make_layout(n, NC, Tree<NC>::S, Tree<NC>::NN, kcap);
+}
 
-// Launch the fused solver kernel for I instances on `stream`.
+// Warps per CTA maximising resident warps per SM for a per-warp shared-memory footprint.
+static far_status pick_shape(far_ctx* ctx, const void* fn, int bytes, int& warps, int& per_sm) {
+  for (int i = 0; i < ctx->nshapes; ++i)
+    if (ctx->shapes[i].fn == fn && ctx->shapes[i].bytes == bytes) {
+      warps = ctx->shapes[i].warps;
+      per_sm = ctx->shapes[i].per_sm;
+      return FAR_OK;
+    }
+  int best_w = 0, best_b = 0, best_tot = 0;
+  for (int w = 1; w <= 4; ++w) {
+    const size_t smem = (size_t)w * bytes;
+    if (smem > (size_t)SMEM_MAX) break;
+    int b = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, w * 32, smem));
+    if (b * w > best_tot || (b * w == best_tot && w > best_w)) { best_tot = b * w; best_w = w; best_b = b; }
+  }
+  if (best_w == 0) return fail(ctx, FAR_E_TOO_LARGE, "instance does not fit in shared memory");
+  warps = best_w;
+  per_sm = std::max(1, best_b);
+  if (ctx->nshapes < 16) ctx->shapes[ctx->nshapes++] = {fn, bytes, warps, per_sm};
+  return FAR_OK;
+}
+
+// Launch the fused solver for I instances on `stream`: a fast pass whose shared-memory
+// layout holds families of up to kfast allocations, then (only if some family was larger)
+// an overflow pass with the full layout over the flagged instances.
 static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
   if (P.I <= 0) return FAR_OK;
   const bool a30 = ctx->nc == 3;
-  const Layout L = a30 ? layout_for<3>(P.n) : layout_for<5>(P.n);
-  int warps = std::min(4, SMEM_MAX / std::max(1, L.bytes));
-  if (warps < 1) return fail(ctx, FAR_E_TOO_LARGE, "instance does not fit in shared memory");
-  const size_t smem = (size_t)warps * L.bytes;
-  const void* fn = a30 ? (const void*)far_solve_kernel<3> : (const void*)far_solve_kernel<5>;
-  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, warps * 32, smem));
-  if (per_sm < 1) per_sm = 1;
-  const int64_t need = (P.I + warps - 1) / warps;
-  const int grid = (int)std::min<int64_t>(need, (int64_t)ctx->sms * per_sm);
-  const int slot = ctx->launch_id++ % RING;
-  P.counter = ctx->d_counter + slot;
+  const int kmax = 1 + P.n * (ctx->nc - 1);
+  int kfast = std::min(kmax, std::max(64, P.n));
+  if (P.mode != MODE_SOLVE) kfast = 1;
+  const bool need_ovf = P.mode == MODE_SOLVE && kfast < kmax;
+  const int slot = (ctx->launch_id++ % (RING / 4)) * 4;
+  CK(cudaMemsetAsync(ctx->d_counter + slot, 0, 3 * sizeof(unsigned long long), stream));
   P.errflag = ctx->d_errflag;
-  CK(cudaMemsetAsync(P.counter, 0, sizeof(unsigned long long), stream));
-  if (a30)
-    far_solve_kernel<3><<<grid, warps * 32, smem, stream>>>(P);
-  else
-    far_solve_kernel<5><<<grid, warps * 32, smem, stream>>>(P);
-  CK(cudaGetLastError());
+  P.ovf_count = ctx->d_counter + slot + 2;
+  P.ovf = nullptr;
+  if (need_ovf) {
+    const int r = (slot / 4) & 3;
+    const size_t words = (size_t)((P.I + 31) / 32);
+    if (ctx->ovf_words[r] < words) {
+      if (ctx->d_ovf[r]) {
+        CK(cudaDeviceSynchronize());
+        CK(cudaFree(ctx->d_ovf[r]));
+      }
+      if (cudaMalloc(&ctx->d_ovf[r], words * 4) != cudaSuccess) return fail(ctx, FAR_E_OOM, "overflow mask");
+      ctx->ovf_words[r] = words;
+    }
+    P.ovf = ctx->d_ovf[r];
+    CK(cudaMemsetAsync(P.ovf, 0, words * 4, stream));
+  }
+  const void* fn = a30 ? (const void*)far_solve_kernel<3> : (const void*)far_solve_kernel<5>;
+  for (int pass = 0; pass < (need_ovf ? 2 : 1); ++pass) {
+    P.kcap = pass == 0 ? kfast : kmax;
+    P.ovf_pass = pass;
+    P.counter = ctx->d_counter + slot + pass;
+    const Layout L = a30 ? layout_for<3>(P.n, P.kcap) : layout_for<5>(P.n, P.kcap);
+    int warps = 0, per_sm = 0;
+    far_status st = pick_shape(ctx, fn, L.bytes, warps, per_sm);
+    if (st) return st;
+    const size_t smem = (size_t)warps * L.bytes;
+    int64_t need = pass == 0 ? (P.I + warps - 1) / warps : ((P.I + 31) / 32 + warps - 1) / warps;
+    const int grid = (int)std::min<int64_t>(need, (int64_t)ctx->sms * per_sm);
+    if (a30)
+      far_solve_kernel<3><<<grid, warps * 32, smem, stream>>>(P);
+    else
+      far_solve_kernel<5><<<grid, warps * 32, smem, stream>>>(P);
+    CK(cudaGetLastError());
+  }
   return FAR_OK;
 }
 
@@ -173,6 +235,8 @@ void far_destroy(far_ctx* ctx) {
     cudaDeviceSynchronize();
     cudaFree(ctx->d_counter);
     cudaFree(ctx->d_errflag);
+    for (int r = 0; r < 4; ++r)
+      if (ctx->d_ovf[r]) cudaFree(ctx->d_ovf[r]);
     if (ctx->d_buf) cudaFree(ctx->d_buf);
     cudaStreamDestroy(ctx->s[0]);
     cudaStreamDestroy(ctx->s[1]);
@@ -407,8 +471,6 @@ extern "C" far_status far_concat_streams(far_ctx* ctx, const int32_t* d_times, i
   int warps = std::min(4, SMEM_MAX / std::max(1, L.bytes));
   if (warps < 1) return fail(ctx, FAR_E_TOO_LARGE, "stream state does not fit in shared memory");
   const size_t smem = (size_t)warps * L.bytes;
-  const void* fn = a30 ? (const void*)far_stream_kernel<3> : (const void*)far_stream_kernel<5>;
-  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = (int)((S + warps - 1) / warps);
   if (a30)
     far_stream_kernel<3><<<grid, warps * 32, smem, stream>>>(Q);

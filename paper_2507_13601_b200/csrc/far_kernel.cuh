@@ -45,40 +45,49 @@ struct KParams {
   int mode;
   unsigned long long* counter;  // dynamic instance scheduler (reset to 0 before launch)
   int* errflag;                 // sticky input-error flag
+  int kcap;                     // family-size capacity of the shared-memory layout
+  unsigned* ovf;                // bit per instance: family larger than kcap -> overflow pass
+  unsigned long long* ovf_count;
+  int ovf_pass;                 // 1: solve only the instances flagged in ovf (full layout)
 };
 
-// Per-warp shared-memory layout (bytes), identical on host and device.
+// Per-warp shared-memory layout (bytes), identical on host and device.  kcap bounds the
+// family size K this layout holds (the per-size lists hold at most n + K - 1 entries).
 struct Layout {
-  int times, lent, ltask, cnts, cur, su, bestnode, scratch, lstate, lslice, start, misc, bytes;
+  int times, lent, ltask, cnts, cur, su, bestnode, scratch, lstate, start, misc, bytes, ecap;
 };
 
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
 
-__host__ __device__ inline Layout make_layout(int n, int NC, int S, int NN) {
+__host__ __device__ inline Layout make_layout(int n, int NC, int S, int NN, int kcap) {
   Layout L;
-  const int Kmax = 1 + n * (NC - 1), Emax = n * NC;
+  (void)S;
+  int Ecap = n + kcap - 1;
+  if (Ecap > n * NC) Ecap = n * NC;
+  if (Ecap < 0) Ecap = 0;
+  L.ecap = Ecap;
   int o = 0;
   L.times = o;    o = al16(o + 4 * n * NC);
-  L.lent = o;     o = al16(o + 8 * Emax);
-  L.ltask = o;    o = al16(o + 2 * Emax);
-  L.cnts = o;     o = al16(o + 8 * Kmax);
+  L.lent = o;     o = al16(o + 8 * Ecap);
+  L.ltask = o;    o = al16(o + 2 * Ecap);
+  L.cnts = o;     o = al16(o + 8 * kcap);
   L.cur = o;      o = al16(o + n);
   L.su = o;       o = al16(o + n);
   L.bestnode = o; o = al16(o + n);
-  int sc = 32 * n;
-  if (10 * Emax > sc) sc = 10 * Emax;
-  if (2 * NN * n > sc) sc = 2 * NN * n;
+  int sc = 32 * n;                              // phase-2 node record [n][32]
+  if (10 * Ecap > sc) sc = 10 * Ecap;           // list sort scratch
+  if (4 * n * NC > sc) sc = 4 * n * NC;         // phase-1 member intervals
+  if (2 * NN * n > sc) sc = 2 * NN * n;         // node lists
   L.scratch = o;  o = al16(o + sc);
   L.lstate = o;   o = al16(o + 4 * NC * 32);
-  L.lslice = o;   o = al16(o + 4 * S * 32);
   L.start = o;    o = al16(o + 4 * n);
-  L.misc = o;     o = al16(o + 4 * 96);
+  L.misc = o;     o = al16(o + 4 * 160);
   L.bytes = o;
   return L;
 }
 
 // misc int slots
-enum { M_LOFF = 0, M_NCNT = 8, M_LP = 24, M_SEND = 40, M_BSEND = 48, M_Q = 56 };
+enum { M_LOFF = 0, M_NCNT = 8, M_NSUM = 24, M_SEND = 40, M_BSEND = 48, M_LIFE = 56 };
 
 __device__ __forceinline__ long long warp_sum_ll(long long v) {
 #pragma unroll
@@ -144,53 +153,93 @@ template <int S> struct Frontier {
 };
 
 // ---------------------------------------------------------------------------
-// Replay (Alg. 2 line 26, O7): the Alg. 1 event loop taking each node's tasks from its
-// ordered list.  One lane.  Writes start[j], onode[j]; returns the makespan.
+// Node-level replay (Alg. 2 line 26, O7).  Between two reconfiguration events of the
+// Alg. 1 event loop only task placements happen, and a node's tasks run back to back, so
+// the loop is replayed at node granularity: each node contributes a CREATE event at its
+// push key (a_v, lo_v) and a SPLIT event at (f_v, lo_v), f_v = creation end + sum of its
+// durations.  The event loop pops keys in non-decreasing (time, first slice) order, so
+// both loops apply the same reconfiguration events in the same order and give identical
+// starts (a destroy charged after the last task started cannot delay any creation).  This
+// takes <= 2*#nodes heap steps on one lane instead of n + #nodes; task starts are then
+// prefix sums over each node list (one lane per node).  life[v*6] = {cs, ce, ds, de}.
 // ---------------------------------------------------------------------------
 template <int NC>
-__device__ int replay_one(int n, const int32_t* T, const uint8_t* su, const uint16_t* nlist, const int* ncnt,
-                          int* lp, int* start, uint8_t* onode, const uint32_t* ninfo, const int* cr, const int* de) {
+__device__ int node_sim(const int* ncnt, const int* nsum, int* life, const uint32_t* ninfo, const int* cr,
+                        const int* de, int* Eout) {
   constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
-  for (int v = 0; v < NN; ++v) lp[v] = 0;
+  for (int v = 0; v < NN; ++v) life[v * 6] = -1;
   Frontier<S> F;
   F.init();
-  int rec = 0, ms = 0, remaining = n;
-  while (remaining > 0) {
+  int rec = 0, ms = 0, E = 0;
+  while (F.live) {
     int bs, be;
     F.pop(bs, be);
-    if (be == INT_MAX) break;  // unreachable: every listed task is reachable
     const int v = F.node(bs);
     const uint32_t w = ninfo[v];
-    if (lp[v] < ncnt[v]) {
-      if (!((F.has >> bs) & 1)) {
-        rec = max(rec, be) + cr[nd_szi(w)];
-        be = rec;
-        F.has |= 1u << bs;
+    if (!((F.has >> bs) & 1) && ncnt[v] > 0) {  // creation (lines 8-11), then all of v's tasks
+      const int cs = max(rec, be);
+      rec = cs + cr[nd_szi(w)];
+      life[v * 6 + 0] = cs;
+      life[v * 6 + 1] = rec;
+      const int f = rec + nsum[v];
+      ms = max(ms, f);
+      E = max(E, f);
+      F.has |= 1u << bs;
+      F.set(bs, f);
+    } else {  // repartitioning (lines 17-24): destroy if it had tasks
+      if ((F.has >> bs) & 1) {
+        const int ds = max(rec, be);
+        rec = ds + de[nd_szi(w)];
+        life[v * 6 + 2] = ds;
+        life[v * 6 + 3] = rec;
+        E = max(E, rec);
       }
-      const int j = nlist[v * n + lp[v]];
-      lp[v]++;
-      start[j] = be;
-      onode[j] = (uint8_t)v;
-      be += T[j * NC + su[j]];
-      ms = max(ms, be);
-      --remaining;
-      F.set(bs, be);
-    } else {
-      if ((F.has >> bs) & 1) rec = max(rec, be) + de[nd_szi(w)];
       F.split(bs, be, w);
     }
   }
+  *Eout = E;
+  return ms;
+}
+
+template <int NC>
+__device__ __forceinline__ int dur_of(const int32_t* T, const uint8_t* su, int j) {
+  return T[j * NC + su[j]];
+}
+
+// Replay of node lists nlist[v][0..ncnt[v]) -> start[j], onode[j]; returns the makespan.
+template <int NC>
+__device__ int replay_warp(int n, const int32_t* T, const uint8_t* su, const uint16_t* nlist, const int* ncnt,
+                           int* nsum, int* life, int* start, uint8_t* onode, const uint32_t* ninfo, const int* cr,
+                           const int* de, int lane, int* Eout = nullptr) {
+  constexpr int NN = Tree<NC>::NN;
+  if (lane < NN) {
+    int sm = 0;
+    for (int q = 0; q < ncnt[lane]; ++q) sm += dur_of<NC>(T, su, nlist[lane * n + q]);
+    nsum[lane] = sm;
+  }
+  __syncwarp();
+  int ms = 0, E = 0;
+  if (lane == 0) ms = node_sim<NC>(ncnt, nsum, life, ninfo, cr, de, &E);
+  ms = __shfl_sync(FULL, ms, 0);
+  E = __shfl_sync(FULL, E, 0);
+  __syncwarp();
+  if (lane < NN && ncnt[lane] > 0) {
+    int t = life[lane * 6 + 1];
+    for (int q = 0; q < ncnt[lane]; ++q) {
+      const int j = nlist[lane * n + q];
+      start[j] = t;
+      onode[j] = (uint8_t)lane;
+      t += dur_of<NC>(T, su, j);
+    }
+  }
+  __syncwarp();
+  if (Eout) *Eout = E;
   return ms;
 }
 
 // ---------------------------------------------------------------------------
 // Phase 3: Alg. 2 on node lists (warp-cooperative).  sliceEnd in smem.
 // ---------------------------------------------------------------------------
-template <int NC>
-__device__ __forceinline__ int dur_of(const int32_t* T, const uint8_t* su, int j) {
-  return T[j * NC + su[j]];
-}
-
 template <int NC>
 __device__ void list_remove(uint16_t* lst, int* cnt, int j, int lane) {
   if (lane == 0) {
@@ -340,26 +389,38 @@ __device__ void refine_warp(int n, const int32_t* T, const uint8_t* su, uint16_t
 
 // Build per-node ordered lists of member k from the per-size LPT lists: sizes in
 // decreasing order so the A100 {S0..S3} node lists its size-4 tasks before its size-3
-// tasks.  Lane 0.
+// tasks.  Lanes over list entries; __match_any_sync ranks entries per node.
 template <int NC>
 __device__ void build_node_lists(int n, int k, const int2* lent, const uint16_t* ltask, const int* loff,
                                  const uint8_t* node_of, uint16_t* nlist, int* ncnt, uint8_t* su, int lane) {
   constexpr int NN = Tree<NC>::NN;
-  if (lane == 0) {
-    for (int v = 0; v < NN; ++v) ncnt[v] = 0;
-    for (int c = NC - 1; c >= 0; --c)
-      for (int p = loff[c]; p < loff[c + 1]; ++p) {
+  if (lane < NN) ncnt[lane] = 0;
+  __syncwarp();
+  for (int c = NC - 1; c >= 0; --c) {
+    const int pe = loff[c + 1];
+    for (int p0 = loff[c]; p0 < pe; p0 += 32) {
+      const int p = p0 + lane;
+      int v = -1, j = 0;
+      if (p < pe) {
         const int y = lent[p].y;
         const int lo = y & 0xFFFF, hi = (int)((unsigned)y >> 16);
         if (lo <= k && k < hi) {
-          const int j = ltask[p];
-          const int v = node_of[j];
-          nlist[v * n + ncnt[v]++] = (uint16_t)j;
+          j = ltask[p];
+          v = node_of[j];
           su[j] = (uint8_t)c;
         }
       }
+      const unsigned grp = __match_any_sync(FULL, v);
+      const int rank = __popc(grp & ((1u << lane) - 1));
+      const int base = v >= 0 ? ncnt[v] : 0;
+      __syncwarp();
+      if (v >= 0) {
+        nlist[v * n + base + rank] = (uint16_t)j;
+        if (rank == __popc(grp) - 1) ncnt[v] = base + __popc(grp);
+      }
+      __syncwarp();
+    }
   }
-  __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
@@ -379,14 +440,14 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   uint8_t* bestnode = wsm + L.bestnode;
   unsigned char* scratch = wsm + L.scratch;
   uint32_t* lstate = (uint32_t*)(wsm + L.lstate);
-  int* lslice = (int*)(wsm + L.lslice);
   int* start = (int*)(wsm + L.start);
   int* misc = (int*)(wsm + L.misc);
   int* loff = misc + M_LOFF;
   int* ncnt = misc + M_NCNT;
-  int* lp = misc + M_LP;
+  int* nsum = misc + M_NSUM;
   int* send = misc + M_SEND;
   int* bsend = misc + M_BSEND;
+  int* life = misc + M_LIFE;
 
   // ---- H0: stage the runtime table (contiguous n*NC int32) into shared memory
   const int cntT = n * NC;
@@ -508,11 +569,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       long long ev;
       refine_warp<NC>(n, T, su, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
       R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
-      int msR = 0;
-      if (lane == 0) msR = replay_one<NC>(n, T, su, nlist, ncnt, lp, start + 0, bestnode, ninfo, cr, de);
-      // replay wrote into start[] / bestnode[] only on lane 0's view; broadcast
-      msR = __shfl_sync(FULL, msR, 0);
-      __syncwarp();
+      const int msR = replay_warp<NC>(n, T, su, nlist, ncnt, nsum, life, start, bestnode, ninfo, cr, de, lane);
       if (!(P.flags & FAR_NO_GUARD) && msR > ms2) {
         R.reverted = 1;
       } else {
@@ -594,6 +651,13 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       const int jj = (int)__reduce_min_sync(FULL, (unsigned)(lm == m ? lj : INT_MAX));
       const int cj = cur[jj];
       if (cj == NC - 1) break;
+      if (K >= P.kcap) {  // family larger than this layout holds: defer to the overflow pass
+        if (lane == 0) {
+          atomicOr(P.ovf + (inst >> 5), 1u << (inst & 31));
+          atomicAdd(P.ovf_count, 1ull);
+        }
+        return;
+      }
       int best = -1;
       long long bw = 0;
       for (int c = cj + 1; c < NC; ++c) {
@@ -652,7 +716,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     __syncwarp();
     // rank sort inside each segment -> scratch (ivl is dead), then copy back
     int2* sent = (int2*)scratch;
-    uint16_t* stask = (uint16_t*)(scratch + 8 * n * NC);
+    uint16_t* stask = (uint16_t*)(scratch + 8 * L.ecap);
     for (int c = 0; c < NC; ++c) {
       const int b = off[c], m = off[c + 1] - off[c];
       for (int e = lane; e < m; e += 32) {
@@ -682,6 +746,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   for (int kb = 0; kb < K; kb += 32) {
     const int k = kb + lane;
     int ms = INT_MAX, pops = 0;
+    int sl[S];  // slice ends of this lane's member at termination
     if (k < K) {
       const unsigned long long cp = cnts[k];
       int total = 0;
@@ -695,6 +760,8 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       F.init();
       int rec = 0;
       ms = 0;
+#pragma unroll
+      for (int s = 0; s < S; ++s) sl[s] = 0;
       while (total > 0) {
         int bs, be;
         F.pop(bs, be);
@@ -733,7 +800,10 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
           F.set(bs, be);
         } else {  // lines 17-24 (total > 0 here)
           if ((F.has >> bs) & 1) rec = max(rec, be) + de[nd_szi(w)];
-          if (!F.split(bs, be, w)) lslice[bs * 32 + lane] = be;  // removed leaf keeps its slice end
+          if (!F.split(bs, be, w)) {  // a removed leaf keeps its slice end
+#pragma unroll
+            for (int s = 0; s < S; ++s) sl[s] = (s == bs) ? be : sl[s];
+          }
         }
       }
       pops += __popc(F.live);  // the remaining frontier nodes are popped and dropped (heap empties)
@@ -741,7 +811,8 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       for (int s = 0; s < S; ++s)
         if ((F.live >> s) & 1) {
           const int sz = nd_sz(ninfo[F.node(s)]);
-          for (int q = s; q < s + sz; ++q) lslice[q * 32 + lane] = F.e[s];
+#pragma unroll
+          for (int q = 0; q < S; ++q) sl[q] = (q >= s && q < s + sz) ? F.e[s] : sl[q];
         }
     }
     events += warp_sum_ll(pops);
@@ -754,7 +825,11 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       bestk = kw;
       const int wl = kw - kb;
       for (int j = lane; j < n; j += 32) bestnode[j] = recnode[j * 32 + wl];
-      if (lane < S) bsend[lane] = lslice[lane * 32 + wl];
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int x = __shfl_sync(FULL, sl[s], wl);
+        if (lane == 0) bsend[s] = x;
+      }
     }
     __syncwarp();
   }
@@ -775,10 +850,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     long long ev;
     refine_warp<NC>(n, T, su, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
     R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
-    int msR = 0;
-    if (lane == 0) msR = replay_one<NC>(n, T, su, nlist, ncnt, lp, start, cur, ninfo, cr, de);
-    msR = __shfl_sync(FULL, msR, 0);
-    __syncwarp();
+    const int msR = replay_warp<NC>(n, T, su, nlist, ncnt, nsum, life, start, cur, ninfo, cr, de, lane);
     if (!(P.flags & FAR_NO_GUARD) && msR > ms2) {
       R.reverted = 1;  // keep-best guard: return the phase-2 schedule
       build_node_lists<NC>(n, bestk, lent, ltask, loff, bestnode, nlist, ncnt, su, lane);
@@ -788,8 +860,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     }
   }
   if (want_sched && !have_starts) {
-    if (lane == 0) replay_one<NC>(n, T, su, nlist, ncnt, lp, start, cur, ninfo, cr, de);  // fixpoint = phase 2
-    __syncwarp();
+    replay_warp<NC>(n, T, su, nlist, ncnt, nsum, life, start, cur, ninfo, cr, de, lane);  // fixpoint = phase 2
   }
   R.makespan = msF;
   if (want_sched) {
@@ -831,15 +902,33 @@ __global__ void __launch_bounds__(128) far_solve_kernel(KParams P) {
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Layout L = make_layout(P.n, NC, Tree<NC>::S, NN);
+  const Layout L = make_layout(P.n, NC, Tree<NC>::S, NN, P.kcap);
   unsigned char* wsm = smem + (size_t)warp * L.bytes;
-  for (;;) {
-    unsigned long long inst = 0;
-    if (lane == 0) inst = atomicAdd(P.counter, 1ull);
-    inst = __shfl_sync(FULL, inst, 0);
-    if ((int64_t)inst >= P.I) break;
-    solve_instance<NC>(P, (int64_t)inst, wsm, L, ninfo, cr, de, lane);
-    __syncwarp();
+  if (!P.ovf_pass) {
+    for (;;) {
+      unsigned long long inst = 0;
+      if (lane == 0) inst = atomicAdd(P.counter, 1ull);
+      inst = __shfl_sync(FULL, inst, 0);
+      if ((int64_t)inst >= P.I) break;
+      solve_instance<NC>(P, (int64_t)inst, wsm, L, ninfo, cr, de, lane);
+      __syncwarp();
+    }
+  } else {
+    if (*(volatile unsigned long long*)P.ovf_count == 0) return;
+    const int64_t nwords = (P.I + 31) >> 5;
+    for (;;) {
+      unsigned long long wd = 0;
+      if (lane == 0) wd = atomicAdd(P.counter, 1ull);
+      wd = __shfl_sync(FULL, wd, 0);
+      if ((int64_t)wd >= nwords) break;
+      unsigned bits = P.ovf[wd];
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        solve_instance<NC>(P, (int64_t)wd * 32 + b, wsm, L, ninfo, cr, de, lane);
+        __syncwarp();
+      }
+    }
   }
 }
 

@@ -35,7 +35,7 @@ struct SParams {
 };
 
 struct SLayout {
-  int times, su, nl, nl2, ncnt, ncnt2, lp, start, fstart, life, win, misc, bytes;
+  int times, su, onode, nl, nl2, ncnt, ncnt2, nsum, start, fstart, life, win, misc, bytes;
 };
 
 __host__ __device__ inline SLayout make_slayout(int n, int NC, int NN) {
@@ -43,11 +43,12 @@ __host__ __device__ inline SLayout make_slayout(int n, int NC, int NN) {
   int o = 0;
   L.times = o;  o = al16(o + 4 * n * NC);
   L.su = o;     o = al16(o + n);
+  L.onode = o;  o = al16(o + n);
   L.nl = o;     o = al16(o + 2 * NN * n);
   L.nl2 = o;    o = al16(o + 2 * NN * n);
   L.ncnt = o;   o = al16(o + 4 * 16);
   L.ncnt2 = o;  o = al16(o + 4 * 16);
-  L.lp = o;     o = al16(o + 4 * 16);
+  L.nsum = o;   o = al16(o + 4 * 16);
   L.start = o;  o = al16(o + 4 * n);
   L.fstart = o; o = al16(o + 4 * n);
   L.life = o;   o = al16(o + 4 * 16 * 6);
@@ -73,60 +74,9 @@ __device__ __forceinline__ long long warp_min_ll(long long v) {
   return v;
 }
 
-// Full-lifecycle event loop (lane 0): the O7 replay where every node with tasks is also
-// destroyed when dropped.  life[v] = {cs, ce, ds, de} (-1 if the node has no tasks).
-// Returns E = end of the last event (or task).
-template <int NC>
-__device__ int lifecycle_sim(int n, const int32_t* T, const uint8_t* su, const uint16_t* nl, const int* ncnt, int* lp,
-                             int* start, int* life, const uint32_t* ninfo, const int* cr, const int* de) {
-  constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
-  for (int v = 0; v < NN; ++v) {
-    lp[v] = 0;
-    life[v * 6 + 0] = -1;
-  }
-  Frontier<S> F;
-  F.init();
-  int rec = 0, remaining = n, E = 0;
-  while (F.live) {
-    int bs, be;
-    F.pop(bs, be);
-    const int v = F.node(bs);
-    const uint32_t w = ninfo[v];
-    if (lp[v] < ncnt[v]) {
-      if (!((F.has >> bs) & 1)) {
-        const int cs = max(rec, be);
-        rec = cs + cr[nd_szi(w)];
-        life[v * 6 + 0] = cs;
-        life[v * 6 + 1] = rec;
-        be = rec;
-        F.has |= 1u << bs;
-      }
-      const int j = nl[v * n + lp[v]];
-      lp[v]++;
-      start[j] = be;
-      be += T[j * NC + su[j]];
-      E = max(E, be);
-      --remaining;
-      F.set(bs, be);
-    } else {
-      if ((F.has >> bs) & 1) {
-        const int ds = max(rec, be);
-        rec = ds + de[nd_szi(w)];
-        life[v * 6 + 2] = ds;
-        life[v * 6 + 3] = rec;
-        E = max(E, rec);
-      }
-      if (remaining > 0) {
-        F.split(bs, be, w);
-      } else {
-        F.has &= ~(1u << bs);
-        F.live &= ~(1u << bs);
-        F.set(bs, INT_MAX);
-      }
-    }
-  }
-  return E;
-}
+// The full-lifecycle timeline of a batch (R22) is the node-level replay of far_kernel.cuh:
+// node_sim charges a destroy for every node with tasks at its SPLIT key, which is exactly
+// the O7 loop extended with a destroy at drop time.
 
 // Per-stream fold state (shared memory, misc region)
 struct StreamSt {
@@ -149,14 +99,12 @@ struct SeamRes {
 
 // Timeline of the batch described by (nl, ncnt) + its seam against the stream state.
 template <int NC>
-__device__ SeamRes eval_seam(int n, const int32_t* T, const uint8_t* su, const uint16_t* nl, const int* ncnt, int* lp,
-                             int* start, int* life, const uint32_t* ninfo, const int* cr, const int* de, bool rev,
-                             const StreamSt* st, const WinEv* win, int lane) {
+__device__ SeamRes eval_seam(int n, const int32_t* T, const uint8_t* su, const uint16_t* nl, const int* ncnt,
+                             int* nsum, uint8_t* onode, int* start, int* life, const uint32_t* ninfo, const int* cr,
+                             const int* de, bool rev, const StreamSt* st, const WinEv* win, int lane) {
   constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
   int E = 0;
-  if (lane == 0) E = lifecycle_sim<NC>(n, T, su, nl, ncnt, lp, start, life, ninfo, rev ? de : cr, rev ? cr : de);
-  E = __shfl_sync(FULL, E, 0);
-  __syncwarp();
+  replay_warp<NC>(n, T, su, nl, ncnt, nsum, life, start, onode, ninfo, rev ? de : cr, rev ? cr : de, lane, &E);
   if (rev) {  // mirror about E: tasks and lifecycles (a mirrored forward destroy is the create)
     for (int j = lane; j < n; j += 32) start[j] = E - (start[j] + T[j * NC + su[j]]);
     if (lane < NN && life[lane * 6] >= 0) {
@@ -297,7 +245,8 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
   uint16_t* nl2 = (uint16_t*)(wsm + L.nl2);
   int* ncnt = (int*)(wsm + L.ncnt);
   int* ncnt2 = (int*)(wsm + L.ncnt2);
-  int* lp = (int*)(wsm + L.lp);
+  int* nsum = (int*)(wsm + L.nsum);
+  uint8_t* onode = wsm + L.onode;
   int* start = (int*)(wsm + L.start);
   int* fstart = (int*)(wsm + L.fstart);
   int* life = (int*)(wsm + L.life);
@@ -350,9 +299,7 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
       StreamSt dummy;
       (void)dummy;
       int E = 0;
-      if (lane == 0) E = lifecycle_sim<NC>(n, T, su, nl, ncnt, lp, start, life, ninfo, cr, de);
-      E = __shfl_sync(FULL, E, 0);
-      __syncwarp();
+      replay_warp<NC>(n, T, su, nl, ncnt, nsum, life, start, onode, ninfo, cr, de, lane, &E);
       int te = 0;
       for (int j = lane; j < n; j += 32) te = max(te, start[j] + T[j * NC + su[j]]);
       te = __reduce_max_sync(FULL, te);
@@ -365,7 +312,7 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
     int moves = 0, swaps = 0;
     // ---- seam move/swap on reversed batches (R24)
     if (rev && k > 0) {
-      SeamRes cur = eval_seam<NC>(n, T, su, nl, ncnt, lp, start, life, ninfo, cr, de, true, st, win, lane);
+      SeamRes cur = eval_seam<NC>(n, T, su, nl, ncnt, nsum, onode, start, life, ninfo, cr, de, true, st, win, lane);
       for (int it = 0; it < P.max_it; ++it) {
         unsigned long long Q = 0;
         int qh = 0, qt = 0;
@@ -411,7 +358,7 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
               copy_lists<NC>(n, nl, ncnt, nl2, ncnt2, lane);
               list_remove<NC>(nl2 + I * n, &ncnt2[I], Tm, lane);
               list_insert<NC>(nl2 + A * n, &ncnt2[A], Tm, T, su, lane);
-              SeamRes e2 = eval_seam<NC>(n, T, su, nl2, ncnt2, lp, start, life, ninfo, cr, de, true, st, win, lane);
+              SeamRes e2 = eval_seam<NC>(n, T, su, nl2, ncnt2, nsum, onode, start, life, ninfo, cr, de, true, st, win, lane);
               if (e2.end < cur.end) {
                 copy_lists<NC>(n, nl2, ncnt2, nl, ncnt, lane);
                 cur = e2;
@@ -442,7 +389,7 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
                 list_remove<NC>(nl2 + A * n, &ncnt2[A], jj, lane);
                 list_insert<NC>(nl2 + A * n, &ncnt2[A], kk, T, su, lane);
                 list_insert<NC>(nl2 + I * n, &ncnt2[I], jj, T, su, lane);
-                SeamRes e2 = eval_seam<NC>(n, T, su, nl2, ncnt2, lp, start, life, ninfo, cr, de, true, st, win, lane);
+                SeamRes e2 = eval_seam<NC>(n, T, su, nl2, ncnt2, nsum, onode, start, life, ninfo, cr, de, true, st, win, lane);
                 if (e2.end < cur.end) {
                   copy_lists<NC>(n, nl2, ncnt2, nl, ncnt, lane);
                   cur = e2;
@@ -464,7 +411,7 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
       }
     }
     // ---- final timeline + seam of the (refined) batch; place it
-    const SeamRes R = eval_seam<NC>(n, T, su, nl, ncnt, lp, start, life, ninfo, cr, de, rev, st, win, lane);
+    const SeamRes R = eval_seam<NC>(n, T, su, nl, ncnt, nsum, onode, start, life, ninfo, cr, de, rev, st, win, lane);
     const long long O = R.O;
     ms = max(ms, O + R.task_end);
     if (lane == 0) {
