@@ -240,32 +240,53 @@ __device__ int replay_warp(int n, const int32_t* T, const uint8_t* su, const uin
 // ---------------------------------------------------------------------------
 // Phase 3: Alg. 2 on node lists (warp-cooperative).  sliceEnd in smem.
 // ---------------------------------------------------------------------------
+// Remove task j from an ordered node list (warp: ballot to find it, chunked shift left).
 template <int NC>
 __device__ void list_remove(uint16_t* lst, int* cnt, int j, int lane) {
-  if (lane == 0) {
-    int q = 0;
-    while (lst[q] != j) ++q;
-    for (; q + 1 < *cnt; ++q) lst[q] = lst[q + 1];
-    *cnt -= 1;
+  const int c = *cnt;
+  int q = c;
+  for (int b = 0; b < c; b += 32) {
+    const unsigned m = __ballot_sync(FULL, b + lane < c && lst[b + lane] == j);
+    if (m) { q = b + __ffs(m) - 1; break; }
   }
+  for (int b = q; b < c - 1; b += 32) {
+    const int i = b + lane;
+    const uint16_t v = i < c - 1 ? lst[i + 1] : 0;
+    __syncwarp();
+    if (i < c - 1) lst[i] = v;
+    __syncwarp();
+  }
+  if (lane == 0) *cnt = c - 1;
   __syncwarp();
 }
 
 // "Insert T in I^a.tasks ordered by T.time": decreasing time, ties -> lower index.
+// Warp: the insertion point is the number of entries ordered before j; chunked shift right.
 template <int NC>
 __device__ void list_insert(uint16_t* lst, int* cnt, int j, const int32_t* T, const uint8_t* su, int lane) {
-  if (lane == 0) {
-    const int dj = dur_of<NC>(T, su, j);
-    int q = *cnt;
-    while (q > 0) {
-      const int x = lst[q - 1];
+  const int c = *cnt;
+  const int dj = dur_of<NC>(T, su, j);
+  int pos = 0;
+  for (int b = 0; b < c; b += 32) {
+    const int i = b + lane;
+    bool before = false;
+    if (i < c) {
+      const int x = lst[i];
       const int dx = dur_of<NC>(T, su, x);
-      if (dx > dj || (dx == dj && x < j)) break;
-      lst[q] = lst[q - 1];
-      --q;
+      before = dx > dj || (dx == dj && x < j);
     }
-    lst[q] = (uint16_t)j;
-    *cnt += 1;
+    pos += __popc(__ballot_sync(FULL, before));
+  }
+  for (int top = c - 1; top >= pos; top -= 32) {
+    const int i = top - lane;
+    const uint16_t v = i >= pos ? lst[i] : 0;
+    __syncwarp();
+    if (i >= pos) lst[i + 1] = v;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    lst[pos] = (uint16_t)j;
+    *cnt = c + 1;
   }
   __syncwarp();
 }
@@ -307,13 +328,19 @@ __device__ void refine_warp(int n, const int32_t* T, const uint8_t* su, uint16_t
       const int I = (int)((Q >> (4 * qh++)) & 15);
       if (I == 0) { stop = true; break; }
       const uint32_t wI = ninfo[I];
-      int A = -1, eA = 0;
-      for (int u = 0; u < NN; ++u) {
-        const uint32_t wu = ninfo[u];
-        if (u == I || nd_sz(wu) != nd_sz(wI)) continue;
-        const int eu = end_of(wu);
-        if (A < 0 || eu < eA || (eu == eA && nd_lo(wu) < nd_lo(ninfo[A]))) { A = u; eA = eu; }
+      // alternative I^a: same size, != I, minimum (end, first slice) -- lanes over nodes
+      bool valid = false;
+      int eu = INT_MAX, lou = 15;
+      if (lane < NN && lane != I && nd_sz(ninfo[lane]) == nd_sz(wI)) {
+        valid = true;
+        eu = end_of(ninfo[lane]);
+        lou = nd_lo(ninfo[lane]);
       }
+      const int eA = __reduce_min_sync(FULL, eu);
+      const bool c1 = valid && eu == eA;
+      const int lmin = __reduce_min_sync(FULL, c1 ? lou : 15);
+      const unsigned sel = __ballot_sync(FULL, c1 && lou == lmin);
+      const int A = sel ? __ffs(sel) - 1 : -1;
       bool done = false;
       if (A >= 0) {
         const int m = omega - eA;
@@ -423,85 +450,93 @@ __device__ void build_node_lists(int n, int k, const int2* lent, const uint16_t*
   }
 }
 
-// ---------------------------------------------------------------------------
-// One instance, one warp.
-// ---------------------------------------------------------------------------
+// Warp bitonic sort of 32*R (key, val) pairs held in registers (element i = r*32 + lane),
+// ascending by key.  Keys are unique (they carry the task index), padding is 0xFFFFFFFF.
+template <int R>
+__device__ __forceinline__ void warp_bitonic(unsigned (&key)[R], unsigned (&val)[R], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32 * R; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int rj = j >> 5;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if ((r & rj) == 0) {
+            const int r2 = r | rj;
+            const bool up = (((r << 5) | lane) & k) == 0;
+            const bool sw = up ? (key[r] > key[r2]) : (key[r] < key[r2]);
+            const unsigned k0 = key[r], v0 = val[r];
+            key[r] = sw ? key[r2] : k0;
+            val[r] = sw ? val[r2] : v0;
+            key[r2] = sw ? k0 : key[r2];
+            val[r2] = sw ? v0 : val[r2];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const unsigned ok = __shfl_xor_sync(FULL, key[r], j);
+          const unsigned ov = __shfl_xor_sync(FULL, val[r], j);
+          const bool lower = (lane & j) == 0;
+          const bool up = (((r << 5) | lane) & k) == 0;
+          const bool take = (lower == up) ? (ok < key[r]) : (ok > key[r]);
+          key[r] = take ? ok : key[r];
+          val[r] = take ? ov : val[r];
+        }
+      }
+    }
+  }
+}
+
+// Sort one LPT list segment (t < 2^22, m <= 32*R) by (-t, task) with the packed key
+// ((2^22 - 1 - t) << 10) | task.
+template <int R>
+__device__ void sort_segment(int2* ent, uint16_t* tsk, int m, int lane) {
+  unsigned key[R], val[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = r * 32 + lane;
+    if (i < m) {
+      const int2 x = ent[i];
+      key[r] = ((unsigned)(0x3FFFFF - x.x) << 10) | (unsigned)tsk[i];
+      val[r] = (unsigned)x.y;
+    } else {
+      key[r] = 0xFFFFFFFFu;
+      val[r] = 0;
+    }
+  }
+  warp_bitonic<R>(key, val, lane);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = r * 32 + lane;
+    if (i < m) {
+      ent[i] = make_int2(0x3FFFFF - (int)(key[r] >> 10), (int)val[r]);
+      tsk[i] = (uint16_t)(key[r] & 1023u);
+    }
+  }
+}
+
+// Phase 3 + replay + guard on an input schedule (far_local_search, MODE_LOCAL).
 template <int NC>
-__device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* wsm, const Layout& L,
-                               const uint32_t* ninfo, const int* cr, const int* de, int lane) {
+__device__ __noinline__ void solve_local(const KParams& P, int64_t inst, unsigned char* wsm, const Layout& L,
+                                         const uint32_t* ninfo, const int* cr, const int* de, int lane,
+                                         far_result R, bool want_sched, bool refine) {
   constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
   const int n = P.n;
   int32_t* T = (int32_t*)(wsm + L.times);
-  int2* lent = (int2*)(wsm + L.lent);
-  uint16_t* ltask = (uint16_t*)(wsm + L.ltask);
-  unsigned long long* cnts = (unsigned long long*)(wsm + L.cnts);
   uint8_t* cur = wsm + L.cur;
   uint8_t* su = wsm + L.su;
   uint8_t* bestnode = wsm + L.bestnode;
   unsigned char* scratch = wsm + L.scratch;
-  uint32_t* lstate = (uint32_t*)(wsm + L.lstate);
   int* start = (int*)(wsm + L.start);
   int* misc = (int*)(wsm + L.misc);
-  int* loff = misc + M_LOFF;
   int* ncnt = misc + M_NCNT;
   int* nsum = misc + M_NSUM;
   int* send = misc + M_SEND;
-  int* bsend = misc + M_BSEND;
   int* life = misc + M_LIFE;
+  int ms2 = 0;
 
-  // ---- H0: stage the runtime table (contiguous n*NC int32) into shared memory
-  const int cntT = n * NC;
-  const int32_t* src = P.times + inst * (int64_t)cntT;
-  if ((((uintptr_t)src) & 15) == 0) {
-    const int n4 = cntT >> 2;
-    const int4* s4 = (const int4*)src;
-    int4* d4 = (int4*)T;
-    for (int q = lane; q < n4; q += 32) d4[q] = __ldcs(s4 + q);
-    for (int q = (n4 << 2) + lane; q < cntT; q += 32) T[q] = __ldcs(src + q);
-  } else {
-    for (int q = lane; q < cntT; q += 32) T[q] = __ldcs(src + q);
-  }
-  __syncwarp();
-
-  far_result R;
-  R.makespan = 0; R.makespan_phase2 = 0; R.alloc_index = 0; R.family_size = 0;
-  R.moves = 0; R.swaps = 0; R.iterations = 0; R.reverted = 0; R.status = FAR_OK; R.reserved = 0;
-  R.evals = 0; R.events = 0;
-  const bool want_sched = P.sched != nullptr && !(P.flags & FAR_NO_SCHEDULE);
-  const bool refine = !(P.flags & FAR_NO_REFINE);
-
-  // ---- input checks (include/far.h "Integer range")
-  {
-    int bad = 0;
-    long long bsum = 0;
-    for (int j = lane; j < n; j += 32) {
-      int mx = 0;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const int t = T[j * NC + c];
-        bad |= (t < 1);
-        mx = max(mx, t);
-      }
-      bsum += mx;
-    }
-    bad = __any_sync(FULL, bad);
-    bsum = warp_sum_ll(bsum);
-    long long rsum = 0;
-    for (int v = 0; v < NN; ++v) rsum += cr[nd_szi(ninfo[v])] + de[nd_szi(ninfo[v])];
-    if (bad || bsum + rsum >= BOUND) {
-      if (lane == 0) {
-        R.makespan = -1;
-        R.status = FAR_E_BAD_TIME;
-        P.makespan[inst] = -1;
-        if (P.res) P.res[inst] = R;
-        atomicOr(P.errflag, 1);
-      }
-      return;
-    }
-  }
-
-  int ms2 = 0, bestk = 0;
-  if (P.mode == MODE_LOCAL) {
     // ---- rebuild the tree from an input schedule: node lists ordered by (start, task)
     const far_task_slot* in = P.sched_in + inst * (int64_t)n;
     int bad = 0, msIn = 0;
@@ -600,6 +635,91 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     return;
   }
 
+// ---------------------------------------------------------------------------
+// One instance, one warp.
+// ---------------------------------------------------------------------------
+template <int NC>
+__device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* wsm, const Layout& L,
+                               const uint32_t* ninfo, const int* cr, const int* de, int lane) {
+  constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
+  const int n = P.n;
+  int32_t* T = (int32_t*)(wsm + L.times);
+  int2* lent = (int2*)(wsm + L.lent);
+  uint16_t* ltask = (uint16_t*)(wsm + L.ltask);
+  unsigned long long* cnts = (unsigned long long*)(wsm + L.cnts);
+  uint8_t* cur = wsm + L.cur;
+  uint8_t* su = wsm + L.su;
+  uint8_t* bestnode = wsm + L.bestnode;
+  unsigned char* scratch = wsm + L.scratch;
+  uint32_t* lstate = (uint32_t*)(wsm + L.lstate);
+  int* start = (int*)(wsm + L.start);
+  int* misc = (int*)(wsm + L.misc);
+  int* loff = misc + M_LOFF;
+  int* ncnt = misc + M_NCNT;
+  int* nsum = misc + M_NSUM;
+  int* send = misc + M_SEND;
+  int* bsend = misc + M_BSEND;
+  int* life = misc + M_LIFE;
+
+  // ---- H0: stage the runtime table (contiguous n*NC int32) into shared memory
+  const int cntT = n * NC;
+  const int32_t* src = P.times + inst * (int64_t)cntT;
+  if ((((uintptr_t)src) & 15) == 0) {
+    const int n4 = cntT >> 2;
+    const int4* s4 = (const int4*)src;
+    int4* d4 = (int4*)T;
+    for (int q = lane; q < n4; q += 32) d4[q] = __ldcs(s4 + q);
+    for (int q = (n4 << 2) + lane; q < cntT; q += 32) T[q] = __ldcs(src + q);
+  } else {
+    for (int q = lane; q < cntT; q += 32) T[q] = __ldcs(src + q);
+  }
+  __syncwarp();
+
+  far_result R;
+  R.makespan = 0; R.makespan_phase2 = 0; R.alloc_index = 0; R.family_size = 0;
+  R.moves = 0; R.swaps = 0; R.iterations = 0; R.reverted = 0; R.status = FAR_OK; R.reserved = 0;
+  R.evals = 0; R.events = 0;
+  const bool want_sched = P.sched != nullptr && !(P.flags & FAR_NO_SCHEDULE);
+  const bool refine = !(P.flags & FAR_NO_REFINE);
+
+  // ---- input checks (include/far.h "Integer range")
+  int tmax = 0;
+  {
+    int bad = 0;
+    long long bsum = 0;
+    for (int j = lane; j < n; j += 32) {
+      int mx = 0;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int t = T[j * NC + c];
+        bad |= (t < 1);
+        mx = max(mx, t);
+      }
+      bsum += mx;
+      tmax = max(tmax, mx);
+    }
+    bad = __any_sync(FULL, bad);
+    bsum = warp_sum_ll(bsum);
+    tmax = __reduce_max_sync(FULL, tmax);
+    long long rsum = 0;
+    for (int v = 0; v < NN; ++v) rsum += cr[nd_szi(ninfo[v])] + de[nd_szi(ninfo[v])];
+    if (bad || bsum + rsum >= BOUND) {
+      if (lane == 0) {
+        R.makespan = -1;
+        R.status = FAR_E_BAD_TIME;
+        P.makespan[inst] = -1;
+        if (P.res) P.res[inst] = R;
+        atomicOr(P.errflag, 1);
+      }
+      return;
+    }
+  }
+
+  if (P.mode == MODE_LOCAL) {
+    solve_local<NC>(P, inst, wsm, L, ninfo, cr, de, lane, R, want_sched, refine);
+    return;
+  }
+  int ms2 = 0, bestk = 0;
   if (n == 0) {
     if (lane == 0) {
       P.makespan[inst] = 0;
@@ -638,17 +758,34 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
 
   // ---- H2: a^{k+1}: grow the longest task (ties -> lowest index) to
   //          argmin_{s > a_j} s*t_j(s) (ties -> smallest s); stop when it is at max size
+  // With t < 2^22 the argmax key (t, lowest index) packs into 32 bits: one REDUX.MAX per
+  // step, and only the lane owning the grown task rescans its tasks.
+  const bool small = tmax < (1 << 22);
   int K = 1;
   {
     unsigned long long cp = c0pack;
-    for (;;) {
-      int lm = -1, lj = INT_MAX;
+    uint32_t* ck = (uint32_t*)start;  // packed current key per task (start[] is free until H7)
+    unsigned lk = 0;
+    if (small) {
       for (int j = lane; j < n; j += 32) {
-        const int t = T[j * NC + cur[j]];
-        if (t > lm) { lm = t; lj = j; }
+        const unsigned key = ((unsigned)T[j * NC + cur[j]] << 10) | (unsigned)(1023 - j);
+        ck[j] = key;
+        lk = max(lk, key);
       }
-      const int m = __reduce_max_sync(FULL, lm);
-      const int jj = (int)__reduce_min_sync(FULL, (unsigned)(lm == m ? lj : INT_MAX));
+    }
+    for (;;) {
+      int jj;
+      if (small) {
+        jj = 1023 - (int)(__reduce_max_sync(FULL, lk) & 1023u);
+      } else {
+        int lm = -1, lj = INT_MAX;
+        for (int j = lane; j < n; j += 32) {
+          const int t = T[j * NC + cur[j]];
+          if (t > lm) { lm = t; lj = j; }
+        }
+        const int m = __reduce_max_sync(FULL, lm);
+        jj = (int)__reduce_min_sync(FULL, (unsigned)(lm == m ? lj : INT_MAX));
+      }
       const int cj = cur[jj];
       if (cj == NC - 1) break;
       if (K >= P.kcap) {  // family larger than this layout holds: defer to the overflow pass
@@ -671,8 +808,13 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         ivl[jj * NC + cj] = (ivl[jj * NC + cj] & 0xFFFFu) | ((uint32_t)K << 16);  // leaves size cj at member K
         ivl[jj * NC + best] = (uint32_t)K | 0xFFFF0000u;                          // enters size best at member K
         cnts[K] = cp;
+        if (small) ck[jj] = ((unsigned)T[jj * NC + best] << 10) | (unsigned)(1023 - jj);
       }
       __syncwarp();
+      if (small && lane == (jj & 31)) {
+        lk = 0;
+        for (int j = lane; j < n; j += 32) lk = max(lk, ck[j]);
+      }
       ++K;
     }
   }
@@ -680,23 +822,20 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
 
   // ---- H3: per-size LPT lists of the (task, size) pairs used by some member, with the
   //          member interval; order (-t(s), task) (Alg. 1 lines 1-2)
-  int off[NC + 1];
   {
-    off[0] = 0;
-#pragma unroll
+    int acc = 0;
     for (int c = 0; c < NC; ++c) {
       int cnt = 0;
       for (int j = lane; j < n; j += 32) cnt += ((ivl[j * NC + c] & 0xFFFFu) != 0xFFFFu);
-      off[c + 1] = off[c] + __reduce_add_sync(FULL, cnt);
+      cnt = __reduce_add_sync(FULL, cnt);
+      if (lane == 0) loff[c] = acc;
+      acc += cnt;
     }
-    if (lane == 0) {
-#pragma unroll
-      for (int c = 0; c <= NC; ++c) loff[c] = off[c];
-    }
+    if (lane == 0) loff[NC] = acc;
+    __syncwarp();
     // compaction (unsorted) into the final segments
-#pragma unroll
     for (int c = 0; c < NC; ++c) {
-      int base = off[c];
+      int base = loff[c];
       for (int j0 = 0; j0 < n; j0 += 32) {
         const int j = j0 + lane;
         uint32_t iv = 0xFFFFFFFFu;
@@ -714,29 +853,35 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       }
     }
     __syncwarp();
-    // rank sort inside each segment -> scratch (ivl is dead), then copy back
+    // sort each segment by (-t, task): warp bitonic sort on packed 32-bit keys when t < 2^22
+    // and the segment has <= 64 entries, else a rank sort through scratch (ivl is dead)
     int2* sent = (int2*)scratch;
     uint16_t* stask = (uint16_t*)(scratch + 8 * L.ecap);
     for (int c = 0; c < NC; ++c) {
-      const int b = off[c], m = off[c + 1] - off[c];
-      for (int e = lane; e < m; e += 32) {
-        const int2 x = lent[b + e];
-        const int tj = ltask[b + e];
-        int rank = 0;
-        for (int f = 0; f < m; ++f) {
-          const int tf = lent[b + f].x;
-          rank += (tf > x.x) || (tf == x.x && (int)ltask[b + f] < tj);
+      const int b = loff[c], m = loff[c + 1] - loff[c];
+      if (m <= 1) continue;
+      if (small && m <= 32) sort_segment<1>(lent + b, ltask + b, m, lane);
+      else if (small && m <= 64) sort_segment<2>(lent + b, ltask + b, m, lane);
+      else {
+        for (int e = lane; e < m; e += 32) {
+          const int2 x = lent[b + e];
+          const int tj = ltask[b + e];
+          int rank = 0;
+          for (int f = 0; f < m; ++f) {
+            const int tf = lent[b + f].x;
+            rank += (tf > x.x) || (tf == x.x && (int)ltask[b + f] < tj);
+          }
+          sent[b + rank] = x;
+          stask[b + rank] = (uint16_t)tj;
         }
-        sent[b + rank] = x;
-        stask[b + rank] = (uint16_t)tj;
+        __syncwarp();
+        for (int p = b + lane; p < b + m; p += 32) {
+          lent[p] = sent[p];
+          ltask[p] = stask[p];
+        }
       }
+      __syncwarp();
     }
-    __syncwarp();
-    for (int p = lane; p < off[NC]; p += 32) {
-      lent[p] = sent[p];
-      ltask[p] = stask[p];
-    }
-    __syncwarp();
   }
 
   // ---- H4: Alg. 1 for every family member, one member per lane
@@ -838,29 +983,32 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   R.makespan_phase2 = bestms;
   ms2 = bestms;
 
-  // ---- H6/H7: node lists of k*, phase 3, replay, guard
+  // ---- H6/H7: node lists of k*, phase 3, replay, keep-best guard.  One call site per
+  // helper (pass 1 only runs when the guard reverts to the phase-2 tree) keeps the code
+  // small enough for the instruction cache.
   uint16_t* nlist = (uint16_t*)scratch;
   int msF = ms2;
-  bool have_starts = false;
-  build_node_lists<NC>(n, bestk, lent, ltask, loff, bestnode, nlist, ncnt, su, lane);
-  if (refine) {
-    if (lane < S) send[lane] = bsend[lane];
-    __syncwarp();
-    int mv, sw, it;
-    long long ev;
-    refine_warp<NC>(n, T, su, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
-    R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
-    const int msR = replay_warp<NC>(n, T, su, nlist, ncnt, nsum, life, start, cur, ninfo, cr, de, lane);
-    if (!(P.flags & FAR_NO_GUARD) && msR > ms2) {
-      R.reverted = 1;  // keep-best guard: return the phase-2 schedule
-      build_node_lists<NC>(n, bestk, lent, ltask, loff, bestnode, nlist, ncnt, su, lane);
-    } else {
-      msF = msR;
-      have_starts = true;
+  const bool need_replay = refine || want_sched;
+  for (int pass = 0; pass < 2; ++pass) {
+    build_node_lists<NC>(n, bestk, lent, ltask, loff, bestnode, nlist, ncnt, su, lane);
+    const bool ref = refine && pass == 0;
+    if (ref) {
+      if (lane < S) send[lane] = bsend[lane];
+      __syncwarp();
+      int mv, sw, it;
+      long long ev;
+      refine_warp<NC>(n, T, su, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
+      R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
     }
-  }
-  if (want_sched && !have_starts) {
-    replay_warp<NC>(n, T, su, nlist, ncnt, nsum, life, start, cur, ninfo, cr, de, lane);  // fixpoint = phase 2
+    if (!need_replay) break;
+    const int msR = replay_warp<NC>(n, T, su, nlist, ncnt, nsum, life, start, cur, ninfo, cr, de, lane);
+    if (ref && !(P.flags & FAR_NO_GUARD) && msR > ms2) {
+      R.reverted = 1;  // keep-best guard: return the phase-2 schedule (replayed in pass 1)
+      if (!want_sched) break;
+      continue;
+    }
+    if (ref) msF = msR;
+    break;
   }
   R.makespan = msF;
   if (want_sched) {
