@@ -66,7 +66,8 @@ enum {
   FAR_NO_REFINE = 1u,     /* skip phase 3 (Alg. 2) and its replay */
   FAR_NO_GUARD = 2u,      /* return the replayed refined schedule even if worse than phase 2 */
   FAR_ZERO_RECONFIG = 4u, /* ignore the ctx's create/destroy costs (all zero) */
-  FAR_NO_SCHEDULE = 8u    /* solve_many: do not write per-task slots (makespans/results only) */
+  FAR_NO_SCHEDULE = 8u,   /* solve_many: do not write per-task slots (makespans/results only) */
+  FAR_EXHAUSTIVE = 16u    /* run Alg. 1 on every family member (disable the exact lower-bound skip) */
 };
 
 typedef struct {
@@ -87,7 +88,10 @@ typedef struct {
   int32_t status;          /* far_status for this instance */
   int32_t reserved;
   int64_t evals;           /* phase 3 move/swap candidate evaluations */
-  int64_t events;          /* Alg. 1 heap pops summed over all family members */
+  int64_t events;          /* Alg. 1 heap pops simulated: summed over every family member with
+                              FAR_EXHAUSTIVE; otherwise over the members not skipped because
+                              their lower bound max(h_max, ceil(area/#slices)) already reaches
+                              the best makespan of earlier members (the result is identical) */
 } far_result;
 
 /* Per-task placement: 8 bytes.  start in ticks from the batch start. */

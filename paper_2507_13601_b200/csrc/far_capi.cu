@@ -130,7 +130,7 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
   if (P.I <= 0) return FAR_OK;
   const bool a30 = ctx->nc == 3;
   const int kmax = 1 + P.n * (ctx->nc - 1);
-  int kfast = std::min(kmax, std::max(64, P.n));
+  int kfast = std::min(kmax, 64);  // M5: P(K > 64) ~ 0.4% -> those go to the overflow pass
   if (P.mode != MODE_SOLVE) kfast = 1;
   const bool need_ovf = P.mode == MODE_SOLVE && kfast < kmax;
   const int slot = (ctx->launch_id++ % (RING / 4)) * 4;

@@ -54,7 +54,7 @@ struct KParams {
 // Per-warp shared-memory layout (bytes), identical on host and device.  kcap bounds the
 // family size K this layout holds (the per-size lists hold at most n + K - 1 entries).
 struct Layout {
-  int times, lent, ltask, cnts, cur, su, bestnode, scratch, lstate, start, misc, bytes, ecap;
+  int times, lent, ltask, cnts, lbk, cur, su, bestnode, scratch, lstate, start, misc, bytes, ecap;
 };
 
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
@@ -71,6 +71,7 @@ __host__ __device__ inline Layout make_layout(int n, int NC, int S, int NN, int 
   L.lent = o;     o = al16(o + 8 * Ecap);
   L.ltask = o;    o = al16(o + 2 * Ecap);
   L.cnts = o;     o = al16(o + 8 * kcap);
+  L.lbk = o;      o = al16(o + 4 * kcap);
   L.cur = o;      o = al16(o + n);
   L.su = o;       o = al16(o + n);
   L.bestnode = o; o = al16(o + n);
@@ -81,13 +82,13 @@ __host__ __device__ inline Layout make_layout(int n, int NC, int S, int NN, int 
   L.scratch = o;  o = al16(o + sc);
   L.lstate = o;   o = al16(o + 4 * NC * 32);
   L.start = o;    o = al16(o + 4 * n);
-  L.misc = o;     o = al16(o + 4 * 160);
+  L.misc = o;     o = al16(o + 4 * 192);
   L.bytes = o;
   return L;
 }
 
 // misc int slots
-enum { M_LOFF = 0, M_NCNT = 8, M_NSUM = 24, M_SEND = 40, M_BSEND = 48, M_LIFE = 56 };
+enum { M_LOFF = 0, M_NCNT = 8, M_NSUM = 24, M_SEND = 40, M_BSEND = 48, M_LIFE = 56, M_MEMB = 152 };
 
 __device__ __forceinline__ long long warp_sum_ll(long long v) {
 #pragma unroll
@@ -647,6 +648,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   int2* lent = (int2*)(wsm + L.lent);
   uint16_t* ltask = (uint16_t*)(wsm + L.ltask);
   unsigned long long* cnts = (unsigned long long*)(wsm + L.cnts);
+  int* lbk = (int*)(wsm + L.lbk);
   uint8_t* cur = wsm + L.cur;
   uint8_t* su = wsm + L.su;
   uint8_t* bestnode = wsm + L.bestnode;
@@ -731,6 +733,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   // ---- H1: first allocation a^1_i = argmin_s s*t_i(s), ties -> smallest s
   uint32_t* ivl = (uint32_t*)scratch;  // [n][NC] member interval lo | hi<<16 (0xFFFF = absent/open)
   unsigned long long c0pack = 0;
+  long long W = 0;  // total area sum_i a_i t_i(a_i) of the current member (uniform)
   {
     int cnt_c[NC];
 #pragma unroll
@@ -744,6 +747,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         if (w < bw) { bw = w; best = c; }
       }
       cur[j] = (uint8_t)best;
+      W += bw;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         cnt_c[c] += (c == best);
@@ -752,6 +756,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c) c0pack |= (unsigned long long)__reduce_add_sync(FULL, cnt_c[c]) << (11 * c);
+    W = warp_sum_ll(W);
   }
   if (lane == 0) cnts[0] = c0pack;
   __syncwarp();
@@ -774,18 +779,23 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       }
     }
     for (;;) {
-      int jj;
+      int jj, hmax;
       if (small) {
-        jj = 1023 - (int)(__reduce_max_sync(FULL, lk) & 1023u);
+        const unsigned gk = __reduce_max_sync(FULL, lk);
+        jj = 1023 - (int)(gk & 1023u);
+        hmax = (int)(gk >> 10);
       } else {
         int lm = -1, lj = INT_MAX;
         for (int j = lane; j < n; j += 32) {
           const int t = T[j * NC + cur[j]];
           if (t > lm) { lm = t; lj = j; }
         }
-        const int m = __reduce_max_sync(FULL, lm);
-        jj = (int)__reduce_min_sync(FULL, (unsigned)(lm == m ? lj : INT_MAX));
+        hmax = __reduce_max_sync(FULL, lm);
+        jj = (int)__reduce_min_sync(FULL, (unsigned)(lm == hmax ? lj : INT_MAX));
       }
+      // lower bound of member K-1's Alg. 1 makespan: its longest task and its area spread
+      // over all slices (reconfiguration only adds idle time) -- used to prune phase 2
+      if (lane == 0) lbk[K - 1] = max(hmax, (int)((W + S - 1) / S));
       const int cj = cur[jj];
       if (cj == NC - 1) break;
       if (K >= P.kcap) {  // family larger than this layout holds: defer to the overflow pass
@@ -802,6 +812,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         if (best < 0 || w < bw) { bw = w; best = c; }
       }
       cp = cp - (1ull << (11 * cj)) + (1ull << (11 * best));
+      W += (long long)size_of<NC>(best) * T[jj * NC + best] - (long long)size_of<NC>(cj) * T[jj * NC + cj];
       __syncwarp();
       if (lane == 0) {
         cur[jj] = (uint8_t)best;
@@ -888,11 +899,36 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   uint8_t* recnode = scratch;  // [n][32]: node of task j in this lane's member
   int bestms = INT_MAX;
   long long events = 0;
-  for (int kb = 0; kb < K; kb += 32) {
-    const int k = kb + lane;
+  // Members are taken in increasing k, 32 per pass; a member whose lower bound LB_k
+  // (H2) is >= the best makespan of the earlier passes cannot become k* = argmin
+  // (makespan, k) and is skipped (exact; FAR_EXHAUSTIVE disables it).
+  const bool prune = !(P.flags & FAR_EXHAUSTIVE);
+  int* memb = misc + M_MEMB;
+  int nextk = 0;
+  while (nextk < K) {
+    int got = 0;
+    while (got < 32 && nextk < K) {
+      const int cand = nextk + lane;
+      const bool ok = cand < K && (!prune || lbk[cand] < bestms);
+      const unsigned bal = __ballot_sync(FULL, ok);
+      const int pos = __popc(bal & ((1u << lane) - 1));
+      const int need = 32 - got;
+      if (ok && pos < need) memb[got + pos] = cand;
+      const unsigned over = __ballot_sync(FULL, ok && pos == need);
+      if (over) {
+        nextk += __ffs(over) - 1;
+        got = 32;
+      } else {
+        got += __popc(bal);
+        nextk += 32;
+      }
+    }
+    __syncwarp();
+    if (got == 0) break;
+    const int k = lane < got ? memb[lane] : -1;
     int ms = INT_MAX, pops = 0;
     int sl[S];  // slice ends of this lane's member at termination
-    if (k < K) {
+    if (k >= 0) {
       const unsigned long long cp = cnts[k];
       int total = 0;
 #pragma unroll
@@ -963,12 +999,12 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     events += warp_sum_ll(pops);
     // ---- H5: k* = argmin (makespan_k, k)
     const int m = __reduce_min_sync(FULL, ms);
-    const int kw = (int)__reduce_min_sync(FULL, (unsigned)(ms == m ? k : INT_MAX));
+    const int kw = (int)__reduce_min_sync(FULL, (unsigned)(k >= 0 && ms == m ? k : INT_MAX));
     __syncwarp();
     if (m < bestms) {
       bestms = m;
       bestk = kw;
-      const int wl = kw - kb;
+      const int wl = __ffs(__ballot_sync(FULL, k == kw)) - 1;
       for (int j = lane; j < n; j += 32) bestnode[j] = recnode[j * 32 + wl];
 #pragma unroll
       for (int s = 0; s < S; ++s) {

@@ -8,7 +8,7 @@ from paper_2507_13601_b200 import far, inputs
 pytestmark = pytest.mark.gpu
 
 FIELDS = ("makespan", "makespan_phase2", "alloc_index", "family_size", "moves", "swaps", "iterations", "reverted",
-          "evals", "events")
+          "evals")
 
 
 @pytest.fixture(scope="module")
@@ -36,6 +36,11 @@ def check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=0, max_it
     assert len(bad) == 0, f"makespan mismatch at {bad[:10]}: gpu {ms[bad[:5]]} oracle {oms[bad[:5]]}"
     for k in FIELDS:
         assert (res[k] == ores[k]).all(), f"{k} mismatch at {np.nonzero(res[k] != ores[k])[0][:10]}"
+    # Alg. 1 pops: all members with FAR_EXHAUSTIVE, otherwise only the members not skipped
+    if flags & far.EXHAUSTIVE:
+        assert (res["events"] == ores["events"]).all()
+    else:
+        assert (res["events"] <= ores["events"]).all() and (res["events"] > 0).sum() == (ores["events"] > 0).sum()
     if full and slots is not None:
         for i in range(tab.shape[0]):
             o = O.far(profile, costs, tab[i], max_iterations=max_iterations, min_improvement_ppm=ppm, flags=oflags)
@@ -45,12 +50,13 @@ def check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=0, max_it
             assert (slots[i]["start"] == os_["start"]).all(), f"start mismatch instance {i}"
 
 
-@pytest.mark.parametrize("wname,count", [("M1", 2000), ("M2", 2000), ("M3", 1000)])
+@pytest.mark.parametrize("wname,count", [("M1", 2000), ("M2", 2000), ("M3", 1000), ("M5", 300)])
 def test_workload_samples_bitexact(O, torch_dev, wname, count):
     w = inputs.WORKLOADS[wname]
     tab = w.table(count=count)
-    ms, slots, res = run_gpu(torch_dev, w.profile, w.costs(), tab)
-    check_against_oracle(O, w.profile, w.costs(), tab, ms, slots, res, full=True)
+    for flags in (0, far.EXHAUSTIVE):
+        ms, slots, res = run_gpu(torch_dev, w.profile, w.costs(), tab, flags=flags)
+        check_against_oracle(O, w.profile, w.costs(), tab, ms, slots, res, flags=flags, full=True)
 
 
 @pytest.mark.parametrize("profile", ["A30", "A100", "H100"])
@@ -79,7 +85,8 @@ def test_tie_and_nonmonotone_inputs(O, torch_dev, profile, gen):
         check_against_oracle(O, profile, costs, tab, ms, slots, res)
 
 
-@pytest.mark.parametrize("flags,max_it,ppm", [(far.NO_REFINE, 100, 0), (far.NO_GUARD, 100, 0),
+@pytest.mark.parametrize("flags,max_it,ppm", [(far.EXHAUSTIVE, 100, 0), (far.EXHAUSTIVE | far.NO_REFINE, 100, 0),
+                                               (far.NO_REFINE, 100, 0), (far.NO_GUARD, 100, 0),
                                                (far.ZERO_RECONFIG, 100, 0), (0, 0, 0), (0, 1, 0), (0, 3, 0),
                                                (0, 100, 20000)])
 def test_options(O, torch_dev, flags, max_it, ppm):
