@@ -54,7 +54,7 @@ struct KParams {
 // Per-warp shared-memory layout (bytes), identical on host and device.  kcap bounds the
 // family size K this layout holds (the per-size lists hold at most n + K - 1 entries).
 struct Layout {
-  int times, lent, ltask, cnts, lbk, cur, su, bestnode, scratch, lstate, start, misc, bytes, ecap;
+  int times, lent, ltask, cnts, lbw, lbh, cur, su, bestnode, scratch, lstate, start, misc, bytes, ecap, scr;
 };
 
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
@@ -71,7 +71,8 @@ __host__ __device__ inline Layout make_layout(int n, int NC, int S, int NN, int 
   L.lent = o;     o = al16(o + 8 * Ecap);
   L.ltask = o;    o = al16(o + 2 * Ecap);
   L.cnts = o;     o = al16(o + 8 * kcap);
-  L.lbk = o;      o = al16(o + 4 * kcap);
+  L.lbw = o;      o = al16(o + 8 * kcap);
+  L.lbh = o;      o = al16(o + 4 * kcap);
   L.cur = o;      o = al16(o + n);
   L.su = o;       o = al16(o + n);
   L.bestnode = o; o = al16(o + n);
@@ -80,6 +81,7 @@ __host__ __device__ inline Layout make_layout(int n, int NC, int S, int NN, int 
   if (4 * n * NC > sc) sc = 4 * n * NC;         // phase-1 member intervals
   if (2 * NN * n > sc) sc = 2 * NN * n;         // node lists
   L.scratch = o;  o = al16(o + sc);
+  L.scr = sc;
   L.lstate = o;   o = al16(o + 4 * NC * 32);
   L.start = o;    o = al16(o + 4 * n);
   L.misc = o;     o = al16(o + 4 * 192);
@@ -490,6 +492,27 @@ __device__ __forceinline__ void warp_bitonic(unsigned (&key)[R], unsigned (&val)
   }
 }
 
+// Warp in-place bitonic sort of P (power of two) packed (key, val) pairs in shared memory.
+__device__ void smem_bitonic(unsigned* key, unsigned* val, int P, int lane) {
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = lane; t < (P >> 1); t += 32) {
+        const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const int l = i | j;
+        const bool up = (i & k) == 0;
+        const unsigned a = key[i], b = key[l];
+        if ((a > b) == up) {
+          key[i] = b;
+          key[l] = a;
+          const unsigned va = val[i];
+          val[i] = val[l];
+          val[l] = va;
+        }
+      }
+      __syncwarp();
+    }
+}
+
 // Sort one LPT list segment (t < 2^22, m <= 32*R) by (-t, task) with the packed key
 // ((2^22 - 1 - t) << 10) | task.
 template <int R>
@@ -648,7 +671,8 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   int2* lent = (int2*)(wsm + L.lent);
   uint16_t* ltask = (uint16_t*)(wsm + L.ltask);
   unsigned long long* cnts = (unsigned long long*)(wsm + L.cnts);
-  int* lbk = (int*)(wsm + L.lbk);
+  long long* lbw = (long long*)(wsm + L.lbw);  // area of each member
+  int* lbh = (int*)(wsm + L.lbh);              // longest task of each member
   uint8_t* cur = wsm + L.cur;
   uint8_t* su = wsm + L.su;
   uint8_t* bestnode = wsm + L.bestnode;
@@ -748,6 +772,20 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       }
       cur[j] = (uint8_t)best;
       W += bw;
+      // next size for phase-1 growth: nx(c) = argmin_{c' > c} (size(c') t(c'), c')
+      {
+        unsigned packed = 0;
+        int above = NC - 1;
+        long long wa = (long long)size_of<NC>(NC - 1) * T[j * NC + NC - 1];
+#pragma unroll
+        for (int c = NC - 2; c >= 0; --c) {
+          packed |= (unsigned)above << (3 * c);
+          const long long wc = (long long)size_of<NC>(c) * T[j * NC + c];
+          if (wc <= wa) { wa = wc; above = c; }
+        }
+        su[j] = (uint8_t)(packed & 0xFF);
+        bestnode[j] = (uint8_t)(packed >> 8);
+      }
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         cnt_c[c] += (c == best);
@@ -795,7 +833,10 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       }
       // lower bound of member K-1's Alg. 1 makespan: its longest task and its area spread
       // over all slices (reconfiguration only adds idle time) -- used to prune phase 2
-      if (lane == 0) lbk[K - 1] = max(hmax, (int)((W + S - 1) / S));
+      if (lane == 0) {
+        lbh[K - 1] = hmax;
+        lbw[K - 1] = W;
+      }
       const int cj = cur[jj];
       if (cj == NC - 1) break;
       if (K >= P.kcap) {  // family larger than this layout holds: defer to the overflow pass
@@ -805,12 +846,8 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         }
         return;
       }
-      int best = -1;
-      long long bw = 0;
-      for (int c = cj + 1; c < NC; ++c) {
-        const long long w = (long long)size_of<NC>(c) * T[jj * NC + c];
-        if (best < 0 || w < bw) { bw = w; best = c; }
-      }
+      const unsigned nxp = (unsigned)su[jj] | ((unsigned)bestnode[jj] << 8);
+      const int best = (int)((nxp >> (3 * cj)) & 7u);
       cp = cp - (1ull << (11 * cj)) + (1ull << (11 * best));
       W += (long long)size_of<NC>(best) * T[jj * NC + best] - (long long)size_of<NC>(cj) * T[jj * NC + cj];
       __syncwarp();
@@ -873,7 +910,27 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       if (m <= 1) continue;
       if (small && m <= 32) sort_segment<1>(lent + b, ltask + b, m, lane);
       else if (small && m <= 64) sort_segment<2>(lent + b, ltask + b, m, lane);
-      else {
+      else if (small && 8 * (1 << (32 - __clz(m - 1))) <= L.scr) {
+        // larger lists: bitonic in scratch (ivl is dead), padded to a power of two
+        const int P2 = 1 << (32 - __clz(m - 1));
+        unsigned* kk = (unsigned*)scratch;
+        unsigned* vv = kk + P2;
+        for (int i = lane; i < P2; i += 32) {
+          if (i < m) {
+            const int2 x = lent[b + i];
+            kk[i] = ((unsigned)(0x3FFFFF - x.x) << 10) | (unsigned)ltask[b + i];
+            vv[i] = (unsigned)x.y;
+          } else {
+            kk[i] = 0xFFFFFFFFu;
+          }
+        }
+        __syncwarp();
+        smem_bitonic(kk, vv, P2, lane);
+        for (int i = lane; i < m; i += 32) {
+          lent[b + i] = make_int2(0x3FFFFF - (int)(kk[i] >> 10), (int)vv[i]);
+          ltask[b + i] = (uint16_t)(kk[i] & 1023u);
+        }
+      } else {
         for (int e = lane; e < m; e += 32) {
           const int2 x = lent[b + e];
           const int tj = ltask[b + e];
@@ -909,7 +966,8 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     int got = 0;
     while (got < 32 && nextk < K) {
       const int cand = nextk + lane;
-      const bool ok = cand < K && (!prune || lbk[cand] < bestms);
+      // prune iff max(h_k, ceil(W_k / S)) >= bestms  <=>  h_k >= bestms || W_k > S*(bestms-1)
+      const bool ok = cand < K && (!prune || (lbh[cand] < bestms && lbw[cand] <= (long long)S * (bestms - 1)));
       const unsigned bal = __ballot_sync(FULL, ok);
       const int pos = __popc(bal & ((1u << lane) - 1));
       const int need = 32 - got;
