@@ -363,15 +363,13 @@ __device__ void refine_warp(int n, const int32_t* T, const uint8_t* su, uint16_t
           }
         }
         const unsigned dmin = __reduce_min_sync(FULL, bd);
+        // an operation is one or two transfers (task, from, to); one call site keeps code small
+        int nt = 0, tk0 = 0, tk1 = 0, delta = 0;
         if (dmin != UINT_MAX) {
-          const int Tm = __reduce_min_sync(FULL, (unsigned)(bd == dmin ? bj : INT_MAX));
-          const int t = dur_of<NC>(T, su, Tm);
-          list_remove<NC>(LI, &ncnt[I], Tm, lane);
-          list_insert<NC>(LA, &ncnt[A], Tm, T, su, lane);
-          add_on(wI, -t);
-          add_on(ninfo[A], t);
+          tk0 = __reduce_min_sync(FULL, (unsigned)(bd == dmin ? bj : INT_MAX));
+          delta = dur_of<NC>(T, su, tk0);
+          nt = 1;
           ++moves;
-          done = true;
         } else {
           const int nA = ncnt[A];
           evals += (long long)nI * nA;
@@ -380,9 +378,9 @@ __device__ void refine_warp(int n, const int32_t* T, const uint8_t* su, uint16_t
           for (int p = lane; p < tot; p += 32) {
             const int qi = p / nA, qa = p - qi * nA;
             const int k = LI[qi], j = LA[qa];
-            const int delta = dur_of<NC>(T, su, k) - dur_of<NC>(T, su, j);
-            if (0 < delta && delta < m) {
-              const unsigned d = (unsigned)abs(2 * delta - m);
+            const int dl = dur_of<NC>(T, su, k) - dur_of<NC>(T, su, j);
+            if (0 < dl && dl < m) {
+              const unsigned d = (unsigned)abs(2 * dl - m);
               const unsigned key = ((unsigned)k << 10) | (unsigned)j;
               if (d < bd2 || (d == bd2 && key < bkey)) { bd2 = d; bkey = key; }
             }
@@ -390,17 +388,22 @@ __device__ void refine_warp(int n, const int32_t* T, const uint8_t* su, uint16_t
           const unsigned d2 = __reduce_min_sync(FULL, bd2);
           if (d2 != UINT_MAX) {
             const unsigned key = __reduce_min_sync(FULL, bd2 == d2 ? bkey : UINT_MAX);
-            const int k = (int)(key >> 10), j = (int)(key & 1023);
-            const int delta = dur_of<NC>(T, su, k) - dur_of<NC>(T, su, j);
-            list_remove<NC>(LI, &ncnt[I], k, lane);
-            list_remove<NC>(LA, &ncnt[A], j, lane);
-            list_insert<NC>(LA, &ncnt[A], k, T, su, lane);
-            list_insert<NC>(LI, &ncnt[I], j, T, su, lane);
-            add_on(wI, -delta);
-            add_on(ninfo[A], delta);
+            tk0 = (int)(key >> 10);
+            tk1 = (int)(key & 1023);
+            delta = dur_of<NC>(T, su, tk0) - dur_of<NC>(T, su, tk1);
+            nt = 2;
             ++swaps;
-            done = true;
           }
+        }
+        for (int x = 0; x < nt; ++x) {  // move: I->A; swap: K I->A then J A->I (same final lists)
+          const int from = x == 0 ? I : A, to = x == 0 ? A : I, task = x == 0 ? tk0 : tk1;
+          list_remove<NC>(nlist + from * n, &ncnt[from], task, lane);
+          list_insert<NC>(nlist + to * n, &ncnt[to], task, T, su, lane);
+        }
+        if (nt) {
+          add_on(wI, -delta);
+          add_on(ninfo[A], delta);
+          done = true;
         }
       }
       if (!done) {
@@ -453,45 +456,6 @@ __device__ void build_node_lists(int n, int k, const int2* lent, const uint16_t*
   }
 }
 
-// Warp bitonic sort of 32*R (key, val) pairs held in registers (element i = r*32 + lane),
-// ascending by key.  Keys are unique (they carry the task index), padding is 0xFFFFFFFF.
-template <int R>
-__device__ __forceinline__ void warp_bitonic(unsigned (&key)[R], unsigned (&val)[R], int lane) {
-#pragma unroll
-  for (int k = 2; k <= 32 * R; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j >= 32) {
-        const int rj = j >> 5;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if ((r & rj) == 0) {
-            const int r2 = r | rj;
-            const bool up = (((r << 5) | lane) & k) == 0;
-            const bool sw = up ? (key[r] > key[r2]) : (key[r] < key[r2]);
-            const unsigned k0 = key[r], v0 = val[r];
-            key[r] = sw ? key[r2] : k0;
-            val[r] = sw ? val[r2] : v0;
-            key[r2] = sw ? k0 : key[r2];
-            val[r2] = sw ? v0 : val[r2];
-          }
-        }
-      } else {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const unsigned ok = __shfl_xor_sync(FULL, key[r], j);
-          const unsigned ov = __shfl_xor_sync(FULL, val[r], j);
-          const bool lower = (lane & j) == 0;
-          const bool up = (((r << 5) | lane) & k) == 0;
-          const bool take = (lower == up) ? (ok < key[r]) : (ok > key[r]);
-          key[r] = take ? ok : key[r];
-          val[r] = take ? ov : val[r];
-        }
-      }
-    }
-  }
-}
-
 // Warp in-place bitonic sort of P (power of two) packed (key, val) pairs in shared memory.
 __device__ void smem_bitonic(unsigned* key, unsigned* val, int P, int lane) {
   for (int k = 2; k <= P; k <<= 1)
@@ -511,34 +475,6 @@ __device__ void smem_bitonic(unsigned* key, unsigned* val, int P, int lane) {
       }
       __syncwarp();
     }
-}
-
-// Sort one LPT list segment (t < 2^22, m <= 32*R) by (-t, task) with the packed key
-// ((2^22 - 1 - t) << 10) | task.
-template <int R>
-__device__ void sort_segment(int2* ent, uint16_t* tsk, int m, int lane) {
-  unsigned key[R], val[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = r * 32 + lane;
-    if (i < m) {
-      const int2 x = ent[i];
-      key[r] = ((unsigned)(0x3FFFFF - x.x) << 10) | (unsigned)tsk[i];
-      val[r] = (unsigned)x.y;
-    } else {
-      key[r] = 0xFFFFFFFFu;
-      val[r] = 0;
-    }
-  }
-  warp_bitonic<R>(key, val, lane);
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = r * 32 + lane;
-    if (i < m) {
-      ent[i] = make_int2(0x3FFFFF - (int)(key[r] >> 10), (int)val[r]);
-      tsk[i] = (uint16_t)(key[r] & 1023u);
-    }
-  }
 }
 
 // Phase 3 + replay + guard on an input schedule (far_local_search, MODE_LOCAL).
@@ -908,9 +844,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     for (int c = 0; c < NC; ++c) {
       const int b = loff[c], m = loff[c + 1] - loff[c];
       if (m <= 1) continue;
-      if (small && m <= 32) sort_segment<1>(lent + b, ltask + b, m, lane);
-      else if (small && m <= 64) sort_segment<2>(lent + b, ltask + b, m, lane);
-      else if (small && 8 * (1 << (32 - __clz(m - 1))) <= L.scr) {
+      if (small && 8 * (1 << (32 - __clz(m - 1))) <= L.scr) {
         // larger lists: bitonic in scratch (ivl is dead), padded to a power of two
         const int P2 = 1 << (32 - __clz(m - 1));
         unsigned* kk = (unsigned*)scratch;

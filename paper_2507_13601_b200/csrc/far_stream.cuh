@@ -213,6 +213,17 @@ __device__ SeamRes eval_seam(int n, const int32_t* T, const uint8_t* su, const u
   return R;
 }
 
+// Move task k from node I to node A and (swap) task j from A to I, keeping lists ordered.
+template <int NC>
+__device__ __noinline__ void transfer(int n, uint16_t* nl, int* ncnt, int I, int A, int k, int j, const int32_t* T,
+                                      const uint8_t* su, int lane) {
+  for (int x = 0; x < (j >= 0 ? 2 : 1); ++x) {
+    const int from = x == 0 ? I : A, to = x == 0 ? A : I, task = x == 0 ? k : j;
+    list_remove<NC>(nl + from * n, &ncnt[from], task, lane);
+    list_insert<NC>(nl + to * n, &ncnt[to], task, T, su, lane);
+  }
+}
+
 template <int NC>
 __device__ void copy_lists(int n, const uint16_t* a, const int* ca, uint16_t* b, int* cb, int lane) {
   constexpr int NN = Tree<NC>::NN;
@@ -356,8 +367,7 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
             if (dmin != LL_MAX) {
               const int Tm = (int)__reduce_min_sync(FULL, (unsigned)(bd == dmin ? bj : INT_MAX));
               copy_lists<NC>(n, nl, ncnt, nl2, ncnt2, lane);
-              list_remove<NC>(nl2 + I * n, &ncnt2[I], Tm, lane);
-              list_insert<NC>(nl2 + A * n, &ncnt2[A], Tm, T, su, lane);
+              transfer<NC>(n, nl2, ncnt2, I, A, Tm, -1, T, su, lane);
               SeamRes e2 = eval_seam<NC>(n, T, su, nl2, ncnt2, nsum, onode, start, life, ninfo, cr, de, true, st, win, lane);
               if (e2.end < cur.end) {
                 copy_lists<NC>(n, nl2, ncnt2, nl, ncnt, lane);
@@ -385,10 +395,7 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
                 const unsigned key = __reduce_min_sync(FULL, bd2 == d2 ? bkey : UINT_MAX);
                 const int kk = (int)(key >> 10), jj = (int)(key & 1023);
                 copy_lists<NC>(n, nl, ncnt, nl2, ncnt2, lane);
-                list_remove<NC>(nl2 + I * n, &ncnt2[I], kk, lane);
-                list_remove<NC>(nl2 + A * n, &ncnt2[A], jj, lane);
-                list_insert<NC>(nl2 + A * n, &ncnt2[A], kk, T, su, lane);
-                list_insert<NC>(nl2 + I * n, &ncnt2[I], jj, T, su, lane);
+                transfer<NC>(n, nl2, ncnt2, I, A, kk, jj, T, su, lane);
                 SeamRes e2 = eval_seam<NC>(n, T, su, nl2, ncnt2, nsum, onode, start, life, ninfo, cr, de, true, st, win, lane);
                 if (e2.end < cur.end) {
                   copy_lists<NC>(n, nl2, ncnt2, nl, ncnt, lane);
