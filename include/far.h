@@ -20,8 +20,9 @@
  *     the profile's order: A30 {1,2,4}; A100/H100 {1,2,3,4,7}.  Many
  *     instances: [I][n][nsizes].
  *   - Integer range: per instance, sum_i max_s t_i(s) + sum over tree nodes of
- *     (t_create + t_destroy) must be < 2^30, so every makespan, start and the
- *     |2x - m| comparisons of Alg. 2 fit in int32.  Violations: FAR_E_BAD_TIME.
+ *     (t_create + t_destroy) must be < 2^29, so every makespan, start and the
+ *     |2x - m| comparisons of Alg. 2 fit in int32 and a frontier key (end << 3 |
+ *     first slice) fits in 32 bits.  Violations: FAR_E_BAD_TIME.
  *   - Tree node ids (far_task_slot.node) index the fixed repartitioning trees of
  *     Fig. 3: A30 0=[0,4) 1=[0,2) 2=[2,4) 3..6 = leaves S0..S3;
  *     A100/H100 0=[0,7) 1=[0,4) (hosts sizes 4 then 3) 2=[4,7) 3=[0,2) 4=[2,4)

@@ -123,7 +123,7 @@ int load_problem(int profile, const int32_t* costs, const int32_t* times, int n,
     bound += mx;
   }
   for (size_t v = 0; v < P.m.node.size(); ++v) bound += P.c.cr(P.m, (int)v) + P.c.de(P.m, (int)v);
-  if (bound >= (i64(1) << 30)) return -3;
+  if (bound >= (i64(1) << 29)) return -3;
   return 0;
 }
 

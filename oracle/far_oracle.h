@@ -13,7 +13,7 @@
  *   negative cost, or the makespan bound below exceeded), -4 too large.
  * Makespan bound (same rule as the CUDA path):
  *   sum_i max_c t_i(c) + sum_{tree nodes v} (t_create(|v|) + t_destroy(|v|))
- *   must be < 2^30.
+ *   must be < 2^29.
  */
 #ifndef FAR_ORACLE_H
 #define FAR_ORACLE_H

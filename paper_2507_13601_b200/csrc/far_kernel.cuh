@@ -27,7 +27,7 @@ namespace farb {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int MAXN = 1024;
-constexpr int BOUND = 1 << 30;
+constexpr int BOUND = 1 << 29;
 enum { MODE_SOLVE = 0, MODE_LOCAL = 1 };
 
 struct KParams {
@@ -68,8 +68,8 @@ __host__ __device__ inline Layout make_layout(int n, int NC, int S, int NN, int 
   L.ecap = Ecap;
   int o = 0;
   L.times = o;    o = al16(o + 4 * n * NC);
-  L.lent = o;     o = al16(o + 8 * Ecap);
-  L.ltask = o;    o = al16(o + 2 * Ecap);
+  L.lent = o;     o = al16(o + 8 * (Ecap + 1));
+  L.ltask = o;    o = al16(o + 2 * (Ecap + 1));
   L.cnts = o;     o = al16(o + 8 * kcap);
   L.lbw = o;      o = al16(o + 8 * kcap);
   L.lbh = o;      o = al16(o + 4 * kcap);
@@ -84,13 +84,14 @@ __host__ __device__ inline Layout make_layout(int n, int NC, int S, int NN, int 
   L.scr = sc;
   L.lstate = o;   o = al16(o + 4 * NC * 32);
   L.start = o;    o = al16(o + 4 * n);
-  L.misc = o;     o = al16(o + 4 * 192);
+  L.misc = o;     o = al16(o + 4 * 224);
   L.bytes = o;
   return L;
 }
 
 // misc int slots
-enum { M_LOFF = 0, M_NCNT = 8, M_NSUM = 24, M_SEND = 40, M_BSEND = 48, M_LIFE = 56, M_MEMB = 152 };
+enum { M_LOFF = 0, M_NCNT = 8, M_NSUM = 24, M_SEND = 40, M_BSEND = 48, M_LIFE = 56, M_MEMB = 152, M_NINFO = 184,
+       M_CR = 200, M_DE = 208 };
 
 __device__ __forceinline__ long long warp_sum_ll(long long v) {
 #pragma unroll
@@ -112,30 +113,40 @@ template <int NC> __device__ __forceinline__ int leaf_of(int s) {
 // time, and whether it already has tasks.  Pop = min (end, slot) by an unrolled scan.
 // ---------------------------------------------------------------------------
 template <int S> struct Frontier {
-  int e[S];
+  // e[s] = end << 3 | s (ends < 2^29, include/far.h "Integer range"); 0xFFFFFFFF = empty.
+  // The unsigned min over the slots is exactly the (end, first slice) tie-break.
+  unsigned e[S];
   uint32_t slotnode = 0, live = 1, has = 0;
   __device__ __forceinline__ void init() {
 #pragma unroll
-    for (int s = 0; s < S; ++s) e[s] = INT_MAX;
+    for (int s = 0; s < S; ++s) e[s] = 0xFFFFFFFFu;
     e[0] = 0;
     slotnode = 0;  // root (node 0) in slot 0
     live = 1;
     has = 0;
   }
   __device__ __forceinline__ void pop(int& bs, int& be) const {
-    bs = 0;
-    be = e[0];
+    unsigned m;
+    if (S == 7) {
+      m = min(min(min(e[0], e[1]), min(e[2], e[3])), min(min(e[4], e[5]), e[S - 1]));
+    } else {
+      m = e[0];
 #pragma unroll
-    for (int s = 1; s < S; ++s) {
-      const bool lt = e[s] < be;
-      be = lt ? e[s] : be;
-      bs = lt ? s : bs;
+      for (int s = 1; s < S; ++s) m = min(m, e[s]);
     }
+    bs = (int)(m & 7u);
+    be = (int)(m >> 3);
   }
   __device__ __forceinline__ void set(int bs, int v) {
+    const unsigned key = ((unsigned)v << 3) | (unsigned)bs;
 #pragma unroll
-    for (int s = 0; s < S; ++s) e[s] = (s == bs) ? v : e[s];
+    for (int s = 0; s < S; ++s) e[s] = (s == bs) ? key : e[s];
   }
+  __device__ __forceinline__ void clear(int bs) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) e[s] = (s == bs) ? 0xFFFFFFFFu : e[s];
+  }
+  __device__ __forceinline__ int endv(int s) const { return (int)(e[s] >> 3); }
   __device__ __forceinline__ int node(int s) const { return (slotnode >> (4 * s)) & 15; }
   // Alg. 1 lines 17-24 (repartitioning) after the optional destroy; returns false if v was a leaf.
   __device__ __forceinline__ bool split(int bs, int be, uint32_t w) {
@@ -150,7 +161,7 @@ template <int S> struct Frontier {
       return true;
     }
     live &= ~(1u << bs);
-    set(bs, INT_MAX);
+    clear(bs);
     return false;
   }
 };
@@ -926,7 +937,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         const int r = (int)((cp >> (11 * c)) & 2047);
-        lstate[c * 32 + lane] = (uint32_t)r << 16;
+        lstate[c * 32 + lane] = ((uint32_t)r << 16) | (uint32_t)loff[c];  // remaining | absolute cursor
         total += r;
       }
       Frontier<S> F;
@@ -955,17 +966,17 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
             be = rec;
             F.has |= 1u << bs;
           }
-          // line 12: longest unscheduled task of size c for member k (skip other members' entries)
+          // line 12: longest unscheduled task of size c for member k (skip other members'
+          // entries; two entries per step -- the list has one padding entry)
           int p = (int)(sv & 0xFFFFu);
-          const int base = loff[c];
           int2 ent;
           for (;;) {
-            ent = lent[base + p];
-            ++p;
-            const int lo = ent.y & 0xFFFF, hi = (int)((unsigned)ent.y >> 16);
-            if (lo <= k && k < hi) break;
+            const int2 e0 = lent[p], e1 = lent[p + 1];
+            if ((e0.y & 0xFFFF) <= k && k < (int)((unsigned)e0.y >> 16)) { ent = e0; p += 1; break; }
+            if ((e1.y & 0xFFFF) <= k && k < (int)((unsigned)e1.y >> 16)) { ent = e1; p += 2; break; }
+            p += 2;
           }
-          recnode[(int)ltask[base + p - 1] * 32 + lane] = (uint8_t)v;
+          recnode[(int)ltask[p - 1] * 32 + lane] = (uint8_t)v;
           lstate[c * 32 + lane] = ((sv & 0xFFFF0000u) - 0x10000u) | (uint32_t)p;
           be += ent.x;  // lines 13-15
           ms = max(ms, be);
@@ -985,7 +996,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         if ((F.live >> s) & 1) {
           const int sz = nd_sz(ninfo[F.node(s)]);
 #pragma unroll
-          for (int q = 0; q < S; ++q) sl[q] = (q >= s && q < s + sz) ? F.e[s] : sl[q];
+          for (int q = 0; q < S; ++q) sl[q] = (q >= s && q < s + sz) ? F.endv(s) : sl[q];
         }
     }
     events += warp_sum_ll(pops);
@@ -1080,13 +1091,26 @@ __global__ void __launch_bounds__(128) far_solve_kernel(KParams P) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Layout L = make_layout(P.n, NC, Tree<NC>::S, NN, P.kcap);
   unsigned char* wsm = smem + (size_t)warp * L.bytes;
+  // per-warp copies of the node table and costs (addressed off the warp's base register)
+  {
+    int* misc = (int*)(wsm + L.misc);
+    if (lane < 16) misc[M_NINFO + lane] = (int)ninfo[lane];
+    if (lane < 8) {
+      misc[M_CR + lane] = cr[lane];
+      misc[M_DE + lane] = de[lane];
+    }
+    __syncwarp();
+  }
+  const uint32_t* wninfo = (const uint32_t*)(wsm + L.misc) + M_NINFO;
+  const int* wcr = (const int*)(wsm + L.misc) + M_CR;
+  const int* wde = (const int*)(wsm + L.misc) + M_DE;
   if (!P.ovf_pass) {
     for (;;) {
       unsigned long long inst = 0;
       if (lane == 0) inst = atomicAdd(P.counter, 1ull);
       inst = __shfl_sync(FULL, inst, 0);
       if ((int64_t)inst >= P.I) break;
-      solve_instance<NC>(P, (int64_t)inst, wsm, L, ninfo, cr, de, lane);
+      solve_instance<NC>(P, (int64_t)inst, wsm, L, wninfo, wcr, wde, lane);
       __syncwarp();
     }
   } else {
@@ -1101,7 +1125,7 @@ __global__ void __launch_bounds__(128) far_solve_kernel(KParams P) {
       while (bits) {
         const int b = __ffs(bits) - 1;
         bits &= bits - 1;
-        solve_instance<NC>(P, (int64_t)wd * 32 + b, wsm, L, ninfo, cr, de, lane);
+        solve_instance<NC>(P, (int64_t)wd * 32 + b, wsm, L, wninfo, wcr, wde, lane);
         __syncwarp();
       }
     }

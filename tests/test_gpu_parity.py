@@ -104,7 +104,7 @@ def test_large_n(O, torch_dev, n):
     costs = inputs.reconfig_costs(profile)
     tab = inputs.synthetic(profile, n, 24 if n < 1024 else 3, 31, times="narrow" if n == 1024 else "wide")
     if n == 1024:
-        tab = np.minimum(tab, 900)  # keep the makespan bound < 2^30
+        tab = np.minimum(tab, 900)  # keep the makespan bound < 2^29
     ms, slots, res = run_gpu(torch_dev, profile, costs, tab)
     check_against_oracle(O, profile, costs, tab, ms, slots, res)
 
