@@ -281,6 +281,9 @@ def main():
             dist.destroy_process_group()
         return
 
+    # far_solve_many = the fast-layout pass + (families larger than its cap) the overflow pass
+    kmax = 1 + WORKLOAD.n * (nc - 1)
+    launches_per_step = 2 if min(kmax, 64) < kmax else 1
     pk, pk_src = peaks()
     sm_max = float(pk.get("sm_max_mhz", 1965.0))
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -288,16 +291,27 @@ def main():
     # algorithmic integer ops per launch (DESIGN.md §7 "Roofline"): the method's own work model,
     # Alg. 1 on every family member (n placements + one split per tree node per member) x
     # OPS_EVENT + phase-3 candidate evaluations x OPS_EVAL + phase-1 work products and argmaxes
+    # OPS_EVENT: one Alg. 1 event with a binary heap of <= S = 7 frontier nodes: pop (3 levels x 3
+    # ops) + group check, creation check, take the next LPT task, end update (~7) + push (3 levels
+    # x 3 ops) = 25 integer ops ("each ~20-40 integer ops").  OPS_EVAL: one
+    # move/swap candidate = difference, |2x - m|, compare = 3.
     S, NCs, NN = 7, nc, 13
-    OPS_EVENT, OPS_EVAL = (S - 1) + 4, 3
+    OPS_EVENT, OPS_EVAL = 25, 3
     fam = res["family_size"].astype(np.int64)
     alg_events = int((fam * (WORKLOAD.n + NN)).sum())
     ops_p1 = int((2 * WORKLOAD.n * NCs + (fam - 1) * (WORKLOAD.n + NCs)).sum())
     ops = alg_events * OPS_EVENT + evals_step * OPS_EVAL + ops_p1
     kern_avg_s = kern_total / args.steps / 1000.0
     achieved = ops / kern_avg_s
+    traffic = None
+    try:  # dram__bytes_read.sum + dram__bytes_write.sum per instance from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_M5.json")) as f:
+            tj = json.load(f)
+        traffic = (tj["dram_read_bytes_per_instance"] + tj["dram_write_bytes_per_instance"]) * I
+    except Exception:
+        pass
     roof = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
-            "frac": achieved / peak_ops, "traffic": None,
+            "frac": achieved / peak_ops, "traffic": traffic, "traffic_unit": "bytes per launch (ncu)",
             "peak_source": f"{nsm} SMs x 4 SMSP x 32 lanes x {sm_max:.0f} MHz (sm_max_mhz {pk_src})",
             "kernel_ms": kern_avg_s * 1000.0,
             "hbm_bytes_algorithmic": int(host.nbytes + I * (4 + WORKLOAD.n * 8 + 56)),
@@ -315,7 +329,7 @@ def main():
             "alg1_events_simulated_per_s": events_all / (ms_per_step / 1000.0),
             "alg1_events_algorithmic_per_step": alg_events,
             "moves_swaps_per_step": moves_swaps,
-            "gpu_launches": args.steps * 1,
+            "gpu_launches": args.steps * launches_per_step,
             "roofline": roof, "clocks": clocks, "e2e": e2e}
     if not args.no_baseline and not args.profile_run:
         line["cpu_baseline"] = oracle_baseline(args.baseline_seconds)

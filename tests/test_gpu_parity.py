@@ -156,3 +156,53 @@ def test_host_pipeline_matches_device(torch_dev):
     F = far.Far(w.profile, w.costs())
     hms, hsl, hres = F.solve_many_host(tab)
     assert (hms == ms).all() and (hsl["start"] == slots["start"]).all() and (hres["evals"] == res["evals"]).all()
+
+
+def test_full_size_m3_parity(O, torch_dev):
+    """BASELINE configs[2]: all 100k A100 x n=32 instances, every field bit-exact (makespans and
+    reports on all instances; oracle fanned out over the host cores)."""
+    w = inputs.WORKLOADS["M3"]
+    tab = w.table(parallel=True)
+    ms, slots, res = run_gpu(torch_dev, w.profile, w.costs(), tab)
+    oms, ores = O.far_many_parallel(w.profile, w.costs(), tab)
+    assert (ms == oms).all()
+    for k in FIELDS:
+        assert (res[k] == ores[k]).all(), k
+    rng = np.random.default_rng(0)
+    for i in rng.choice(len(tab), 200, replace=False):
+        o = O.far(w.profile, w.costs(), tab[i])
+        assert (slots[i]["node"] == o["slots"]["node"]).all() and (slots[i]["start"] == o["slots"]["start"]).all()
+
+
+def test_full_size_m5_sampled(O, torch_dev):
+    """BASELINE configs[4] at full size in the bench's launch configuration (1M x n=128 on one GPU):
+    sampled instances bit-exact against the oracle; properties on every instance."""
+    torch, dev = torch_dev
+    w = inputs.WORKLOADS["M5"]
+    tab = w.table(parallel=True)
+    F = far.Far(w.profile, w.costs())
+    d = torch.from_numpy(tab).to(dev)
+    ms, sd, rs = F.solve_many(d)
+    torch.cuda.synchronize()
+    F.sync()
+    ms = ms.cpu().numpy()
+    res = far.results_np(rs)
+    del d
+    # properties on all 1M: lower bounds (P:1060), guard (P:812), family bound (P:355)
+    t64 = tab.astype(np.int64)
+    sizes = np.array(inputs.SIZES[w.profile], np.int64)
+    W = (t64 * sizes).min(axis=2).sum(axis=1)
+    H = t64.min(axis=2).max(axis=1)
+    assert (7 * ms.astype(np.int64) >= W).all() and (ms >= H).all()
+    assert (res["makespan"] <= res["makespan_phase2"]).all() and (res["status"] == 0).all()
+    assert (res["family_size"] >= 1).all() and (res["family_size"] <= 1 + 128 * 4).all()
+    rng = np.random.default_rng(1)
+    idx = np.sort(rng.choice(len(tab), 300, replace=False))
+    slots = far.slots_np(sd[torch.from_numpy(idx).to(sd.device)])
+    oms, ores = O.far_many(w.profile, w.costs(), tab[idx])
+    assert (ms[idx] == oms).all()
+    for k in FIELDS:
+        assert (res[k][idx] == ores[k]).all(), k
+    for q, i in enumerate(idx[:40]):
+        o = O.far(w.profile, w.costs(), tab[i])
+        assert (slots[q]["node"] == o["slots"]["node"]).all() and (slots[q]["start"] == o["slots"]["start"]).all()
