@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-baseline", action="store_true")
     ap.add_argument("--profile-run", action="store_true", help="short run for ncu (no clocks/e2e/baseline)")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the M3 / M4-stream secondary measurements")
     return ap.parse_args()
 
 
@@ -124,6 +125,50 @@ def oracle_baseline(seconds, rank_table=None):
     return {"value": done / dt, "unit": "instances/s", "cores": 1, "kind": "oracle",
             "evals_per_s": evals / dt,
             "sample": f"first {done} instances of {WORKLOAD.name} (A100, n=128, seed 5), single-threaded C++ oracle"}
+
+
+def secondary(far, torch, dev, reps=5):
+    """The other BASELINE.json configs as secondary device-timed numbers (not the headline):
+    M3 (configs[2]: 100k A100 x n=32, phases 1-3) and M4 (configs[3]: streams of 64 batches x 64
+    tasks, A30 and A100 trees; throughput variant with 1024 independent streams)."""
+    out = {}
+    st = torch.cuda.current_stream(dev)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(reps):
+            fn()
+        b.record(st)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    w = inputs.WORKLOADS["M3"]
+    d = torch.from_numpy(w.table(parallel=True)).to(dev)
+    F = far.Far(w.profile, w.costs())
+    bufs = (torch.empty(d.shape[0], dtype=torch.int32, device=dev),
+            torch.empty((d.shape[0], w.n, 8), dtype=torch.uint8, device=dev),
+            torch.empty((d.shape[0], 56), dtype=torch.uint8, device=dev))
+    ms = timed(lambda: F.solve_many(d, out=bufs, stream=st))
+    F.sync()
+    out["M3_instances_per_s"] = d.shape[0] / (ms / 1000.0)
+    out["M3_ms"] = ms
+    for prof in ("A30", "A100"):
+        w = inputs.WORKLOADS["M4_" + prof]
+        S = 1024
+        tab = inputs.synthetic_parallel(w.profile, w.n, S * 64, w.seed).reshape(S, 64, w.n, -1)
+        d = torch.from_numpy(tab).to(dev)
+        F = far.Far(w.profile, w.costs())
+        ms = timed(lambda: F.concat_streams(d, stream=st))
+        F.sync()
+        out[f"M4_{prof}_streams_1024x64x64_ms"] = ms
+        out[f"M4_{prof}_batches_per_s"] = S * 64 / (ms / 1000.0)
+        one = d[:1].contiguous()
+        ms1 = timed(lambda: F.concat_streams(one, stream=st))
+        out[f"M4_{prof}_single_stream_64x64_ms"] = ms1
+    return out
 
 
 def run_reference(args, rank, world):
@@ -331,6 +376,8 @@ def main():
             "moves_swaps_per_step": moves_swaps,
             "gpu_launches": args.steps * launches_per_step,
             "roofline": roof, "clocks": clocks, "e2e": e2e}
+    if not args.no_secondary and not args.profile_run:
+        line["secondary"] = secondary(far, torch, dev)
     if not args.no_baseline and not args.profile_run:
         line["cpu_baseline"] = oracle_baseline(args.baseline_seconds)
     print(json.dumps(line), flush=True)
