@@ -467,27 +467,6 @@ __device__ void build_node_lists(int n, int k, const int2* lent, const uint16_t*
   }
 }
 
-// Warp in-place bitonic sort of P (power of two) packed (key, val) pairs in shared memory.
-__device__ void smem_bitonic(unsigned* key, unsigned* val, int P, int lane) {
-  for (int k = 2; k <= P; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = lane; t < (P >> 1); t += 32) {
-        const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
-        const int l = i | j;
-        const bool up = (i & k) == 0;
-        const unsigned a = key[i], b = key[l];
-        if ((a > b) == up) {
-          key[i] = b;
-          key[l] = a;
-          const unsigned va = val[i];
-          val[i] = val[l];
-          val[l] = va;
-        }
-      }
-      __syncwarp();
-    }
-}
-
 // Phase 3 + replay + guard on an input schedule (far_local_search, MODE_LOCAL).
 template <int NC>
 __device__ __noinline__ void solve_local(const KParams& P, int64_t inst, unsigned char* wsm, const Layout& L,
@@ -848,32 +827,43 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       }
     }
     __syncwarp();
-    // sort each segment by (-t, task): warp bitonic sort on packed 32-bit keys when t < 2^22
-    // and the segment has <= 64 entries, else a rank sort through scratch (ivl is dead)
+    // sort each segment by (-t, task).  With t < 2^22 the order is the ascending order of the
+    // packed key ((2^22-1-t) << 10 | task); each lane ranks its <= 4 entries against every key
+    // read once by broadcast.  Otherwise (or > 128 entries) a rank sort through scratch.
     int2* sent = (int2*)scratch;
     uint16_t* stask = (uint16_t*)(scratch + 8 * L.ecap);
     for (int c = 0; c < NC; ++c) {
       const int b = loff[c], m = loff[c + 1] - loff[c];
       if (m <= 1) continue;
-      if (small && 8 * (1 << (32 - __clz(m - 1))) <= L.scr) {
-        // larger lists: bitonic in scratch (ivl is dead), padded to a power of two
-        const int P2 = 1 << (32 - __clz(m - 1));
-        unsigned* kk = (unsigned*)scratch;
-        unsigned* vv = kk + P2;
-        for (int i = lane; i < P2; i += 32) {
-          if (i < m) {
-            const int2 x = lent[b + i];
-            kk[i] = ((unsigned)(0x3FFFFF - x.x) << 10) | (unsigned)ltask[b + i];
-            vv[i] = (unsigned)x.y;
-          } else {
-            kk[i] = 0xFFFFFFFFu;
+      if (small && m <= 128) {
+        unsigned* kk = (unsigned*)scratch;  // ivl is dead
+        for (int i = lane; i < m; i += 32) kk[i] = ((unsigned)(0x3FFFFF - lent[b + i].x) << 10) | ltask[b + i];
+        __syncwarp();
+        unsigned key[4];
+        int yv[4], rk[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int i = r * 32 + lane;
+          key[r] = i < m ? kk[i] : 0xFFFFFFFFu;
+          yv[r] = i < m ? lent[b + i].y : 0;
+          rk[r] = 0;
+        }
+        if (m <= 32) {
+          for (int f = 0; f < m; ++f) rk[0] += kk[f] < key[0];
+        } else {
+          for (int f = 0; f < m; ++f) {
+            const unsigned v = kk[f];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) rk[r] += v < key[r];
           }
         }
         __syncwarp();
-        smem_bitonic(kk, vv, P2, lane);
-        for (int i = lane; i < m; i += 32) {
-          lent[b + i] = make_int2(0x3FFFFF - (int)(kk[i] >> 10), (int)vv[i]);
-          ltask[b + i] = (uint16_t)(kk[i] & 1023u);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (r * 32 + lane < m) {
+            lent[b + rk[r]] = make_int2(0x3FFFFF - (int)(key[r] >> 10), yv[r]);
+            ltask[b + rk[r]] = (uint16_t)(key[r] & 1023u);
+          }
         }
       } else {
         for (int e = lane; e < m; e += 32) {
