@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -157,7 +158,8 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     P.kcap = pass == 0 ? kfast : kmax;
     P.ovf_pass = pass;
     P.counter = ctx->d_counter + slot + pass;
-    const Layout L = a30 ? layout_for<3>(P.n, P.kcap) : layout_for<5>(P.n, P.kcap);
+    Layout L = a30 ? layout_for<3>(P.n, P.kcap) : layout_for<5>(P.n, P.kcap);
+    if (const char* pad = getenv("FAR_DEBUG_SMEM_PAD")) L.bytes += (atoi(pad) + 15) & ~15;  // occupancy experiments
     int warps = 0, per_sm = 0;
     far_status st = pick_shape(ctx, fn, L.bytes, warps, per_sm);
     if (st) return st;

@@ -684,6 +684,8 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   uint32_t* ivl = (uint32_t*)scratch;  // [n][NC] member interval lo | hi<<16 (0xFFFF = absent/open)
   unsigned long long c0pack = 0;
   long long W = 0;  // total area sum_i a_i t_i(a_i) of the current member (uniform)
+  bool mono = true;
+  unsigned tstar = 0;
   {
     int cnt_c[NC];
 #pragma unroll
@@ -711,6 +713,15 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         }
         su[j] = (uint8_t)(packed & 0xFF);
         bestnode[j] = (uint8_t)(packed >> 8);
+        // growth chain a^1 -> nx -> ... -> max size: monotone (non-increasing t) chains allow
+        // the parallel phase-1 below
+        int c = best;
+        while (c != NC - 1) {
+          const int c2 = (int)((packed >> (3 * c)) & 7u);
+          mono = mono && T[j * NC + c2] <= T[j * NC + c];
+          c = c2;
+        }
+        tstar = max(tstar, ((unsigned)T[j * NC + NC - 1] << 10) | (unsigned)(1023 - j));
       }
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
@@ -727,11 +738,108 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
 
   // ---- H2: a^{k+1}: grow the longest task (ties -> lowest index) to
   //          argmin_{s > a_j} s*t_j(s) (ties -> smallest s); stop when it is at max size
-  // With t < 2^22 the argmax key (t, lowest index) packs into 32 bits: one REDUX.MAX per
-  // step, and only the lane owning the grown task rescans its tasks.
   const bool small = tmax < (1 << 22);
   int K = 1;
-  {
+  // Parallel form for monotone chains (every task's t non-increasing along its growth chain;
+  // property 1 of P:260-263 implies it).  With key(t, j) = t << 10 | (1023 - j) the growth
+  // process is the merge of the per-task chains by (key desc, chain position asc): each step
+  // takes the largest current key, and a chain's later keys are never larger.  It stops at
+  // the first terminal element (max size) on top, i.e. at T* = the largest terminal key, so
+  // the growth steps are exactly the non-terminal chain elements with key >= T*, in that order.
+  mono = __all_sync(FULL, mono && small && P.kcap <= 64);  // (fast layout: <= 63 steps)
+  tstar = __reduce_max_sync(FULL, tstar);
+  if (mono) {
+    int2* G = lent;  // temporary (filled in H3): {key, task | from << 10 | to << 13 | pos << 16}
+    int* rnk = (int*)lstate;  // step rank per element (lstate is free until H4; <= 63 steps)
+    int cntl = 0;
+    for (int j = lane; j < n; j += 32) {
+      const unsigned nxp = (unsigned)su[j] | ((unsigned)bestnode[j] << 8);
+      for (int c = cur[j]; c != NC - 1; c = (int)((nxp >> (3 * c)) & 7u)) {
+        if ((((unsigned)T[j * NC + c] << 10) | (unsigned)(1023 - j)) < tstar) break;
+        ++cntl;
+      }
+    }
+    int excl = cntl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, excl, o);
+      if (lane >= o) excl += y;
+    }
+    const int Gn = __shfl_sync(FULL, excl, 31);
+    excl -= cntl;
+    if (Gn + 1 > P.kcap) {  // family larger than this layout holds: defer to the overflow pass
+      if (lane == 0) {
+        atomicOr(P.ovf + (inst >> 5), 1u << (inst & 31));
+        atomicAdd(P.ovf_count, 1ull);
+      }
+      return;
+    }
+    for (int j = lane; j < n; j += 32) {
+      const unsigned nxp = (unsigned)su[j] | ((unsigned)bestnode[j] << 8);
+      int pos = 0;
+      for (int c = cur[j]; c != NC - 1; ++pos) {
+        const unsigned key = ((unsigned)T[j * NC + c] << 10) | (unsigned)(1023 - j);
+        if (key < tstar) break;
+        const int c2 = (int)((nxp >> (3 * c)) & 7u);
+        G[excl++] = make_int2((int)key, j | (c << 10) | (c2 << 13) | (pos << 16));
+        c = c2;
+      }
+    }
+    __syncwarp();
+    // rank of each step: larger keys first; equal keys (same task) in chain order
+    for (int e = lane; e < Gn; e += 32) {
+      const unsigned ke = (unsigned)G[e].x;
+      const int pe = G[e].y >> 16;
+      int rk = 0;
+      for (int f = 0; f < Gn; ++f) {
+        const int2 g = G[f];
+        rk += ((unsigned)g.x > ke) || ((unsigned)g.x == ke && (g.y >> 16) < pe);
+      }
+      // step rk produces member rk + 1: longest task of member rk, deltas of member rk + 1
+      const int j = G[e].y & 1023, cf = (G[e].y >> 10) & 7, ct = (G[e].y >> 13) & 7;
+      lbh[rk] = (int)(ke >> 10);
+      cnts[rk + 1] = (1ull << (11 * ct)) - (1ull << (11 * cf));
+      lbw[rk + 1] = (long long)size_of<NC>(ct) * T[j * NC + ct] - (long long)size_of<NC>(cf) * T[j * NC + cf];
+      rnk[e] = rk;
+    }
+    __syncwarp();
+    // member intervals: entering size ct at member rk + 1, leaving it at the task's next step
+    for (int e = lane; e < Gn; e += 32) {
+      const int y = G[e].y, j = y & 1023, cf = (y >> 10) & 7, ct = (y >> 13) & 7, pos = y >> 16;
+      const int rk = rnk[e];
+      const bool next = e + 1 < Gn && (G[e + 1].y & 1023) == j;
+      ivl[j * NC + ct] = (uint32_t)(rk + 1) | ((next ? (uint32_t)(rnk[e + 1] + 1) : 0xFFFFu) << 16);
+      if (pos == 0) ivl[j * NC + cf] = (uint32_t)(rk + 1) << 16;  // a^1 interval [0, rk + 1)
+    }
+    if (lane == 0) {
+      lbh[Gn] = (int)(tstar >> 10);
+      cnts[0] = c0pack;
+      lbw[0] = W;
+    }
+    __syncwarp();
+    // prefix sums over members of the packed size counts and of the area
+    unsigned long long cc = 0;
+    long long ww = 0;
+    for (int k0 = 0; k0 <= Gn; k0 += 32) {
+      const int k = k0 + lane;
+      unsigned long long dc = k <= Gn ? cnts[k] : 0;
+      long long dw = k <= Gn ? lbw[k] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long yc = __shfl_up_sync(FULL, dc, o);
+        const long long yw = __shfl_up_sync(FULL, dw, o);
+        if (lane >= o) { dc += yc; dw += yw; }
+      }
+      if (k <= Gn) {
+        cnts[k] = cc + dc;
+        lbw[k] = ww + dw;
+      }
+      cc += __shfl_sync(FULL, dc, 31);
+      ww += __shfl_sync(FULL, dw, 31);
+    }
+    __syncwarp();
+    K = Gn + 1;
+  } else {
     unsigned long long cp = c0pack;
     uint32_t* ck = (uint32_t*)start;  // packed current key per task (start[] is free until H7)
     unsigned lk = 0;
