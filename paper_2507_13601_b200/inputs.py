@@ -204,6 +204,14 @@ def small_ties(profile: str, n: int, count: int, seed: int, start: int = 0) -> n
     return uniform_random(profile, n, count, seed, 1, 4, start)
 
 
+def monotone_ties(profile: str, n: int, count: int, seed: int, hi: int = 6, start: int = 0) -> np.ndarray:
+    """Monotone (property 1) times in {1..hi}, non-increasing in the size: equal times along a
+    task's sizes and across tasks everywhere (stresses the growth tie rules)."""
+    nc = len(SIZES[profile])
+    return _chunked(lambda rng, B: -np.sort(-rng.integers(1, hi + 1, (B, n, nc)), axis=2).astype(np.int32),
+                    n, nc, count, seed, 4, start)
+
+
 @dataclass(frozen=True)
 class Workload:
     """A BASELINE.json config as a concrete seeded recipe."""

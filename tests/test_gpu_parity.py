@@ -69,11 +69,13 @@ def test_ragged_sizes(O, torch_dev, profile, n):
 
 
 @pytest.mark.parametrize("profile", ["A30", "A100"])
-@pytest.mark.parametrize("gen", ["ties", "uniform", "narrow", "poor", "good"])
+@pytest.mark.parametrize("gen", ["ties", "monoties", "uniform", "narrow", "poor", "good"])
 def test_tie_and_nonmonotone_inputs(O, torch_dev, profile, gen):
     n = 24
     if gen == "ties":
         tab = inputs.small_ties(profile, n, 300, 5)
+    elif gen == "monoties":
+        tab = inputs.monotone_ties(profile, n, 300, 15)
     elif gen == "uniform":
         tab = inputs.uniform_random(profile, n, 300, 6)       # non-monotone runtimes
     elif gen == "narrow":

@@ -76,7 +76,7 @@ def test_empty_and_single(O):
 def test_family_invariants(O, profile):
     sizes = inputs.SIZES[profile]
     tabs = [inputs.synthetic(profile, 12, 40, 1), inputs.uniform_random(profile, 12, 40, 2),
-            inputs.small_ties(profile, 12, 40, 3)]
+            inputs.small_ties(profile, 12, 40, 3), inputs.monotone_ties(profile, 12, 40, 4)]
     for tab in tabs:
         for t in tab:
             fam = O.family(profile, t)
