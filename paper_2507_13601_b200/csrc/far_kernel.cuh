@@ -220,16 +220,22 @@ __device__ __forceinline__ int dur_of(const int32_t* T, const uint8_t* su, int j
   return T[j * NC + su[j]];
 }
 
-// Replay of node lists nlist[v][0..ncnt[v]) -> start[j], onode[j]; returns the makespan.
+// Replay of node lists nlist[v][0..ncnt[v]) with task durations D[j] -> start[j], onode[j];
+// returns the makespan.  Prefix sums over each node list are warp scans.
 template <int NC>
-__device__ int replay_warp(int n, const int32_t* T, const uint8_t* su, const uint16_t* nlist, const int* ncnt,
-                           int* nsum, int* life, int* start, uint8_t* onode, const uint32_t* ninfo, const int* cr,
-                           const int* de, int lane, int* Eout = nullptr) {
+__device__ int replay_warp(int n, const int* D, const uint16_t* nlist, const int* ncnt, int* nsum, int* life,
+                           int* start, uint8_t* onode, const uint32_t* ninfo, const int* cr, const int* de, int lane,
+                           int* Eout = nullptr) {
   constexpr int NN = Tree<NC>::NN;
-  if (lane < NN) {
-    int sm = 0;
-    for (int q = 0; q < ncnt[lane]; ++q) sm += dur_of<NC>(T, su, nlist[lane * n + q]);
-    nsum[lane] = sm;
+  if (lane < NN) {  // one lane per node: exclusive prefix of durations along its list
+    int acc = 0;
+    for (int q = 0; q < ncnt[lane]; ++q) {
+      const int j = nlist[lane * n + q];
+      start[j] = acc;  // relative to the node's creation end
+      onode[j] = (uint8_t)lane;
+      acc += D[j];
+    }
+    nsum[lane] = acc;
   }
   __syncwarp();
   int ms = 0, E = 0;
@@ -237,15 +243,7 @@ __device__ int replay_warp(int n, const int32_t* T, const uint8_t* su, const uin
   ms = __shfl_sync(FULL, ms, 0);
   E = __shfl_sync(FULL, E, 0);
   __syncwarp();
-  if (lane < NN && ncnt[lane] > 0) {
-    int t = life[lane * 6 + 1];
-    for (int q = 0; q < ncnt[lane]; ++q) {
-      const int j = nlist[lane * n + q];
-      start[j] = t;
-      onode[j] = (uint8_t)lane;
-      t += dur_of<NC>(T, su, j);
-    }
-  }
+  for (int j2 = lane; j2 < n; j2 += 32) start[j2] += life[onode[j2] * 6 + 1];
   __syncwarp();
   if (Eout) *Eout = E;
   return ms;
@@ -277,16 +275,16 @@ __device__ void list_remove(uint16_t* lst, int* cnt, int j, int lane) {
 // "Insert T in I^a.tasks ordered by T.time": decreasing time, ties -> lower index.
 // Warp: the insertion point is the number of entries ordered before j; chunked shift right.
 template <int NC>
-__device__ void list_insert(uint16_t* lst, int* cnt, int j, const int32_t* T, const uint8_t* su, int lane) {
+__device__ void list_insert(uint16_t* lst, int* cnt, int j, const int* D, int lane) {
   const int c = *cnt;
-  const int dj = dur_of<NC>(T, su, j);
+  const int dj = D[j];
   int pos = 0;
   for (int b = 0; b < c; b += 32) {
     const int i = b + lane;
     bool before = false;
     if (i < c) {
       const int x = lst[i];
-      const int dx = dur_of<NC>(T, su, x);
+      const int dx = D[x];
       before = dx > dj || (dx == dj && x < j);
     }
     pos += __popc(__ballot_sync(FULL, before));
@@ -306,7 +304,7 @@ __device__ void list_insert(uint16_t* lst, int* cnt, int j, const int32_t* T, co
 }
 
 template <int NC>
-__device__ void refine_warp(int n, const int32_t* T, const uint8_t* su, uint16_t* nlist, int* ncnt, int* send,
+__device__ void refine_warp(int n, const int* D, uint16_t* nlist, int* ncnt, int* send,
                             const uint32_t* ninfo, int max_it, int ppm, int lane, int& moves, int& swaps, int& iters,
                             long long& evals) {
   constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
@@ -321,8 +319,7 @@ __device__ void refine_warp(int n, const int32_t* T, const uint8_t* su, uint16_t
     if (lane >= lo && lane < lo + nd_sz(w)) send[lane] += d;
     __syncwarp();
   };
-  int omega = 0;
-  for (int s = 0; s < S; ++s) omega = max(omega, send[s]);
+  int omega = __reduce_max_sync(FULL, lane < S ? send[lane] : 0);
   moves = swaps = iters = 0;
   evals = 0;
   bool stop = false;
@@ -332,12 +329,12 @@ __device__ void refine_warp(int n, const int32_t* T, const uint8_t* su, uint16_t
     unsigned long long Q = 0;  // FIFO of node ids, 4 bits each
     int qh = 0, qt = 0;
     uint32_t opened = 0;
-    for (int s = 0; s < S; ++s)
-      if (send[s] == omega) {
-        const int leaf = leaf_of<NC>(s);
-        Q |= (unsigned long long)leaf << (4 * qt++);
-        opened |= 1u << leaf;
-      }
+    // line 5: leaves of the slices reaching omega, ascending slice order
+    for (unsigned crit = __ballot_sync(FULL, lane < S && send[lane] == omega); crit; crit &= crit - 1) {
+      const int leaf = leaf_of<NC>(__ffs(crit) - 1);
+      Q |= (unsigned long long)leaf << (4 * qt++);
+      opened |= 1u << leaf;
+    }
     while (qh < qt) {
       const int I = (int)((Q >> (4 * qh++)) & 15);
       if (I == 0) { stop = true; break; }
@@ -367,7 +364,7 @@ __device__ void refine_warp(int n, const int32_t* T, const uint8_t* su, uint16_t
         int bj = INT_MAX;
         for (int q = lane; q < nI; q += 32) {
           const int j = LI[q];
-          const int t = dur_of<NC>(T, su, j);
+          const int t = D[j];
           if (t < m) {
             const unsigned d = (unsigned)abs(2 * t - m);
             if (d < bd || (d == bd && j < bj)) { bd = d; bj = j; }
@@ -378,7 +375,7 @@ __device__ void refine_warp(int n, const int32_t* T, const uint8_t* su, uint16_t
         int nt = 0, tk0 = 0, tk1 = 0, delta = 0;
         if (dmin != UINT_MAX) {
           tk0 = __reduce_min_sync(FULL, (unsigned)(bd == dmin ? bj : INT_MAX));
-          delta = dur_of<NC>(T, su, tk0);
+          delta = D[tk0];
           nt = 1;
           ++moves;
         } else {
@@ -386,10 +383,14 @@ __device__ void refine_warp(int n, const int32_t* T, const uint8_t* su, uint16_t
           evals += (long long)nI * nA;
           unsigned bd2 = UINT_MAX, bkey = UINT_MAX;
           const int tot = nI * nA;
+          const int di = 32 / max(nA, 1), da = 32 - di * nA;
+          int qi = lane / max(nA, 1), qa = lane - qi * nA;
           for (int p = lane; p < tot; p += 32) {
-            const int qi = p / nA, qa = p - qi * nA;
             const int k = LI[qi], j = LA[qa];
-            const int dl = dur_of<NC>(T, su, k) - dur_of<NC>(T, su, j);
+            qi += di;
+            qa += da;
+            if (qa >= nA) { qa -= nA; ++qi; }
+            const int dl = D[k] - D[j];
             if (0 < dl && dl < m) {
               const unsigned d = (unsigned)abs(2 * dl - m);
               const unsigned key = ((unsigned)k << 10) | (unsigned)j;
@@ -401,7 +402,7 @@ __device__ void refine_warp(int n, const int32_t* T, const uint8_t* su, uint16_t
             const unsigned key = __reduce_min_sync(FULL, bd2 == d2 ? bkey : UINT_MAX);
             tk0 = (int)(key >> 10);
             tk1 = (int)(key & 1023);
-            delta = dur_of<NC>(T, su, tk0) - dur_of<NC>(T, su, tk1);
+            delta = D[tk0] - D[tk1];
             nt = 2;
             ++swaps;
           }
@@ -409,7 +410,7 @@ __device__ void refine_warp(int n, const int32_t* T, const uint8_t* su, uint16_t
         for (int x = 0; x < nt; ++x) {  // move: I->A; swap: K I->A then J A->I (same final lists)
           const int from = x == 0 ? I : A, to = x == 0 ? A : I, task = x == 0 ? tk0 : tk1;
           list_remove<NC>(nlist + from * n, &ncnt[from], task, lane);
-          list_insert<NC>(nlist + to * n, &ncnt[to], task, T, su, lane);
+          list_insert<NC>(nlist + to * n, &ncnt[to], task, D, lane);
         }
         if (nt) {
           add_on(wI, -delta);
@@ -425,8 +426,7 @@ __device__ void refine_warp(int n, const int32_t* T, const uint8_t* su, uint16_t
         }
       }
     }
-    omega = 0;
-    for (int s = 0; s < S; ++s) omega = max(omega, send[s]);
+    omega = __reduce_max_sync(FULL, lane < S ? send[lane] : 0);
     if (ppm > 0 && (long long)(omega_prev - omega) * 1000000LL < (long long)ppm * omega_prev) break;
   }
 }
@@ -552,9 +552,12 @@ __device__ __noinline__ void solve_local(const KParams& P, int64_t inst, unsigne
     if (refine && n > 0) {
       int mv, sw, it;
       long long ev;
-      refine_warp<NC>(n, T, su, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
+      int* D = (int*)(scratch + ((2 * NN * n + 3) & ~3));  // durations at the tasks' sizes
+      for (int j = lane; j < n; j += 32) D[j] = T[j * NC + su[j]];
+      __syncwarp();
+      refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
       R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
-      const int msR = replay_warp<NC>(n, T, su, nlist, ncnt, nsum, life, start, bestnode, ninfo, cr, de, lane);
+      const int msR = replay_warp<NC>(n, D, nlist, ncnt, nsum, life, start, bestnode, ninfo, cr, de, lane);
       if (!(P.flags & FAR_NO_GUARD) && msR > ms2) {
         R.reverted = 1;
       } else {
@@ -1128,17 +1131,20 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   const bool need_replay = refine || want_sched;
   for (int pass = 0; pass < 2; ++pass) {
     build_node_lists<NC>(n, bestk, lent, ltask, loff, bestnode, nlist, ncnt, su, lane);
+    int* D = (int*)(scratch + ((2 * NN * n + 3) & ~3));  // durations at the tasks' sizes (scratch >= 32n)
+    for (int j = lane; j < n; j += 32) D[j] = T[j * NC + su[j]];
+    __syncwarp();
     const bool ref = refine && pass == 0;
     if (ref) {
       if (lane < S) send[lane] = bsend[lane];
       __syncwarp();
       int mv, sw, it;
       long long ev;
-      refine_warp<NC>(n, T, su, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
+      refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
       R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
     }
     if (!need_replay) break;
-    const int msR = replay_warp<NC>(n, T, su, nlist, ncnt, nsum, life, start, cur, ninfo, cr, de, lane);
+    const int msR = replay_warp<NC>(n, D, nlist, ncnt, nsum, life, start, cur, ninfo, cr, de, lane);
     if (ref && !(P.flags & FAR_NO_GUARD) && msR > ms2) {
       R.reverted = 1;  // keep-best guard: return the phase-2 schedule (replayed in pass 1)
       if (!want_sched) break;

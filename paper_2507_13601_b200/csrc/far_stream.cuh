@@ -35,7 +35,7 @@ struct SParams {
 };
 
 struct SLayout {
-  int times, su, onode, nl, nl2, ncnt, ncnt2, nsum, start, fstart, life, win, misc, bytes;
+  int times, su, onode, nl, nl2, ncnt, ncnt2, nsum, start, fstart, dur, life, win, misc, bytes;
 };
 
 __host__ __device__ inline SLayout make_slayout(int n, int NC, int NN) {
@@ -51,6 +51,7 @@ __host__ __device__ inline SLayout make_slayout(int n, int NC, int NN) {
   L.nsum = o;   o = al16(o + 4 * 16);
   L.start = o;  o = al16(o + 4 * n);
   L.fstart = o; o = al16(o + 4 * n);
+  L.dur = o;    o = al16(o + 4 * n);
   L.life = o;   o = al16(o + 4 * 16 * 6);
   L.win = o;    o = al16(o + WCAP * 24);
   L.misc = o;   o = al16(o + 8 * 64);
@@ -99,12 +100,12 @@ struct SeamRes {
 
 // Timeline of the batch described by (nl, ncnt) + its seam against the stream state.
 template <int NC>
-__device__ SeamRes eval_seam(int n, const int32_t* T, const uint8_t* su, const uint16_t* nl, const int* ncnt,
-                             int* nsum, uint8_t* onode, int* start, int* life, const uint32_t* ninfo, const int* cr,
-                             const int* de, bool rev, const StreamSt* st, const WinEv* win, int lane) {
+__device__ SeamRes eval_seam(int n, const int32_t* T, const uint8_t* su, const int* D, const uint16_t* nl,
+                             const int* ncnt, int* nsum, uint8_t* onode, int* start, int* life, const uint32_t* ninfo,
+                             const int* cr, const int* de, bool rev, const StreamSt* st, const WinEv* win, int lane) {
   constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
   int E = 0;
-  replay_warp<NC>(n, T, su, nl, ncnt, nsum, life, start, onode, ninfo, rev ? de : cr, rev ? cr : de, lane, &E);
+  replay_warp<NC>(n, D, nl, ncnt, nsum, life, start, onode, ninfo, rev ? de : cr, rev ? cr : de, lane, &E);
   if (rev) {  // mirror about E: tasks and lifecycles (a mirrored forward destroy is the create)
     for (int j = lane; j < n; j += 32) start[j] = E - (start[j] + T[j * NC + su[j]]);
     if (lane < NN && life[lane * 6] >= 0) {
@@ -215,12 +216,12 @@ __device__ SeamRes eval_seam(int n, const int32_t* T, const uint8_t* su, const u
 
 // Move task k from node I to node A and (swap) task j from A to I, keeping lists ordered.
 template <int NC>
-__device__ __noinline__ void transfer(int n, uint16_t* nl, int* ncnt, int I, int A, int k, int j, const int32_t* T,
-                                      const uint8_t* su, int lane) {
+__device__ __noinline__ void transfer(int n, uint16_t* nl, int* ncnt, int I, int A, int k, int j, const int* D,
+                                      int lane) {
   for (int x = 0; x < (j >= 0 ? 2 : 1); ++x) {
     const int from = x == 0 ? I : A, to = x == 0 ? A : I, task = x == 0 ? k : j;
     list_remove<NC>(nl + from * n, &ncnt[from], task, lane);
-    list_insert<NC>(nl + to * n, &ncnt[to], task, T, su, lane);
+    list_insert<NC>(nl + to * n, &ncnt[to], task, D, lane);
   }
 }
 
@@ -260,6 +261,7 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
   uint8_t* onode = wsm + L.onode;
   int* start = (int*)(wsm + L.start);
   int* fstart = (int*)(wsm + L.fstart);
+  int* D = (int*)(wsm + L.dur);
   int* life = (int*)(wsm + L.life);
   WinEv* win = (WinEv*)(wsm + L.win);
   StreamSt* st = (StreamSt*)(wsm + L.misc);
@@ -289,6 +291,7 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
       su[j] = (uint8_t)(size_of<NC>(nd_c0(w)) == s.size_used ? nd_c0(w) : nd_c1(w));
       fstart[j] = s.start;
       start[j] = s.node;  // temporarily: node per task
+      D[j] = T[j * NC + su[j]];
     }
     __syncwarp();
     for (int j = lane; j < n; j += 32) {
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
       StreamSt dummy;
       (void)dummy;
       int E = 0;
-      replay_warp<NC>(n, T, su, nl, ncnt, nsum, life, start, onode, ninfo, cr, de, lane, &E);
+      replay_warp<NC>(n, D, nl, ncnt, nsum, life, start, onode, ninfo, cr, de, lane, &E);
       int te = 0;
       for (int j = lane; j < n; j += 32) te = max(te, start[j] + T[j * NC + su[j]]);
       te = __reduce_max_sync(FULL, te);
@@ -323,7 +326,7 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
     int moves = 0, swaps = 0;
     // ---- seam move/swap on reversed batches (R24)
     if (rev && k > 0) {
-      SeamRes cur = eval_seam<NC>(n, T, su, nl, ncnt, nsum, onode, start, life, ninfo, cr, de, true, st, win, lane);
+      SeamRes cur = eval_seam<NC>(n, T, su, D, nl, ncnt, nsum, onode, start, life, ninfo, cr, de, true, st, win, lane);
       for (int it = 0; it < P.max_it; ++it) {
         unsigned long long Q = 0;
         int qh = 0, qt = 0;
@@ -367,8 +370,8 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
             if (dmin != LL_MAX) {
               const int Tm = (int)__reduce_min_sync(FULL, (unsigned)(bd == dmin ? bj : INT_MAX));
               copy_lists<NC>(n, nl, ncnt, nl2, ncnt2, lane);
-              transfer<NC>(n, nl2, ncnt2, I, A, Tm, -1, T, su, lane);
-              SeamRes e2 = eval_seam<NC>(n, T, su, nl2, ncnt2, nsum, onode, start, life, ninfo, cr, de, true, st, win, lane);
+              transfer<NC>(n, nl2, ncnt2, I, A, Tm, -1, D, lane);
+              SeamRes e2 = eval_seam<NC>(n, T, su, D, nl2, ncnt2, nsum, onode, start, life, ninfo, cr, de, true, st, win, lane);
               if (e2.end < cur.end) {
                 copy_lists<NC>(n, nl2, ncnt2, nl, ncnt, lane);
                 cur = e2;
@@ -395,8 +398,8 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
                 const unsigned key = __reduce_min_sync(FULL, bd2 == d2 ? bkey : UINT_MAX);
                 const int kk = (int)(key >> 10), jj = (int)(key & 1023);
                 copy_lists<NC>(n, nl, ncnt, nl2, ncnt2, lane);
-                transfer<NC>(n, nl2, ncnt2, I, A, kk, jj, T, su, lane);
-                SeamRes e2 = eval_seam<NC>(n, T, su, nl2, ncnt2, nsum, onode, start, life, ninfo, cr, de, true, st, win, lane);
+                transfer<NC>(n, nl2, ncnt2, I, A, kk, jj, D, lane);
+                SeamRes e2 = eval_seam<NC>(n, T, su, D, nl2, ncnt2, nsum, onode, start, life, ninfo, cr, de, true, st, win, lane);
                 if (e2.end < cur.end) {
                   copy_lists<NC>(n, nl2, ncnt2, nl, ncnt, lane);
                   cur = e2;
@@ -418,7 +421,7 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
       }
     }
     // ---- final timeline + seam of the (refined) batch; place it
-    const SeamRes R = eval_seam<NC>(n, T, su, nl, ncnt, nsum, onode, start, life, ninfo, cr, de, rev, st, win, lane);
+    const SeamRes R = eval_seam<NC>(n, T, su, D, nl, ncnt, nsum, onode, start, life, ninfo, cr, de, rev, st, win, lane);
     const long long O = R.O;
     ms = max(ms, O + R.task_end);
     if (lane == 0) {

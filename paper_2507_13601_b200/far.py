@@ -15,7 +15,7 @@ import re
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfar.so")
+LIB_PATH = os.environ.get("FAR_LIB_OVERRIDE") or os.path.join(HERE, "libfar.so")  # override: A/B experiments only
 HEADER = os.path.join(os.path.dirname(HERE), "include", "far.h")
 
 PROFILES = {"A30": 0, "A100": 1, "H100": 2}
