@@ -16,7 +16,6 @@ using namespace farb;
 
 namespace {
 constexpr int RING = 256;
-int SMEM_MAX = 227 * 1024 - 1024;  // set from cudaDevAttrMaxSharedMemoryPerBlockOptin (minus static smem)
 }  // namespace
 
 struct far_ctx {
@@ -29,8 +28,11 @@ struct far_ctx {
   int launch_id = 0;
   int* d_errflag = nullptr;
   // staging for host-memory calls
-  char* d_buf = nullptr;
+  char* d_buf = nullptr;   // staging of the synchronous host-memory calls (ctx streams)
   size_t d_buf_bytes = 0;
+  char* d_cbuf = nullptr;  // per-batch schedules of far_concat_streams (caller's stream)
+  size_t d_cbuf_bytes = 0;
+  int smem_max = 0;        // opt-in shared memory per block minus the kernels' static smem
   cudaStream_t s[2] = {nullptr, nullptr};
   bool inited = false;
   // overflow bitmasks (instances whose family exceeds the fast layout), ring of 4
@@ -74,28 +76,29 @@ static far_status ensure_device(far_ctx* ctx) {
   // allow every kernel the full opt-in shared memory; each launch passes its own size
   int optin = 0;
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-  SMEM_MAX = optin - 1024;
+  ctx->smem_max = optin - 1024;
   const void* fns[4] = {(const void*)far_solve_kernel<3>, (const void*)far_solve_kernel<5>,
                         (const void*)far_stream_kernel<3>, (const void*)far_stream_kernel<5>};
-  for (const void* f : fns) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX));
+  for (const void* f : fns) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   ctx->inited = true;
   return FAR_OK;
 }
 
-static far_status ensure_buf(far_ctx* ctx, size_t bytes) {
-  if (ctx->d_buf_bytes >= bytes) return FAR_OK;
-  if (ctx->d_buf) {
-    CK(cudaDeviceSynchronize());
-    CK(cudaFree(ctx->d_buf));
-    ctx->d_buf = nullptr;
-    ctx->d_buf_bytes = 0;
+static far_status grow(far_ctx* ctx, char** buf, size_t* have, size_t bytes) {
+  if (*have >= bytes) return FAR_OK;
+  if (*buf) {
+    CK(cudaDeviceSynchronize());  // the old buffer may still be in use by queued work
+    CK(cudaFree(*buf));
+    *buf = nullptr;
+    *have = 0;
   }
   size_t b = std::max(bytes, (size_t)1 << 20);
-  cudaError_t e = cudaMalloc(&ctx->d_buf, b);
+  cudaError_t e = cudaMalloc(buf, b);
   if (e != cudaSuccess) return fail(ctx, FAR_E_OOM, "device workspace allocation failed");
-  ctx->d_buf_bytes = b;
+  *have = b;
   return FAR_OK;
 }
+static far_status ensure_buf(far_ctx* ctx, size_t bytes) { return grow(ctx, &ctx->d_buf, &ctx->d_buf_bytes, bytes); }
 
 template <int NC> static Layout layout_for(int n, int kcap) {
   return make_layout(n, NC, Tree<NC>::S, Tree<NC>::NN, kcap);
@@ -112,7 +115,7 @@ static far_status pick_shape(far_ctx* ctx, const void* fn, int bytes, int& warps
   int best_w = 0, best_b = 0, best_tot = 0;
   for (int w = 1; w <= 4; ++w) {
     const size_t smem = (size_t)w * bytes;
-    if (smem > (size_t)SMEM_MAX) break;
+    if (smem > (size_t)ctx->smem_max) break;
     int b = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, w * 32, smem));
     if (b * w > best_tot || (b * w == best_tot && w > best_w)) { best_tot = b * w; best_w = w; best_b = b; }
@@ -240,6 +243,7 @@ void far_destroy(far_ctx* ctx) {
     for (int r = 0; r < 4; ++r)
       if (ctx->d_ovf[r]) cudaFree(ctx->d_ovf[r]);
     if (ctx->d_buf) cudaFree(ctx->d_buf);
+    if (ctx->d_cbuf) cudaFree(ctx->d_cbuf);
     cudaStreamDestroy(ctx->s[0]);
     cudaStreamDestroy(ctx->s[1]);
   }
@@ -437,7 +441,7 @@ extern "C" far_status far_concat_streams(far_ctx* ctx, const int32_t* d_times, i
   auto a256 = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t bs = a256((size_t)IB * n * sizeof(far_task_slot)), br = a256((size_t)IB * sizeof(far_result)),
                bm = a256((size_t)IB * 4);
-  if ((st = ensure_buf(ctx, bs + br + bm))) return st;
+  if ((st = grow(ctx, &ctx->d_cbuf, &ctx->d_cbuf_bytes, bs + br + bm))) return st;
   // 1) FAR phases 1-3 on every batch of every stream (data-parallel)
   KParams P;
   fill_params(ctx, opts, P);
@@ -445,9 +449,9 @@ extern "C" far_status far_concat_streams(far_ctx* ctx, const int32_t* d_times, i
   P.times = d_times;
   P.I = IB;
   P.n = n;
-  P.sched = (far_task_slot*)ctx->d_buf;
-  P.res = d_batch_res ? d_batch_res : (far_result*)(ctx->d_buf + bs);
-  P.makespan = (int32_t*)(ctx->d_buf + bs + br);
+  P.sched = (far_task_slot*)ctx->d_cbuf;
+  P.res = d_batch_res ? d_batch_res : (far_result*)(ctx->d_cbuf + bs);
+  P.makespan = (int32_t*)(ctx->d_cbuf + bs + br);
   P.mode = MODE_SOLVE;
   if ((st = launch_solve(ctx, P, stream))) return st;
   // 2) the per-stream fold (one warp per stream)
@@ -470,7 +474,7 @@ extern "C" far_status far_concat_streams(far_ctx* ctx, const int32_t* d_times, i
   Q.errflag = ctx->d_errflag;
   const bool a30 = ctx->nc == 3;
   const SLayout L = make_slayout(n, ctx->nc, ctx->nn);
-  int warps = std::min(4, SMEM_MAX / std::max(1, L.bytes));
+  int warps = std::min(4, ctx->smem_max / std::max(1, L.bytes));
   if (warps < 1) return fail(ctx, FAR_E_TOO_LARGE, "stream state does not fit in shared memory");
   const size_t smem = (size_t)warps * L.bytes;
   const int grid = (int)((S + warps - 1) / warps);

@@ -208,3 +208,38 @@ def test_full_size_m5_sampled(O, torch_dev):
     for q, i in enumerate(idx[:40]):
         o = O.far(w.profile, w.costs(), tab[i])
         assert (slots[q]["node"] == o["slots"]["node"]).all() and (slots[q]["start"] == o["slots"]["start"]).all()
+
+
+def test_local_search_on_other_schedules(O, torch_dev):
+    """far_local_search on schedules other than phase 2's (the refined FAR schedule itself, with
+    its start order) equals the oracle's Alg. 2 + replay + guard on the same input."""
+    for profile in ("A30", "A100"):
+        costs = inputs.reconfig_costs(profile)
+        F = far.Far(profile, costs)
+        for t in inputs.synthetic(profile, 21, 40, 71):
+            o = O.far(profile, costs, t)
+            s_in = np.zeros(len(t), far.SLOT_DT)
+            s_in["node"], s_in["size_used"], s_in["start"] = o["slots"]["node"], o["slots"]["size_used"], o["slots"]["start"]
+            ms_in = int(o["result"]["makespan"])
+            s2, r2 = F.local_search(t, s_in, makespan_phase2=ms_in)
+            q = O.refine(profile, costs, t, o["slots"], ms_in)
+            assert r2["makespan"] == q["result"]["makespan"] and r2["reverted"] == q["result"]["reverted"]
+            assert (s2["node"] == q["slots"]["node"]).all() and (s2["start"] == q["slots"]["start"]).all()
+            assert r2["makespan"] <= ms_in
+
+
+def test_local_search_rejects_bad_schedules(torch_dev):
+    F = far.Far("A30")
+    t = inputs.synthetic("A30", 4, 1, 3)[0]
+    s, r = F.schedule_batch(t)
+    bad = s.copy()
+    bad["node"][0] = 9                     # no such tree node
+    with pytest.raises(far.FarError) as e:
+        F.local_search(t, bad)
+    assert e.value.status == 1
+    bad = s.copy()
+    bad["size_used"][0] = 3                # A30 hosts no size 3
+    with pytest.raises(far.FarError) as e:
+        F.local_search(t, bad)
+    assert e.value.status == 1
+    F.sync()
