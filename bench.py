@@ -221,10 +221,17 @@ def main():
     from paper_2507_13601_b200 import far
 
     assert torch.cuda.is_available(), "bench.py needs a GPU (no CPU fallback)"
+    local = local % torch.cuda.device_count()  # (ranks share a GPU only in the gloo logic test)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # NCCL over NVLink/NVSwitch; FAR_BENCH_BACKEND=gloo only to exercise the multi-rank logic
+    # when several ranks must share one GPU (NCCL refuses duplicate GPUs)
+    backend = os.environ.get("FAR_BENCH_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     I = args.instances
     nc = len(inputs.SIZES[WORKLOAD.profile])
@@ -248,7 +255,11 @@ def main():
         if ev is not None:
             ev[1].record(stream)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, ms)
+            if backend == "nccl":
+                dist.all_gather_into_tensor(gathered, ms)
+            else:
+                g = torch.empty(I * world, dtype=torch.int32)
+                dist.all_gather_into_tensor(g, ms.cpu())
 
     for _ in range(args.warmup):
         step()
@@ -283,7 +294,7 @@ def main():
 
     # max over ranks
     t = torch.tensor([total_ms, sum(kern_ms), float(evals_step), float(events_step)], dtype=torch.float64,
-                     device=dev)
+                     device=dev if backend == "nccl" else "cpu")
     if world > 1:
         mx = t.clone()
         dist.all_reduce(mx[:2], op=dist.ReduceOp.MAX)
@@ -312,7 +323,7 @@ def main():
         for _ in range(args.e2e_steps):
             F.solve_many_host(hin, out=(hms, hsd, hrs))
         dt = (time.perf_counter() - t0) / args.e2e_steps
-        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        tt = torch.tensor([dt], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt[0])
@@ -368,7 +379,7 @@ def main():
             "config": {"workload": WORKLOAD.name, "profile": "A100 (7-slice tree, Table 2 A100 costs)",
                        "n_tasks": WORKLOAD.n, "instances_per_rank": I, "global_instances": inst_all,
                        "generator": "PAPER.md §6.3 MixedScaling/WideTimes, seed 5",
-                       "l2": "inputs (2.56 GB/rank) larger than the 126 MB L2; no flush",
+                       "l2": f"inputs ({host.nbytes / 1e9:.2f} GB/rank) larger than the 126 MB L2; no flush",
                        "parallelism": f"dp{world} (instances sharded, NCCL allgather of makespans)"},
             "evals_per_s": evals_all / (ms_per_step / 1000.0),
             "alg1_events_simulated_per_s": events_all / (ms_per_step / 1000.0),
