@@ -11,6 +11,7 @@
 
 #include "far_kernel.cuh"
 #include "far_stream.cuh"
+#include "far_pipeline.cuh"
 
 using namespace farb;
 
@@ -32,6 +33,8 @@ struct far_ctx {
   size_t d_buf_bytes = 0;
   char* d_cbuf = nullptr;  // per-batch schedules of far_concat_streams (caller's stream)
   size_t d_cbuf_bytes = 0;
+  char* d_pws[2] = {nullptr, nullptr};  // pipelined phase-2 workspaces (ring of 2 launches)
+  size_t d_pws_bytes[2] = {0, 0};
   int smem_max = 0;        // opt-in shared memory per block minus the kernels' static smem
   cudaStream_t s[2] = {nullptr, nullptr};
   bool inited = false;
@@ -79,6 +82,10 @@ static far_status ensure_device(far_ctx* ctx) {
   ctx->smem_max = optin - 1024;
   const void* fns[4] = {(const void*)far_solve_kernel<3>, (const void*)far_solve_kernel<5>,
                         (const void*)far_stream_kernel<3>, (const void*)far_stream_kernel<5>};
+  const void* pfns[6] = {(const void*)far_member0_kernel<3>, (const void*)far_member0_kernel<5>,
+                         (const void*)far_members_kernel<3>, (const void*)far_members_kernel<5>,
+                         (const void*)far_winner_kernel<3>, (const void*)far_winner_kernel<5>};
+  for (const void* f : pfns) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384));
   for (const void* f : fns) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   ctx->inited = true;
   return FAR_OK;
@@ -127,23 +134,47 @@ static far_status pick_shape(far_ctx* ctx, const void* fn, int bytes, int& warps
   return FAR_OK;
 }
 
-// Launch the fused solver for I instances on `stream`: a fast pass whose shared-memory
-// layout holds families of up to kfast allocations, then (only if some family was larger)
-// an overflow pass with the full layout over the flagged instances.
+// One launch of the warp-per-instance kernel over I instances (or over the flagged ones).
+static far_status launch_warp_kernel(far_ctx* ctx, KParams& P, cudaStream_t stream, int64_t units) {
+  const bool a30 = ctx->nc == 3;
+  const void* fn = a30 ? (const void*)far_solve_kernel<3> : (const void*)far_solve_kernel<5>;
+  Layout L = a30 ? layout_for<3>(P.n, P.kcap) : layout_for<5>(P.n, P.kcap);
+  if (const char* pad = getenv("FAR_DEBUG_SMEM_PAD")) L.bytes += (atoi(pad) + 15) & ~15;  // occupancy experiments
+  int warps = 0, per_sm = 0;
+  far_status st = pick_shape(ctx, fn, L.bytes, warps, per_sm);
+  if (st) return st;
+  const size_t smem = (size_t)warps * L.bytes;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((units + warps - 1) / warps, (int64_t)ctx->sms * per_sm));
+  if (a30)
+    far_solve_kernel<3><<<grid, warps * 32, smem, stream>>>(P);
+  else
+    far_solve_kernel<5><<<grid, warps * 32, smem, stream>>>(P);
+  CK(cudaGetLastError());
+  return FAR_OK;
+}
+
+// Launch the solver for I instances on `stream`.
+//   MODE_SOLVE: the pipelined solver (far_pipeline.cuh: K1 prep -> K2 member 0 -> K3 candidate
+//   members -> K4 winner record -> K5 finish) for families of <= 64 members with t < 2^22,
+//   then the fused kernel with the full layout over the instances K1 deferred (overflow mask).
+//   FAR_FUSED_PHASE2 (debug env) forces the fused warp-per-instance kernel for everything.
+//   MODE_LOCAL: the fused kernel (phase 3 only).
 static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
   if (P.I <= 0) return FAR_OK;
   const bool a30 = ctx->nc == 3;
-  const int kmax = 1 + P.n * (ctx->nc - 1);
+  const int NC = ctx->nc, NN = ctx->nn;
+  const int kmax = 1 + P.n * (NC - 1);
   int kfast = std::min(kmax, 64);  // M5: P(K > 64) ~ 0.4% -> those go to the overflow pass
   if (P.mode != MODE_SOLVE) kfast = 1;
-  const bool need_ovf = P.mode == MODE_SOLVE && kfast < kmax;
-  const int slot = (ctx->launch_id++ % (RING / 4)) * 4;
-  CK(cudaMemsetAsync(ctx->d_counter + slot, 0, 3 * sizeof(unsigned long long), stream));
+  const bool pipe = P.mode == MODE_SOLVE && P.n > 0 && P.n <= 1023 && !getenv("FAR_FUSED_PHASE2");
+  const bool need_ovf = P.mode == MODE_SOLVE && (kfast < kmax || pipe);
+  const int slot = (ctx->launch_id++ % (RING / 8)) * 8;
+  CK(cudaMemsetAsync(ctx->d_counter + slot, 0, 8 * sizeof(unsigned long long), stream));
   P.errflag = ctx->d_errflag;
   P.ovf_count = ctx->d_counter + slot + 2;
   P.ovf = nullptr;
   if (need_ovf) {
-    const int r = (slot / 4) & 3;
+    const int r = (slot / 8) & 3;
     const size_t words = (size_t)((P.I + 31) / 32);
     if (ctx->ovf_words[r] < words) {
       if (ctx->d_ovf[r]) {
@@ -156,24 +187,85 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     P.ovf = ctx->d_ovf[r];
     CK(cudaMemsetAsync(P.ovf, 0, words * 4, stream));
   }
-  const void* fn = a30 ? (const void*)far_solve_kernel<3> : (const void*)far_solve_kernel<5>;
-  for (int pass = 0; pass < (need_ovf ? 2 : 1); ++pass) {
-    P.kcap = pass == 0 ? kfast : kmax;
-    P.ovf_pass = pass;
-    P.counter = ctx->d_counter + slot + pass;
-    Layout L = a30 ? layout_for<3>(P.n, P.kcap) : layout_for<5>(P.n, P.kcap);
-    if (const char* pad = getenv("FAR_DEBUG_SMEM_PAD")) L.bytes += (atoi(pad) + 15) & ~15;  // occupancy experiments
-    int warps = 0, per_sm = 0;
-    far_status st = pick_shape(ctx, fn, L.bytes, warps, per_sm);
-    if (st) return st;
-    const size_t smem = (size_t)warps * L.bytes;
-    int64_t need = pass == 0 ? (P.I + warps - 1) / warps : ((P.I + 31) / 32 + warps - 1) / warps;
-    const int grid = (int)std::min<int64_t>(need, (int64_t)ctx->sms * per_sm);
-    if (a30)
-      far_solve_kernel<3><<<grid, warps * 32, smem, stream>>>(P);
-    else
-      far_solve_kernel<5><<<grid, warps * 32, smem, stream>>>(P);
+  far_status st;
+  if (pipe) {
+    // ---- workspace for this launch
+    const Layout LF = a30 ? layout_for<3>(P.n, kfast) : layout_for<5>(P.n, kfast);
+    const int ecap1 = LF.ecap + 1;
+    auto a256 = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t I = (size_t)P.I;
+    const size_t o_ent = 0, o_lb = o_ent + a256(I * ecap1 * 8), o_cnt = o_lb + a256(I * kfast * 4),
+                 o_meta = o_cnt + a256(I * kfast * 8), o_best = o_meta + a256(I * 64), o_evt = o_best + a256(I * 8),
+                 o_rec = o_evt + a256(I * 8), o_sl = o_rec + a256(I * P.n * 4), o_items = o_sl + a256(I * 32),
+                 o_end = o_items + a256(I * (size_t)(kfast - 1 > 0 ? kfast - 1 : 1) * 8);
+    const int r = ctx->launch_id & 1;
+    if ((st = grow(ctx, &ctx->d_pws[r], &ctx->d_pws_bytes[r], o_end))) return st;
+    char* w = ctx->d_pws[r];
+    P.ws_ent = (int2*)(w + o_ent);
+    P.ws_lb = (int*)(w + o_lb);
+    P.ws_cnt = (unsigned long long*)(w + o_cnt);
+    P.ws_meta = (int*)(w + o_meta);
+    P.ws_best = (unsigned long long*)(w + o_best);
+    P.ws_evt = (unsigned long long*)(w + o_evt);
+    P.ws_rec = (uint32_t*)(w + o_rec);
+    P.ws_sl = (int*)(w + o_sl);
+    P.ws_ecap1 = ecap1;
+    P.ws_kcap = kfast;
+    // ---- K1: H0-H3 per instance (warp)
+    P.pipe = PIPE_PREP;
+    P.kcap = kfast;
+    P.ovf_pass = 0;
+    P.counter = ctx->d_counter + slot + 0;
+    if ((st = launch_warp_kernel(ctx, P, stream, P.I))) return st;
+    // ---- K2-K4: phase 2 at lane granularity
+    PParams Q;
+    memset(&Q, 0, sizeof(Q));
+    Q.I = P.I;
+    Q.n = P.n;
+    for (int c = 0; c < 8; ++c) {
+      Q.cr[c] = P.cr[c];
+      Q.de[c] = P.de[c];
+    }
+    Q.flags = P.flags;
+    Q.ws_ent = P.ws_ent; Q.ws_lb = P.ws_lb; Q.ws_cnt = P.ws_cnt; Q.ws_meta = P.ws_meta;
+    Q.ws_best = P.ws_best; Q.ws_evt = P.ws_evt; Q.ws_rec = P.ws_rec; Q.ws_sl = P.ws_sl;
+    Q.ws_ecap1 = ecap1; Q.ws_kcap = kfast;
+    Q.items = (int2*)(w + o_items);
+    Q.nitems = ctx->d_counter + slot + 3;
+    Q.counter = ctx->d_counter + slot + 4;
+    const int tb = 128;
+    const size_t psm = (size_t)4 * NC * tb + (size_t)2 * NN * tb;
+    const int g_inst = (int)std::min<int64_t>((P.I + tb - 1) / tb, (int64_t)ctx->sms * 16);
+    const int g_items = ctx->sms * 16;
+    if (a30) {
+      far_member0_kernel<3><<<g_inst, tb, psm, stream>>>(Q);
+      far_members_kernel<3><<<g_items, tb, psm, stream>>>(Q);
+      far_winner_kernel<3><<<g_inst, tb, psm, stream>>>(Q);
+    } else {
+      far_member0_kernel<5><<<g_inst, tb, psm, stream>>>(Q);
+      far_members_kernel<5><<<g_items, tb, psm, stream>>>(Q);
+      far_winner_kernel<5><<<g_inst, tb, psm, stream>>>(Q);
+    }
     CK(cudaGetLastError());
+    // ---- K5: H6-H7 per instance (warp)
+    P.pipe = PIPE_FINISH;
+    P.kcap = 1;
+    P.counter = ctx->d_counter + slot + 5;
+    if ((st = launch_warp_kernel(ctx, P, stream, P.I))) return st;
+    P.pipe = PIPE_NONE;
+  } else {
+    P.pipe = PIPE_NONE;
+    P.kcap = kfast;
+    P.ovf_pass = 0;
+    P.counter = ctx->d_counter + slot + 0;
+    if ((st = launch_warp_kernel(ctx, P, stream, P.I))) return st;
+  }
+  if (need_ovf) {  // instances deferred by the fast layout / the pipeline: fused kernel, full layout
+    P.pipe = PIPE_NONE;
+    P.kcap = kmax;
+    P.ovf_pass = 1;
+    P.counter = ctx->d_counter + slot + 1;
+    if ((st = launch_warp_kernel(ctx, P, stream, (P.I + 31) / 32))) return st;
   }
   return FAR_OK;
 }
@@ -244,6 +336,8 @@ void far_destroy(far_ctx* ctx) {
       if (ctx->d_ovf[r]) cudaFree(ctx->d_ovf[r]);
     if (ctx->d_buf) cudaFree(ctx->d_buf);
     if (ctx->d_cbuf) cudaFree(ctx->d_cbuf);
+    for (int r = 0; r < 2; ++r)
+      if (ctx->d_pws[r]) cudaFree(ctx->d_pws[r]);
     cudaStreamDestroy(ctx->s[0]);
     cudaStreamDestroy(ctx->s[1]);
   }

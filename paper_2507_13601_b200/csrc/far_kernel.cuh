@@ -49,7 +49,20 @@ struct KParams {
   unsigned* ovf;                // bit per instance: family larger than kcap -> overflow pass
   unsigned long long* ovf_count;
   int ovf_pass;                 // 1: solve only the instances flagged in ovf (full layout)
+  int pipe;                     // PIPE_NONE: fused; PIPE_PREP: H0-H3 -> ws; PIPE_FINISH: ws -> H6-H7
+  // pipelined phase 2 workspace (far_pipeline.cuh), strides in elements
+  int2* ws_ent;                 // [I][ws_ecap1] list entries {t | task << 22, lo | hi << 16}
+  int* ws_lb;                   // [I][ws_kcap]  lower bound of each member's makespan
+  unsigned long long* ws_cnt;   // [I][ws_kcap]  packed size counts of each member
+  int* ws_meta;                 // [I][16]       loff[0..NC], flag (WS_FLAG), K (WS_K)
+  unsigned long long* ws_best;  // [I]           min over simulated members of (makespan << 16 | k)
+  unsigned long long* ws_evt;   // [I]           Alg. 1 pops simulated
+  uint32_t* ws_rec;             // [I][n]        k*'s placement: node | size idx << 4 | position << 7
+  int* ws_sl;                   // [I][8]        k*'s slice ends
+  int ws_ecap1, ws_kcap;
 };
+enum { PIPE_NONE = 0, PIPE_PREP = 1, PIPE_FINISH = 2 };
+enum { WS_FLAG = 8, WS_K = 9 };  // ws_meta slots: flag 0 = phase 2 pending, 1 = finished or deferred
 
 // Per-warp shared-memory layout (bytes), identical on host and device.  kcap bounds the
 // family size K this layout holds (the per-size lists hold at most n + K - 1 entries).
@@ -588,6 +601,94 @@ __device__ __noinline__ void solve_local(const KParams& P, int64_t inst, unsigne
     return;
   }
 
+// Node lists of k* from the pipelined phase-2 record (node, size index, position per task).
+template <int NC>
+__device__ void lists_from_record(int n, const uint32_t* rec, uint16_t* nlist, int* ncnt, uint8_t* su, int lane) {
+  constexpr int NN = Tree<NC>::NN;
+  if (lane < NN) ncnt[lane] = 0;
+  __syncwarp();
+  for (int j = lane; j < n; j += 32) {
+    const uint32_t r = __ldcs(rec + j);
+    const int v = (int)(r & 15u);
+    nlist[v * n + (int)(r >> 7)] = (uint16_t)j;
+    su[j] = (uint8_t)((r >> 4) & 7u);
+    atomicAdd(&ncnt[v], 1);
+  }
+  __syncwarp();
+}
+
+// H6/H7 of one instance (warp): node lists of k*, phase 3, replay, keep-best guard, stores.
+template <int NC>
+__device__ void finish_instance(const KParams& P, int64_t inst, unsigned char* wsm, const Layout& L,
+                                const uint32_t* ninfo, const int* cr, const int* de, int lane, far_result R, int ms2,
+                                int bestk, bool want_sched, bool refine) {
+  constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
+  const int n = P.n;
+  int32_t* T = (int32_t*)(wsm + L.times);
+  int2* lent = (int2*)(wsm + L.lent);
+  uint16_t* ltask = (uint16_t*)(wsm + L.ltask);
+  uint8_t* cur = wsm + L.cur;
+  uint8_t* su = wsm + L.su;
+  uint8_t* bestnode = wsm + L.bestnode;
+  unsigned char* scratch = wsm + L.scratch;
+  int* start = (int*)(wsm + L.start);
+  int* misc = (int*)(wsm + L.misc);
+  int* loff = misc + M_LOFF;
+  int* ncnt = misc + M_NCNT;
+  int* nsum = misc + M_NSUM;
+  int* send = misc + M_SEND;
+  int* bsend = misc + M_BSEND;
+  int* life = misc + M_LIFE;
+  // ---- H6/H7: node lists of k*, phase 3, replay, keep-best guard.  One call site per
+  // helper (pass 1 only runs when the guard reverts to the phase-2 tree) keeps the code
+  // small enough for the instruction cache.
+  uint16_t* nlist = (uint16_t*)scratch;
+  int msF = ms2;
+  const bool need_replay = refine || want_sched;
+  for (int pass = 0; pass < 2; ++pass) {
+    if (P.pipe == PIPE_FINISH) lists_from_record<NC>(n, P.ws_rec + inst * (int64_t)n, nlist, ncnt, su, lane);
+    else build_node_lists<NC>(n, bestk, lent, ltask, loff, bestnode, nlist, ncnt, su, lane);
+    int* D = (int*)(scratch + ((2 * NN * n + 3) & ~3));  // durations at the tasks' sizes (scratch >= 32n)
+    for (int j = lane; j < n; j += 32) D[j] = T[j * NC + su[j]];
+    __syncwarp();
+    const bool ref = refine && pass == 0;
+    if (ref) {
+      if (lane < S) send[lane] = bsend[lane];
+      __syncwarp();
+      int mv, sw, it;
+      long long ev;
+      refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
+      R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
+    }
+    if (!need_replay) break;
+    const int msR = replay_warp<NC>(n, D, nlist, ncnt, nsum, life, start, cur, ninfo, cr, de, lane);
+    if (ref && !(P.flags & FAR_NO_GUARD) && msR > ms2) {
+      R.reverted = 1;  // keep-best guard: return the phase-2 schedule (replayed in pass 1)
+      if (!want_sched) break;
+      continue;
+    }
+    if (ref) msF = msR;
+    break;
+  }
+  R.makespan = msF;
+  if (want_sched) {
+    far_task_slot* out = P.sched + inst * (int64_t)n;
+    for (int j = lane; j < n; j += 32) {
+      far_task_slot s;
+      s.node = cur[j];
+      s.size_used = (uint8_t)size_of<NC>(su[j]);
+      s.pad[0] = s.pad[1] = 0;
+      s.start = start[j];
+      out[j] = s;
+    }
+  }
+  if (lane == 0) {
+    P.makespan[inst] = R.makespan;
+    if (P.res) P.res[inst] = R;
+  }
+  __syncwarp();
+}
+
 // ---------------------------------------------------------------------------
 // One instance, one warp.
 // ---------------------------------------------------------------------------
@@ -665,6 +766,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         P.makespan[inst] = -1;
         if (P.res) P.res[inst] = R;
         atomicOr(P.errflag, 1);
+        if (P.pipe == PIPE_PREP) P.ws_meta[inst * 16 + WS_FLAG] = 1;
       }
       return;
     }
@@ -679,7 +781,23 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     if (lane == 0) {
       P.makespan[inst] = 0;
       if (P.res) P.res[inst] = R;
+      if (P.pipe == PIPE_PREP) P.ws_meta[inst * 16 + WS_FLAG] = 1;
     }
+    return;
+  }
+  if (P.pipe == PIPE_FINISH) {  // phase 2 was done by the lane-level kernels (far_pipeline.cuh)
+    const int* meta = P.ws_meta + inst * 16;
+    if (meta[WS_FLAG]) return;  // error / empty / deferred to the overflow pass
+    const unsigned long long best = P.ws_best[inst];
+    ms2 = (int)(best >> 16);
+    bestk = (int)(best & 0xFFFFu);
+    R.family_size = meta[WS_K];
+    R.alloc_index = bestk;
+    R.makespan_phase2 = ms2;
+    R.events = (long long)P.ws_evt[inst];
+    if (lane < S) bsend[lane] = P.ws_sl[inst * 8 + lane];
+    __syncwarp();
+    finish_instance<NC>(P, inst, wsm, L, ninfo, cr, de, lane, R, ms2, bestk, want_sched, refine);
     return;
   }
 
@@ -742,6 +860,14 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   // ---- H2: a^{k+1}: grow the longest task (ties -> lowest index) to
   //          argmin_{s > a_j} s*t_j(s) (ties -> smallest s); stop when it is at max size
   const bool small = tmax < (1 << 22);
+  if (P.pipe == PIPE_PREP && (!small || n > 1023)) {  // entries pack t < 2^22 and task < 1023
+    if (lane == 0) {
+      atomicOr(P.ovf + (inst >> 5), 1u << (inst & 31));
+      atomicAdd(P.ovf_count, 1ull);
+      P.ws_meta[inst * 16 + WS_FLAG] = 1;
+    }
+    return;
+  }
   int K = 1;
   // Parallel form for monotone chains (every task's t non-increasing along its growth chain;
   // property 1 of P:260-263 implies it).  With key(t, j) = t << 10 | (1023 - j) the growth
@@ -774,6 +900,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       if (lane == 0) {
         atomicOr(P.ovf + (inst >> 5), 1u << (inst & 31));
         atomicAdd(P.ovf_count, 1ull);
+        if (P.pipe == PIPE_PREP) P.ws_meta[inst * 16 + WS_FLAG] = 1;
       }
       return;
     }
@@ -880,6 +1007,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         if (lane == 0) {
           atomicOr(P.ovf + (inst >> 5), 1u << (inst & 31));
           atomicAdd(P.ovf_count, 1ull);
+          if (P.pipe == PIPE_PREP) P.ws_meta[inst * 16 + WS_FLAG] = 1;
         }
         return;
       }
@@ -996,6 +1124,29 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       }
       __syncwarp();
     }
+  }
+
+  if (P.pipe == PIPE_PREP) {  // hand the lists and the family to the lane-level phase 2
+    const int E = loff[NC];
+    int2* ge = P.ws_ent + inst * (int64_t)P.ws_ecap1;
+    for (int e = lane; e < E; e += 32) {
+      const int2 x = lent[e];
+      ge[e] = make_int2((int)((unsigned)x.x | ((unsigned)ltask[e] << 22)), x.y);
+    }
+    if (lane == 0) ge[E] = make_int2(0, 0xFFFF);  // padding entry (never a member)
+    int* gl = P.ws_lb + inst * (int64_t)P.ws_kcap;
+    unsigned long long* gc = P.ws_cnt + inst * (int64_t)P.ws_kcap;
+    for (int k = lane; k < K; k += 32) {
+      gl[k] = max(lbh[k], (int)((lbw[k] + S - 1) / S));  // max(h_k, ceil(W_k / #slices))
+      gc[k] = cnts[k];
+    }
+    int* meta = P.ws_meta + inst * 16;
+    if (lane <= NC) meta[lane] = loff[lane];
+    if (lane == 0) {
+      meta[WS_K] = K;
+      meta[WS_FLAG] = 0;
+    }
+    return;
   }
 
   // ---- H4: Alg. 1 for every family member, one member per lane
@@ -1123,53 +1274,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   R.makespan_phase2 = bestms;
   ms2 = bestms;
 
-  // ---- H6/H7: node lists of k*, phase 3, replay, keep-best guard.  One call site per
-  // helper (pass 1 only runs when the guard reverts to the phase-2 tree) keeps the code
-  // small enough for the instruction cache.
-  uint16_t* nlist = (uint16_t*)scratch;
-  int msF = ms2;
-  const bool need_replay = refine || want_sched;
-  for (int pass = 0; pass < 2; ++pass) {
-    build_node_lists<NC>(n, bestk, lent, ltask, loff, bestnode, nlist, ncnt, su, lane);
-    int* D = (int*)(scratch + ((2 * NN * n + 3) & ~3));  // durations at the tasks' sizes (scratch >= 32n)
-    for (int j = lane; j < n; j += 32) D[j] = T[j * NC + su[j]];
-    __syncwarp();
-    const bool ref = refine && pass == 0;
-    if (ref) {
-      if (lane < S) send[lane] = bsend[lane];
-      __syncwarp();
-      int mv, sw, it;
-      long long ev;
-      refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
-      R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
-    }
-    if (!need_replay) break;
-    const int msR = replay_warp<NC>(n, D, nlist, ncnt, nsum, life, start, cur, ninfo, cr, de, lane);
-    if (ref && !(P.flags & FAR_NO_GUARD) && msR > ms2) {
-      R.reverted = 1;  // keep-best guard: return the phase-2 schedule (replayed in pass 1)
-      if (!want_sched) break;
-      continue;
-    }
-    if (ref) msF = msR;
-    break;
-  }
-  R.makespan = msF;
-  if (want_sched) {
-    far_task_slot* out = P.sched + inst * (int64_t)n;
-    for (int j = lane; j < n; j += 32) {
-      far_task_slot s;
-      s.node = cur[j];
-      s.size_used = (uint8_t)size_of<NC>(su[j]);
-      s.pad[0] = s.pad[1] = 0;
-      s.start = start[j];
-      out[j] = s;
-    }
-  }
-  if (lane == 0) {
-    P.makespan[inst] = R.makespan;
-    if (P.res) P.res[inst] = R;
-  }
-  __syncwarp();
+  finish_instance<NC>(P, inst, wsm, L, ninfo, cr, de, lane, R, ms2, bestk, want_sched, refine);
 }
 
 __constant__ uint32_t c_nodes3[7] = {

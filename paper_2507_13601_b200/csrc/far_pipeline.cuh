@@ -1,0 +1,238 @@
+// far_pipeline.cuh — phase 2 (Alg. 1 over the family) at lane granularity.
+//
+// The fused kernel gives each instance one warp and each family member one lane, so a warp
+// always pays a full 32-lane pass although, on realistic inputs, the exact lower bound
+// max(h_k, ceil(W_k / #slices)) (far_kernel.cuh H2) rules out almost every member once one
+// member's makespan is known (k* = 0 on ~90 % of M5 instances).  The pipelined solver
+// therefore splits the solve into
+//   K1 far_solve_kernel PIPE_PREP    warp / instance: H0-H3, lists + family -> workspace
+//   K2 far_member0_kernel            lane / instance: Alg. 1 for member 0 (recorded), then the
+//                                    members whose (LB_k, k) is below (ms_0, 0) become items
+//   K3 far_members_kernel            lane / item (instance, member): Alg. 1, atomicMin of
+//                                    (makespan << 16 | k) per instance -- argmin (makespan, k)
+//   K4 far_winner_kernel             lane / instance: re-runs k* when k* != 0, recording it
+//   K5 far_solve_kernel PIPE_FINISH  warp / instance: H6-H7 from the record
+// Every lane does useful work, and an instance costs ~1 + (candidates) member simulations
+// instead of a 32-lane pass.  The result is identical to the fused kernel's (same readings,
+// same tie-breaks: the packed key orders (makespan, k) lexicographically).
+#pragma once
+#include "far_kernel.cuh"
+
+namespace farb {
+
+__device__ __forceinline__ unsigned long long best_key(int ms, int k) {
+  return ((unsigned long long)(unsigned)ms << 16) | (unsigned)k;
+}
+
+// Alg. 1 for member k of one instance on ONE thread.  ent: the instance's per-size LPT lists
+// (global, read-only), absolute cursors; st: this thread's [NC] cursor words in shared memory
+// (stride bdim); with REC the placement of every task is recorded (node | size << 4 |
+// position-in-node << 7) and the slice ends are returned.
+template <int NC, bool REC>
+__device__ int sim_member(const int2* __restrict__ ent, const int* loff, unsigned long long cp, int k,
+                          const uint32_t* ninfo, const int* cr, const int* de, uint32_t* st, uint16_t* npos,
+                          int bdim, uint32_t* rec, int* sl_out, int& pops) {
+  constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
+  int total = 0;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int r = (int)((cp >> (11 * c)) & 2047);
+    st[c * bdim] = ((uint32_t)r << 16) | (uint32_t)loff[c];
+    total += r;
+  }
+  if (REC)
+    for (int v = 0; v < NN; ++v) npos[v * bdim] = 0;
+  Frontier<S> F;
+  F.init();
+  int rec_end = 0, ms = 0;
+  int sl[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) sl[s] = 0;
+  while (total > 0) {
+    int bs, be;
+    F.pop(bs, be);
+    const int v = F.node(bs);
+    const uint32_t w = ninfo[v];
+    int c = nd_c0(w);
+    uint32_t sv = st[c * bdim];
+    if (!(sv >> 16)) {
+      c = nd_c1(w);
+      sv = 0;
+      if (c != NONE) sv = st[c * bdim];
+    }
+    ++pops;
+    if (sv >> 16) {
+      if (!((F.has >> bs) & 1)) {
+        rec_end = max(rec_end, be) + cr[nd_szi(w)];
+        be = rec_end;
+        F.has |= 1u << bs;
+      }
+      int p = (int)(sv & 0xFFFFu);
+      int2 e;
+      for (;;) {
+        const int2 e0 = __ldg(ent + p), e1 = __ldg(ent + p + 1);
+        if ((e0.y & 0xFFFF) <= k && k < (int)((unsigned)e0.y >> 16)) { e = e0; p += 1; break; }
+        if ((e1.y & 0xFFFF) <= k && k < (int)((unsigned)e1.y >> 16)) { e = e1; p += 2; break; }
+        p += 2;
+      }
+      if (REC) {
+        const int task = (int)((unsigned)e.x >> 22);
+        const int pos = npos[v * bdim];
+        npos[v * bdim] = (uint16_t)(pos + 1);
+        rec[task] = (uint32_t)v | ((uint32_t)c << 4) | ((uint32_t)pos << 7);
+      }
+      st[c * bdim] = ((sv & 0xFFFF0000u) - 0x10000u) | (uint32_t)p;
+      be += e.x & 0x3FFFFF;
+      ms = max(ms, be);
+      --total;
+      F.set(bs, be);
+    } else {
+      if ((F.has >> bs) & 1) rec_end = max(rec_end, be) + de[nd_szi(w)];
+      if (!F.split(bs, be, w)) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) sl[s] = (s == bs) ? be : sl[s];
+      }
+    }
+  }
+  pops += __popc(F.live);
+  if (REC) {
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+      if ((F.live >> s) & 1) {
+        const int sz = nd_sz(ninfo[F.node(s)]);
+#pragma unroll
+        for (int q = 0; q < S; ++q) sl[q] = (q >= s && q < s + sz) ? F.endv(s) : sl[q];
+      }
+#pragma unroll
+    for (int s = 0; s < S; ++s) sl_out[s] = sl[s];
+  }
+  return ms;
+}
+
+struct PParams {
+  int64_t I;
+  int n;
+  int cr[8], de[8];
+  unsigned flags;
+  int2* ws_ent;
+  int* ws_lb;
+  unsigned long long* ws_cnt;
+  int* ws_meta;
+  unsigned long long* ws_best;
+  unsigned long long* ws_evt;
+  uint32_t* ws_rec;
+  int* ws_sl;
+  int ws_ecap1, ws_kcap;
+  int2* items;                  // (instance, member) work items of K3
+  unsigned long long* nitems;   // item counter
+  unsigned long long* counter;  // K3 item scheduler
+};
+
+template <int NC> struct PipeSmem {
+  uint32_t ninfo[16];
+  int cr[8], de[8];
+};
+
+template <int NC>
+__device__ __forceinline__ void pipe_prologue(const PParams& P, PipeSmem<NC>& sm) {
+  constexpr int NN = Tree<NC>::NN;
+  if (threadIdx.x < NN) sm.ninfo[threadIdx.x] = (NC == 3) ? c_nodes3[threadIdx.x] : c_nodes5[threadIdx.x];
+  if (threadIdx.x < 8) {
+    sm.cr[threadIdx.x] = P.cr[threadIdx.x];
+    sm.de[threadIdx.x] = P.de[threadIdx.x];
+  }
+  __syncthreads();
+}
+
+// K2: member 0 of every pending instance (recorded), then the candidate members as items.
+template <int NC>
+__global__ void __launch_bounds__(128) far_member0_kernel(PParams P) {
+  constexpr int NN = Tree<NC>::NN;
+  __shared__ PipeSmem<NC> sm;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  pipe_prologue<NC>(P, sm);
+  const int bdim = blockDim.x, tid = threadIdx.x;
+  uint32_t* st = (uint32_t*)dsm + tid;
+  uint16_t* npos = (uint16_t*)(dsm + 4 * NC * bdim) + tid;
+  const bool exhaustive = (P.flags & FAR_EXHAUSTIVE) != 0;
+  for (int64_t i = (int64_t)blockIdx.x * bdim + tid; i < P.I; i += (int64_t)gridDim.x * bdim) {
+    const int* meta = P.ws_meta + i * 16;
+    if (meta[WS_FLAG]) continue;
+    int loff[NC + 1];
+#pragma unroll
+    for (int c = 0; c <= NC; ++c) loff[c] = meta[c];
+    const int K = meta[WS_K];
+    const int2* ent = P.ws_ent + i * (int64_t)P.ws_ecap1;
+    const int* lb = P.ws_lb + i * (int64_t)P.ws_kcap;
+    int pops = 0;
+    const int ms0 = sim_member<NC, true>(ent, loff, P.ws_cnt[i * (int64_t)P.ws_kcap], 0, sm.ninfo, sm.cr, sm.de, st,
+                                         npos, bdim, P.ws_rec + i * (int64_t)P.n, P.ws_sl + i * 8, pops);
+    const unsigned long long b0 = best_key(ms0, 0);
+    P.ws_best[i] = b0;
+    P.ws_evt[i] = (unsigned long long)pops;
+    // members that can still beat (ms_0, 0): (LB_k, k) < (ms_0, 0) lexicographically
+    int cand = 0;
+    for (int k = 1; k < K; ++k) cand += exhaustive || best_key(lb[k], k) < b0;
+    if (cand) {
+      unsigned long long base = atomicAdd(P.nitems, (unsigned long long)cand);
+      for (int k = 1; k < K; ++k)
+        if (exhaustive || best_key(lb[k], k) < b0) P.items[base++] = make_int2((int)i, k);
+    }
+  }
+  (void)NN;
+}
+
+// K3: the candidate members (lane per item), pruned again against the instance's current best.
+template <int NC>
+__global__ void __launch_bounds__(128) far_members_kernel(PParams P) {
+  __shared__ PipeSmem<NC> sm;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  pipe_prologue<NC>(P, sm);
+  const int bdim = blockDim.x, tid = threadIdx.x;
+  uint32_t* st = (uint32_t*)dsm + tid;
+  const bool exhaustive = (P.flags & FAR_EXHAUSTIVE) != 0;
+  const unsigned long long nit = *(volatile unsigned long long*)P.nitems;
+  for (unsigned long long it = (unsigned long long)blockIdx.x * bdim + tid; it < nit;
+       it += (unsigned long long)gridDim.x * bdim) {
+    const int2 item = P.items[it];
+    const int64_t i = item.x;
+    const int k = item.y;
+    const int lbk = P.ws_lb[i * (int64_t)P.ws_kcap + k];
+    if (!exhaustive && best_key(lbk, k) >= *(volatile unsigned long long*)(P.ws_best + i)) continue;
+    const int* meta = P.ws_meta + i * 16;
+    int loff[NC + 1];
+#pragma unroll
+    for (int c = 0; c <= NC; ++c) loff[c] = meta[c];
+    int pops = 0;
+    const int ms = sim_member<NC, false>(P.ws_ent + i * (int64_t)P.ws_ecap1, loff,
+                                         P.ws_cnt[i * (int64_t)P.ws_kcap + k], k, sm.ninfo, sm.cr, sm.de, st,
+                                         nullptr, bdim, nullptr, nullptr, pops);
+    atomicMin(P.ws_best + i, best_key(ms, k));
+    atomicAdd(P.ws_evt + i, (unsigned long long)pops);
+  }
+}
+
+// K4: re-run the winner when it is not member 0, recording its placements.
+template <int NC>
+__global__ void __launch_bounds__(128) far_winner_kernel(PParams P) {
+  __shared__ PipeSmem<NC> sm;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  pipe_prologue<NC>(P, sm);
+  const int bdim = blockDim.x, tid = threadIdx.x;
+  uint32_t* st = (uint32_t*)dsm + tid;
+  uint16_t* npos = (uint16_t*)(dsm + 4 * NC * bdim) + tid;
+  for (int64_t i = (int64_t)blockIdx.x * bdim + tid; i < P.I; i += (int64_t)gridDim.x * bdim) {
+    const int* meta = P.ws_meta + i * 16;
+    if (meta[WS_FLAG]) continue;
+    const int k = (int)(P.ws_best[i] & 0xFFFFu);
+    if (k == 0) continue;
+    int loff[NC + 1];
+#pragma unroll
+    for (int c = 0; c <= NC; ++c) loff[c] = meta[c];
+    int pops = 0;
+    sim_member<NC, true>(P.ws_ent + i * (int64_t)P.ws_ecap1, loff, P.ws_cnt[i * (int64_t)P.ws_kcap + k], k,
+                         sm.ninfo, sm.cr, sm.de, st, npos, bdim, P.ws_rec + i * (int64_t)P.n, P.ws_sl + i * 8, pops);
+  }
+}
+
+}  // namespace farb
