@@ -169,6 +169,28 @@ far_status far_concat_streams(far_ctx *ctx, const int32_t *d_times, int64_t S, i
                               const far_opts *opts, int64_t *d_stream_makespan, int64_t *d_offsets,
                               far_task_slot *d_sched, far_result *d_batch_res, int32_t *d_seam, void *cuda_stream);
 
+/* ---- Diagnostics (no compute; for bench.py and profiling).
+ * Kernel stages of far_solve_many / far_concat_streams:
+ *   PREP     H0-H3 (input checks, phase-1 family, per-size LPT lists), warp per instance
+ *   MEMBER0  Alg. 1 for family member 0 (recorded), lane per instance
+ *   MEMBERS  Alg. 1 for the members whose lower bound can still win, lane per (instance, member)
+ *   WINNER   Alg. 1 re-run of k* != 0 (recorded), lane per instance
+ *   FINISH   H6-H7 (phase 3, line-26 replay, guard, output), warp per instance
+ *   OVERFLOW fused H0-H7 for the instances PREP deferred (family > 64 members), warp per instance
+ *   FUSED    fused H0-H7 (far_schedule_batch, far_local_search, n = 1024), warp per instance
+ *   STREAM   multi-batch fold of far_concat_streams, warp per stream */
+enum { FAR_STAGE_PREP = 0, FAR_STAGE_MEMBER0, FAR_STAGE_MEMBERS, FAR_STAGE_WINNER, FAR_STAGE_FINISH,
+       FAR_STAGE_OVERFLOW, FAR_STAGE_FUSED, FAR_STAGE_STREAM, FAR_NUM_STAGES };
+/* enable != 0: from now on every launch of the context is bracketed by CUDA events recorded
+ * on the caller's stream (one event per stage boundary; the events add no synchronisation). */
+far_status far_stage_timing(far_ctx *ctx, int32_t enable);
+/* Waits for the timed launches, writes ms[FAR_NUM_STAGES] = device milliseconds per stage
+ * summed over them, resets the sums, returns the number of timed solver launches (< 0 on a
+ * CUDA error). ms may be NULL (reset only). */
+int32_t far_stage_times(far_ctx *ctx, float *ms);
+/* Number of kernels the context has launched since far_create (host-side count). */
+int64_t far_launch_count(const far_ctx *ctx);
+
 #ifdef __cplusplus
 }
 #endif

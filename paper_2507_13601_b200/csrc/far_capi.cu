@@ -45,6 +45,14 @@ struct far_ctx {
   struct Shape { const void* fn; int bytes, warps, per_sm; };
   Shape shapes[16];
   int nshapes = 0;
+  // diagnostics: kernel launch count, optional per-stage CUDA-event timing (ring of event sets)
+  int64_t launches = 0;
+  bool timing = false;
+  struct EvSet { cudaEvent_t ev[10]; int stage[10]; int nev; bool created, pending; };
+  static constexpr int NSETS = 32;
+  EvSet tsets[NSETS] = {};
+  int tnext = 0, timed = 0;
+  double stage_ms[FAR_NUM_STAGES] = {0};
 };
 
 static far_status fail(far_ctx* c, far_status st, const std::string& m) {
@@ -80,12 +88,15 @@ static far_status ensure_device(far_ctx* ctx) {
   int optin = 0;
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   ctx->smem_max = optin - 1024;
-  const void* fns[4] = {(const void*)far_solve_kernel<3>, (const void*)far_solve_kernel<5>,
+  const void* fns[6] = {(const void*)far_solve_kernel<3, PIPE_NONE>, (const void*)far_solve_kernel<5, PIPE_NONE>,
+                        (const void*)far_solve_kernel<3, PIPE_PREP>, (const void*)far_solve_kernel<5, PIPE_PREP>,
                         (const void*)far_stream_kernel<3>, (const void*)far_stream_kernel<5>};
   const void* pfns[6] = {(const void*)far_member0_kernel<3>, (const void*)far_member0_kernel<5>,
                          (const void*)far_members_kernel<3>, (const void*)far_members_kernel<5>,
                          (const void*)far_winner_kernel<3>, (const void*)far_winner_kernel<5>};
   for (const void* f : pfns) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384));
+  CK(cudaFuncSetAttribute((const void*)far_finish_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
+  CK(cudaFuncSetAttribute((const void*)far_finish_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   for (const void* f : fns) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   ctx->inited = true;
   return FAR_OK;
@@ -106,6 +117,44 @@ static far_status grow(far_ctx* ctx, char** buf, size_t* have, size_t bytes) {
   return FAR_OK;
 }
 static far_status ensure_buf(far_ctx* ctx, size_t bytes) { return grow(ctx, &ctx->d_buf, &ctx->d_buf_bytes, bytes); }
+
+// ---- per-stage timing (far_stage_timing): one event set per solver launch, stage boundaries
+static far_status t_collect(far_ctx* ctx, far_ctx::EvSet& e) {
+  if (!e.pending) return FAR_OK;
+  CK(cudaEventSynchronize(e.ev[e.nev - 1]));
+  for (int i = 1; i < e.nev; ++i) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e.ev[i - 1], e.ev[i]));
+    ctx->stage_ms[e.stage[i]] += ms;
+  }
+  e.pending = false;
+  ++ctx->timed;
+  return FAR_OK;
+}
+static far_status t_begin(far_ctx* ctx, cudaStream_t s, far_ctx::EvSet*& set) {
+  set = nullptr;
+  if (!ctx->timing) return FAR_OK;
+  far_ctx::EvSet& e = ctx->tsets[ctx->tnext];
+  ctx->tnext = (ctx->tnext + 1) % far_ctx::NSETS;
+  far_status st = t_collect(ctx, e);
+  if (st) return st;
+  if (!e.created) {
+    for (int i = 0; i < 10; ++i) CK(cudaEventCreate(&e.ev[i]));
+    e.created = true;
+  }
+  e.nev = 0;
+  CK(cudaEventRecord(e.ev[e.nev], s));
+  e.stage[e.nev++] = -1;
+  set = &e;
+  return FAR_OK;
+}
+static far_status t_mark(far_ctx* ctx, far_ctx::EvSet* set, cudaStream_t s, int stage) {
+  if (!set || set->nev >= 10) return FAR_OK;
+  CK(cudaEventRecord(set->ev[set->nev], s));
+  set->stage[set->nev++] = stage;
+  set->pending = true;
+  return FAR_OK;
+}
 
 template <int NC> static Layout layout_for(int n, int kcap) {
   return make_layout(n, NC, Tree<NC>::S, Tree<NC>::NN, kcap);
@@ -135,21 +184,27 @@ static far_status pick_shape(far_ctx* ctx, const void* fn, int bytes, int& warps
 }
 
 // One launch of the warp-per-instance kernel over I instances (or over the flagged ones).
-static far_status launch_warp_kernel(far_ctx* ctx, KParams& P, cudaStream_t stream, int64_t units) {
+static far_status launch_warp_kernel(far_ctx* ctx, KParams& P, cudaStream_t stream, int64_t units, int pipe) {
   const bool a30 = ctx->nc == 3;
-  const void* fn = a30 ? (const void*)far_solve_kernel<3> : (const void*)far_solve_kernel<5>;
-  Layout L = a30 ? layout_for<3>(P.n, P.kcap) : layout_for<5>(P.n, P.kcap);
+  const void* fn = pipe == PIPE_PREP
+                       ? (a30 ? (const void*)far_solve_kernel<3, PIPE_PREP> : (const void*)far_solve_kernel<5, PIPE_PREP>)
+                       : (a30 ? (const void*)far_solve_kernel<3, PIPE_NONE> : (const void*)far_solve_kernel<5, PIPE_NONE>);
+  Layout L = make_layout(P.n, ctx->nc, ctx->ns, ctx->nn, P.kcap, pipe);
   if (const char* pad = getenv("FAR_DEBUG_SMEM_PAD")) L.bytes += (atoi(pad) + 15) & ~15;  // occupancy experiments
   int warps = 0, per_sm = 0;
   far_status st = pick_shape(ctx, fn, L.bytes, warps, per_sm);
   if (st) return st;
   const size_t smem = (size_t)warps * L.bytes;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((units + warps - 1) / warps, (int64_t)ctx->sms * per_sm));
-  if (a30)
-    far_solve_kernel<3><<<grid, warps * 32, smem, stream>>>(P);
-  else
-    far_solve_kernel<5><<<grid, warps * 32, smem, stream>>>(P);
+  if (pipe == PIPE_PREP) {
+    if (a30) far_solve_kernel<3, PIPE_PREP><<<grid, warps * 32, smem, stream>>>(P);
+    else far_solve_kernel<5, PIPE_PREP><<<grid, warps * 32, smem, stream>>>(P);
+  } else {
+    if (a30) far_solve_kernel<3, PIPE_NONE><<<grid, warps * 32, smem, stream>>>(P);
+    else far_solve_kernel<5, PIPE_NONE><<<grid, warps * 32, smem, stream>>>(P);
+  }
   CK(cudaGetLastError());
+  ++ctx->launches;
   return FAR_OK;
 }
 
@@ -188,6 +243,8 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     CK(cudaMemsetAsync(P.ovf, 0, words * 4, stream));
   }
   far_status st;
+  far_ctx::EvSet* tset = nullptr;
+  if ((st = t_begin(ctx, stream, tset))) return st;
   if (pipe) {
     // ---- workspace for this launch
     const Layout LF = a30 ? layout_for<3>(P.n, kfast) : layout_for<5>(P.n, kfast);
@@ -212,11 +269,11 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     P.ws_ecap1 = ecap1;
     P.ws_kcap = kfast;
     // ---- K1: H0-H3 per instance (warp)
-    P.pipe = PIPE_PREP;
     P.kcap = kfast;
     P.ovf_pass = 0;
     P.counter = ctx->d_counter + slot + 0;
-    if ((st = launch_warp_kernel(ctx, P, stream, P.I))) return st;
+    if ((st = launch_warp_kernel(ctx, P, stream, P.I, PIPE_PREP))) return st;
+    if ((st = t_mark(ctx, tset, stream, FAR_STAGE_PREP))) return st;
     // ---- K2-K4: phase 2 at lane granularity
     PParams Q;
     memset(&Q, 0, sizeof(Q));
@@ -237,35 +294,48 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     const size_t psm = (size_t)4 * NC * tb + (size_t)2 * NN * tb;
     const int g_inst = (int)std::min<int64_t>((P.I + tb - 1) / tb, (int64_t)ctx->sms * 16);
     const int g_items = ctx->sms * 16;
-    if (a30) {
-      far_member0_kernel<3><<<g_inst, tb, psm, stream>>>(Q);
-      far_members_kernel<3><<<g_items, tb, psm, stream>>>(Q);
-      far_winner_kernel<3><<<g_inst, tb, psm, stream>>>(Q);
-    } else {
-      far_member0_kernel<5><<<g_inst, tb, psm, stream>>>(Q);
-      far_members_kernel<5><<<g_items, tb, psm, stream>>>(Q);
-      far_winner_kernel<5><<<g_inst, tb, psm, stream>>>(Q);
-    }
+    if (a30) far_member0_kernel<3><<<g_inst, tb, psm, stream>>>(Q);
+    else far_member0_kernel<5><<<g_inst, tb, psm, stream>>>(Q);
     CK(cudaGetLastError());
-    // ---- K5: H6-H7 per instance (warp)
-    P.pipe = PIPE_FINISH;
-    P.kcap = 1;
+    if ((st = t_mark(ctx, tset, stream, FAR_STAGE_MEMBER0))) return st;
+    if (a30) far_members_kernel<3><<<g_items, tb, psm, stream>>>(Q);
+    else far_members_kernel<5><<<g_items, tb, psm, stream>>>(Q);
+    CK(cudaGetLastError());
+    if ((st = t_mark(ctx, tset, stream, FAR_STAGE_MEMBERS))) return st;
+    if (a30) far_winner_kernel<3><<<g_inst, tb, psm, stream>>>(Q);
+    else far_winner_kernel<5><<<g_inst, tb, psm, stream>>>(Q);
+    CK(cudaGetLastError());
+    ctx->launches += 3;
+    if ((st = t_mark(ctx, tset, stream, FAR_STAGE_WINNER))) return st;
+    // ---- K5: H6-H7 per instance (warp), compact layout
     P.counter = ctx->d_counter + slot + 5;
-    if ((st = launch_warp_kernel(ctx, P, stream, P.I))) return st;
-    P.pipe = PIPE_NONE;
+    {
+      const FLayout FL = make_flayout(P.n, NN);
+      const int fw = 4;
+      int per_sm = 0;
+      const void* ffn = a30 ? (const void*)far_finish_kernel<3> : (const void*)far_finish_kernel<5>;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ffn, fw * 32, (size_t)fw * FL.bytes));
+      if (per_sm < 1) return fail(ctx, FAR_E_TOO_LARGE, "finish layout does not fit in shared memory");
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((P.I + fw - 1) / fw, (int64_t)ctx->sms * per_sm));
+      if (a30) far_finish_kernel<3><<<grid, fw * 32, (size_t)fw * FL.bytes, stream>>>(P);
+      else far_finish_kernel<5><<<grid, fw * 32, (size_t)fw * FL.bytes, stream>>>(P);
+      CK(cudaGetLastError());
+      ++ctx->launches;
+    }
+    if ((st = t_mark(ctx, tset, stream, FAR_STAGE_FINISH))) return st;
   } else {
-    P.pipe = PIPE_NONE;
     P.kcap = kfast;
     P.ovf_pass = 0;
     P.counter = ctx->d_counter + slot + 0;
-    if ((st = launch_warp_kernel(ctx, P, stream, P.I))) return st;
+    if ((st = launch_warp_kernel(ctx, P, stream, P.I, PIPE_NONE))) return st;
+    if ((st = t_mark(ctx, tset, stream, FAR_STAGE_FUSED))) return st;
   }
   if (need_ovf) {  // instances deferred by the fast layout / the pipeline: fused kernel, full layout
-    P.pipe = PIPE_NONE;
     P.kcap = kmax;
     P.ovf_pass = 1;
     P.counter = ctx->d_counter + slot + 1;
-    if ((st = launch_warp_kernel(ctx, P, stream, (P.I + 31) / 32))) return st;
+    if ((st = launch_warp_kernel(ctx, P, stream, (P.I + 31) / 32, PIPE_NONE))) return st;
+    if ((st = t_mark(ctx, tset, stream, FAR_STAGE_OVERFLOW))) return st;
   }
   return FAR_OK;
 }
@@ -340,6 +410,9 @@ void far_destroy(far_ctx* ctx) {
       if (ctx->d_pws[r]) cudaFree(ctx->d_pws[r]);
     cudaStreamDestroy(ctx->s[0]);
     cudaStreamDestroy(ctx->s[1]);
+    for (auto& e : ctx->tsets)
+      if (e.created)
+        for (auto& v : e.ev) cudaEventDestroy(v);
   }
   delete ctx;
 }
@@ -349,6 +422,26 @@ const int32_t* far_sizes(const far_ctx* ctx) { return ctx ? ctx->sizes : nullptr
 int32_t far_num_nodes(const far_ctx* ctx) { return ctx ? ctx->nn : -1; }
 int32_t far_num_slices(const far_ctx* ctx) { return ctx ? ctx->ns : -1; }
 const char* far_last_error(const far_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+far_status far_stage_timing(far_ctx* ctx, int32_t enable) {
+  if (!ctx) return FAR_E_INVALID_ARG;
+  ctx->timing = enable != 0;
+  return FAR_OK;
+}
+
+int32_t far_stage_times(far_ctx* ctx, float* ms) {
+  if (!ctx) return -1;
+  for (int i = 0; i < far_ctx::NSETS; ++i)  // oldest first
+    if (t_collect(ctx, ctx->tsets[(ctx->tnext + i) % far_ctx::NSETS]) != FAR_OK) return -1;
+  if (ms)
+    for (int s = 0; s < FAR_NUM_STAGES; ++s) ms[s] = (float)ctx->stage_ms[s];
+  const int n = ctx->timed;
+  for (double& v : ctx->stage_ms) v = 0.0;
+  ctx->timed = 0;
+  return n;
+}
+
+int64_t far_launch_count(const far_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
 far_status far_node_table(const far_ctx* ctx, int32_t* lo, int32_t* hi, int32_t* parent) {
   if (!ctx || !lo || !hi || !parent) return FAR_E_INVALID_ARG;
@@ -572,10 +665,13 @@ extern "C" far_status far_concat_streams(far_ctx* ctx, const int32_t* d_times, i
   if (warps < 1) return fail(ctx, FAR_E_TOO_LARGE, "stream state does not fit in shared memory");
   const size_t smem = (size_t)warps * L.bytes;
   const int grid = (int)((S + warps - 1) / warps);
+  far_ctx::EvSet* tset = nullptr;
+  if ((st = t_begin(ctx, stream, tset))) return st;
   if (a30)
     far_stream_kernel<3><<<grid, warps * 32, smem, stream>>>(Q);
   else
     far_stream_kernel<5><<<grid, warps * 32, smem, stream>>>(Q);
   CK(cudaGetLastError());
-  return FAR_OK;
+  ++ctx->launches;
+  return t_mark(ctx, tset, stream, FAR_STAGE_STREAM);
 }

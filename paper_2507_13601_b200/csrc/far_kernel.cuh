@@ -49,7 +49,6 @@ struct KParams {
   unsigned* ovf;                // bit per instance: family larger than kcap -> overflow pass
   unsigned long long* ovf_count;
   int ovf_pass;                 // 1: solve only the instances flagged in ovf (full layout)
-  int pipe;                     // PIPE_NONE: fused; PIPE_PREP: H0-H3 -> ws; PIPE_FINISH: ws -> H6-H7
   // pipelined phase 2 workspace (far_pipeline.cuh), strides in elements
   int2* ws_ent;                 // [I][ws_ecap1] list entries {t | task << 22, lo | hi << 16}
   int* ws_lb;                   // [I][ws_kcap]  lower bound of each member's makespan
@@ -61,7 +60,7 @@ struct KParams {
   int* ws_sl;                   // [I][8]        k*'s slice ends
   int ws_ecap1, ws_kcap;
 };
-enum { PIPE_NONE = 0, PIPE_PREP = 1, PIPE_FINISH = 2 };
+enum { PIPE_NONE = 0, PIPE_PREP = 1 };  // far_solve_kernel template modes: fused / H0-H3 -> ws
 enum { WS_FLAG = 8, WS_K = 9 };  // ws_meta slots: flag 0 = phase 2 pending, 1 = finished or deferred
 
 // Per-warp shared-memory layout (bytes), identical on host and device.  kcap bounds the
@@ -72,7 +71,7 @@ struct Layout {
 
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
 
-__host__ __device__ inline Layout make_layout(int n, int NC, int S, int NN, int kcap) {
+__host__ __device__ inline Layout make_layout(int n, int NC, int S, int NN, int kcap, int pipe = 0) {
   Layout L;
   (void)S;
   int Ecap = n + kcap - 1;
@@ -89,10 +88,10 @@ __host__ __device__ inline Layout make_layout(int n, int NC, int S, int NN, int 
   L.cur = o;      o = al16(o + n);
   L.su = o;       o = al16(o + n);
   L.bestnode = o; o = al16(o + n);
-  int sc = 32 * n;                              // phase-2 node record [n][32]
+  int sc = pipe == 1 ? 0 : 32 * n;             // phase-2 node record [n][32] (not in PIPE_PREP)
   if (10 * Ecap > sc) sc = 10 * Ecap;           // list sort scratch
   if (4 * n * NC > sc) sc = 4 * n * NC;         // phase-1 member intervals
-  if (2 * NN * n > sc) sc = 2 * NN * n;         // node lists
+  if (pipe != 1 && 2 * NN * n + 4 * n + 4 > sc) sc = 2 * NN * n + 4 * n + 4;  // node lists + durations
   L.scratch = o;  o = al16(o + sc);
   L.scr = sc;
   L.lstate = o;   o = al16(o + 4 * NC * 32);
@@ -618,38 +617,34 @@ __device__ void lists_from_record(int n, const uint32_t* rec, uint16_t* nlist, i
 }
 
 // H6/H7 of one instance (warp): node lists of k*, phase 3, replay, keep-best guard, stores.
-template <int NC>
-__device__ void finish_instance(const KParams& P, int64_t inst, unsigned char* wsm, const Layout& L,
-                                const uint32_t* ninfo, const int* cr, const int* de, int lane, far_result R, int ms2,
-                                int bestk, bool want_sched, bool refine) {
-  constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
+// FROM_REC: k*'s lists come from the pipelined phase-2 record (far_pipeline.cuh) and the
+// durations from the global runtime table; else from the fused kernel's H3 lists in smem.
+template <int NC, bool FROM_REC>
+__device__ void finish_core(const KParams& P, int64_t inst, uint16_t* nlist, int* D, int* start, uint8_t* onode,
+                            uint8_t* su, int* misc, const int32_t* T, const int2* lent, const uint16_t* ltask,
+                            const uint8_t* bestnode, const uint32_t* ninfo, const int* cr, const int* de, int lane,
+                            far_result R, int ms2, int bestk, bool want_sched, bool refine) {
+  constexpr int S = Tree<NC>::S;
   const int n = P.n;
-  int32_t* T = (int32_t*)(wsm + L.times);
-  int2* lent = (int2*)(wsm + L.lent);
-  uint16_t* ltask = (uint16_t*)(wsm + L.ltask);
-  uint8_t* cur = wsm + L.cur;
-  uint8_t* su = wsm + L.su;
-  uint8_t* bestnode = wsm + L.bestnode;
-  unsigned char* scratch = wsm + L.scratch;
-  int* start = (int*)(wsm + L.start);
-  int* misc = (int*)(wsm + L.misc);
   int* loff = misc + M_LOFF;
   int* ncnt = misc + M_NCNT;
   int* nsum = misc + M_NSUM;
   int* send = misc + M_SEND;
   int* bsend = misc + M_BSEND;
   int* life = misc + M_LIFE;
-  // ---- H6/H7: node lists of k*, phase 3, replay, keep-best guard.  One call site per
-  // helper (pass 1 only runs when the guard reverts to the phase-2 tree) keeps the code
-  // small enough for the instruction cache.
-  uint16_t* nlist = (uint16_t*)scratch;
+  // One call site per helper (pass 1 only runs when the guard reverts to the phase-2 tree)
+  // keeps the code small enough for the instruction cache.
   int msF = ms2;
   const bool need_replay = refine || want_sched;
   for (int pass = 0; pass < 2; ++pass) {
-    if (P.pipe == PIPE_FINISH) lists_from_record<NC>(n, P.ws_rec + inst * (int64_t)n, nlist, ncnt, su, lane);
-    else build_node_lists<NC>(n, bestk, lent, ltask, loff, bestnode, nlist, ncnt, su, lane);
-    int* D = (int*)(scratch + ((2 * NN * n + 3) & ~3));  // durations at the tasks' sizes (scratch >= 32n)
-    for (int j = lane; j < n; j += 32) D[j] = T[j * NC + su[j]];
+    if (FROM_REC) {
+      lists_from_record<NC>(n, P.ws_rec + inst * (int64_t)n, nlist, ncnt, su, lane);
+      const int32_t* gt = P.times + inst * (int64_t)n * NC;
+      for (int j = lane; j < n; j += 32) D[j] = __ldg(gt + j * NC + su[j]);
+    } else {
+      build_node_lists<NC>(n, bestk, lent, ltask, loff, bestnode, nlist, ncnt, su, lane);
+      for (int j = lane; j < n; j += 32) D[j] = T[j * NC + su[j]];
+    }
     __syncwarp();
     const bool ref = refine && pass == 0;
     if (ref) {
@@ -661,7 +656,7 @@ __device__ void finish_instance(const KParams& P, int64_t inst, unsigned char* w
       R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
     }
     if (!need_replay) break;
-    const int msR = replay_warp<NC>(n, D, nlist, ncnt, nsum, life, start, cur, ninfo, cr, de, lane);
+    const int msR = replay_warp<NC>(n, D, nlist, ncnt, nsum, life, start, onode, ninfo, cr, de, lane);
     if (ref && !(P.flags & FAR_NO_GUARD) && msR > ms2) {
       R.reverted = 1;  // keep-best guard: return the phase-2 schedule (replayed in pass 1)
       if (!want_sched) break;
@@ -675,7 +670,7 @@ __device__ void finish_instance(const KParams& P, int64_t inst, unsigned char* w
     far_task_slot* out = P.sched + inst * (int64_t)n;
     for (int j = lane; j < n; j += 32) {
       far_task_slot s;
-      s.node = cur[j];
+      s.node = onode[j];
       s.size_used = (uint8_t)size_of<NC>(su[j]);
       s.pad[0] = s.pad[1] = 0;
       s.start = start[j];
@@ -689,10 +684,23 @@ __device__ void finish_instance(const KParams& P, int64_t inst, unsigned char* w
   __syncwarp();
 }
 
+template <int NC>
+__device__ __forceinline__ void finish_instance(const KParams& P, int64_t inst, unsigned char* wsm, const Layout& L,
+                                                const uint32_t* ninfo, const int* cr, const int* de, int lane,
+                                                far_result R, int ms2, int bestk, bool want_sched, bool refine) {
+  constexpr int NN = Tree<NC>::NN;
+  unsigned char* scratch = wsm + L.scratch;
+  finish_core<NC, false>(P, inst, (uint16_t*)scratch, (int*)(scratch + ((2 * NN * P.n + 3) & ~3)),
+                         (int*)(wsm + L.start), wsm + L.cur, wsm + L.su, (int*)(wsm + L.misc),
+                         (const int32_t*)(wsm + L.times), (const int2*)(wsm + L.lent),
+                         (const uint16_t*)(wsm + L.ltask), wsm + L.bestnode, ninfo, cr, de, lane, R, ms2, bestk,
+                         want_sched, refine);
+}
+
 // ---------------------------------------------------------------------------
 // One instance, one warp.
 // ---------------------------------------------------------------------------
-template <int NC>
+template <int NC, int PIPE>
 __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* wsm, const Layout& L,
                                const uint32_t* ninfo, const int* cr, const int* de, int lane) {
   constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
@@ -766,13 +774,13 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         P.makespan[inst] = -1;
         if (P.res) P.res[inst] = R;
         atomicOr(P.errflag, 1);
-        if (P.pipe == PIPE_PREP) P.ws_meta[inst * 16 + WS_FLAG] = 1;
+        if (PIPE == PIPE_PREP) P.ws_meta[inst * 16 + WS_FLAG] = 1;
       }
       return;
     }
   }
 
-  if (P.mode == MODE_LOCAL) {
+  if (PIPE == PIPE_NONE && P.mode == MODE_LOCAL) {
     solve_local<NC>(P, inst, wsm, L, ninfo, cr, de, lane, R, want_sched, refine);
     return;
   }
@@ -781,26 +789,10 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     if (lane == 0) {
       P.makespan[inst] = 0;
       if (P.res) P.res[inst] = R;
-      if (P.pipe == PIPE_PREP) P.ws_meta[inst * 16 + WS_FLAG] = 1;
+      if (PIPE == PIPE_PREP) P.ws_meta[inst * 16 + WS_FLAG] = 1;
     }
     return;
   }
-  if (P.pipe == PIPE_FINISH) {  // phase 2 was done by the lane-level kernels (far_pipeline.cuh)
-    const int* meta = P.ws_meta + inst * 16;
-    if (meta[WS_FLAG]) return;  // error / empty / deferred to the overflow pass
-    const unsigned long long best = P.ws_best[inst];
-    ms2 = (int)(best >> 16);
-    bestk = (int)(best & 0xFFFFu);
-    R.family_size = meta[WS_K];
-    R.alloc_index = bestk;
-    R.makespan_phase2 = ms2;
-    R.events = (long long)P.ws_evt[inst];
-    if (lane < S) bsend[lane] = P.ws_sl[inst * 8 + lane];
-    __syncwarp();
-    finish_instance<NC>(P, inst, wsm, L, ninfo, cr, de, lane, R, ms2, bestk, want_sched, refine);
-    return;
-  }
-
   // ---- H1: first allocation a^1_i = argmin_s s*t_i(s), ties -> smallest s
   uint32_t* ivl = (uint32_t*)scratch;  // [n][NC] member interval lo | hi<<16 (0xFFFF = absent/open)
   unsigned long long c0pack = 0;
@@ -860,7 +852,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   // ---- H2: a^{k+1}: grow the longest task (ties -> lowest index) to
   //          argmin_{s > a_j} s*t_j(s) (ties -> smallest s); stop when it is at max size
   const bool small = tmax < (1 << 22);
-  if (P.pipe == PIPE_PREP && (!small || n > 1023)) {  // entries pack t < 2^22 and task < 1023
+  if (PIPE == PIPE_PREP && (!small || n > 1023)) {  // entries pack t < 2^22 and task < 1023
     if (lane == 0) {
       atomicOr(P.ovf + (inst >> 5), 1u << (inst & 31));
       atomicAdd(P.ovf_count, 1ull);
@@ -900,7 +892,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       if (lane == 0) {
         atomicOr(P.ovf + (inst >> 5), 1u << (inst & 31));
         atomicAdd(P.ovf_count, 1ull);
-        if (P.pipe == PIPE_PREP) P.ws_meta[inst * 16 + WS_FLAG] = 1;
+        if (PIPE == PIPE_PREP) P.ws_meta[inst * 16 + WS_FLAG] = 1;
       }
       return;
     }
@@ -1007,7 +999,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         if (lane == 0) {
           atomicOr(P.ovf + (inst >> 5), 1u << (inst & 31));
           atomicAdd(P.ovf_count, 1ull);
-          if (P.pipe == PIPE_PREP) P.ws_meta[inst * 16 + WS_FLAG] = 1;
+          if (PIPE == PIPE_PREP) P.ws_meta[inst * 16 + WS_FLAG] = 1;
         }
         return;
       }
@@ -1126,7 +1118,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     }
   }
 
-  if (P.pipe == PIPE_PREP) {  // hand the lists and the family to the lane-level phase 2
+  if (PIPE == PIPE_PREP) {  // hand the lists and the family to the lane-level phase 2
     const int E = loff[NC];
     int2* ge = P.ws_ent + inst * (int64_t)P.ws_ecap1;
     for (int e = lane; e < E; e += 32) {
@@ -1285,7 +1277,7 @@ __constant__ uint32_t c_nodes5[13] = {
     Tree<5>::node[5], Tree<5>::node[6], Tree<5>::node[7],  Tree<5>::node[8],  Tree<5>::node[9],
     Tree<5>::node[10], Tree<5>::node[11], Tree<5>::node[12]};
 
-template <int NC>
+template <int NC, int PIPE>
 __global__ void __launch_bounds__(128) far_solve_kernel(KParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t ninfo[16];
@@ -1298,7 +1290,7 @@ __global__ void __launch_bounds__(128) far_solve_kernel(KParams P) {
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Layout L = make_layout(P.n, NC, Tree<NC>::S, NN, P.kcap);
+  const Layout L = make_layout(P.n, NC, Tree<NC>::S, NN, P.kcap, PIPE);
   unsigned char* wsm = smem + (size_t)warp * L.bytes;
   // per-warp copies of the node table and costs (addressed off the warp's base register)
   {
@@ -1319,7 +1311,7 @@ __global__ void __launch_bounds__(128) far_solve_kernel(KParams P) {
       if (lane == 0) inst = atomicAdd(P.counter, 1ull);
       inst = __shfl_sync(FULL, inst, 0);
       if ((int64_t)inst >= P.I) break;
-      solve_instance<NC>(P, (int64_t)inst, wsm, L, wninfo, wcr, wde, lane);
+      solve_instance<NC, PIPE>(P, (int64_t)inst, wsm, L, wninfo, wcr, wde, lane);
       __syncwarp();
     }
   } else {
@@ -1334,7 +1326,7 @@ __global__ void __launch_bounds__(128) far_solve_kernel(KParams P) {
       while (bits) {
         const int b = __ffs(bits) - 1;
         bits &= bits - 1;
-        solve_instance<NC>(P, (int64_t)wd * 32 + b, wsm, L, wninfo, wcr, wde, lane);
+        solve_instance<NC, PIPE>(P, (int64_t)wd * 32 + b, wsm, L, wninfo, wcr, wde, lane);
         __syncwarp();
       }
     }

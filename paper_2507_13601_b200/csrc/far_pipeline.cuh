@@ -11,7 +11,8 @@
 //   K3 far_members_kernel            lane / item (instance, member): Alg. 1, atomicMin of
 //                                    (makespan << 16 | k) per instance -- argmin (makespan, k)
 //   K4 far_winner_kernel             lane / instance: re-runs k* when k* != 0, recording it
-//   K5 far_solve_kernel PIPE_FINISH  warp / instance: H6-H7 from the record
+//   K5 far_finish_kernel             warp / instance: H6-H7 from the record (compact layout:
+//                                    node lists + durations, no runtime table in smem)
 // Every lane does useful work, and an instance costs ~1 + (candidates) member simulations
 // instead of a 32-lane pass.  The result is identical to the fused kernel's (same readings,
 // same tie-breaks: the packed key orders (makespan, k) lexicographically).
@@ -232,6 +233,69 @@ __global__ void __launch_bounds__(128) far_winner_kernel(PParams P) {
     int pops = 0;
     sim_member<NC, true>(P.ws_ent + i * (int64_t)P.ws_ecap1, loff, P.ws_cnt[i * (int64_t)P.ws_kcap + k], k,
                          sm.ninfo, sm.cr, sm.de, st, npos, bdim, P.ws_rec + i * (int64_t)P.n, P.ws_sl + i * 8, pops);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: H6/H7 per instance (warp) from the record of k*.  Per-warp shared memory holds only
+// what phase 3 and the replay touch: node lists [NN][n] u16, durations D[n] (gathered from
+// the global runtime table at the recorded sizes; durations never change in phase 3),
+// starts, nodes, size indices and the small misc block.
+// ---------------------------------------------------------------------------
+struct FLayout {
+  int misc, nlist, D, start, onode, su, bytes;
+};
+__host__ __device__ inline FLayout make_flayout(int n, int NN) {
+  FLayout L;
+  int o = 0;
+  L.misc = o;  o = al16(o + 4 * 224);
+  L.nlist = o; o = al16(o + 2 * NN * n);
+  L.D = o;     o = al16(o + 4 * n);
+  L.start = o; o = al16(o + 4 * n);
+  L.onode = o; o = al16(o + n);
+  L.su = o;    o = al16(o + n);
+  L.bytes = o;
+  return L;
+}
+
+template <int NC>
+__global__ void __launch_bounds__(128, 8) far_finish_kernel(KParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const FLayout L = make_flayout(P.n, NN);
+  unsigned char* wsm = smem + (size_t)warp * L.bytes;
+  int* misc = (int*)(wsm + L.misc);
+  if (lane < 16) misc[M_NINFO + lane] = lane < NN ? (int)((NC == 3) ? c_nodes3[lane] : c_nodes5[lane]) : 0;
+  if (lane < 8) {
+    misc[M_CR + lane] = P.cr[lane];
+    misc[M_DE + lane] = P.de[lane];
+  }
+  __syncwarp();
+  const uint32_t* ninfo = (const uint32_t*)misc + M_NINFO;
+  const int* cr = misc + M_CR;
+  const int* de = misc + M_DE;
+  const bool want_sched = P.sched != nullptr && !(P.flags & FAR_NO_SCHEDULE);
+  const bool refine = !(P.flags & FAR_NO_REFINE);
+  for (;;) {
+    unsigned long long u = 0;
+    if (lane == 0) u = atomicAdd(P.counter, 1ull);
+    u = __shfl_sync(FULL, u, 0);
+    const int64_t inst = (int64_t)u;
+    if (inst >= P.I) break;
+    const int* meta = P.ws_meta + inst * 16;
+    if (meta[WS_FLAG]) continue;  // error / empty (K1 wrote the outputs) / deferred to the overflow pass
+    const unsigned long long best = P.ws_best[inst];
+    const int ms2 = (int)(best >> 16), bestk = (int)(best & 0xFFFFu);
+    far_result R;
+    R.makespan = 0; R.makespan_phase2 = ms2; R.alloc_index = bestk; R.family_size = meta[WS_K];
+    R.moves = 0; R.swaps = 0; R.iterations = 0; R.reverted = 0; R.status = FAR_OK; R.reserved = 0;
+    R.evals = 0; R.events = (long long)P.ws_evt[inst];
+    if (lane < S) misc[M_BSEND + lane] = P.ws_sl[inst * 8 + lane];
+    __syncwarp();
+    finish_core<NC, true>(P, inst, (uint16_t*)(wsm + L.nlist), (int*)(wsm + L.D), (int*)(wsm + L.start),
+                          wsm + L.onode, wsm + L.su, misc, nullptr, nullptr, nullptr, nullptr, ninfo, cr, de, lane,
+                          R, ms2, bestk, want_sched, refine);
   }
 }
 

@@ -23,6 +23,8 @@ NO_REFINE, NO_GUARD, ZERO_RECONFIG, NO_SCHEDULE, EXHAUSTIVE = 1, 2, 4, 8, 16
 STATUS = {0: "FAR_OK", 1: "FAR_E_INVALID_ARG", 2: "FAR_E_UNSUPPORTED_PROFILE", 3: "FAR_E_BAD_TIME",
           4: "FAR_E_TOO_LARGE", 5: "FAR_E_CUDA", 6: "FAR_E_OOM"}
 
+STAGES = ("prep", "member0", "members", "winner", "finish", "overflow", "fused", "stream")  # FAR_STAGE_*
+
 SLOT_DT = np.dtype([("node", "u1"), ("size_used", "u1"), ("pad", "u1", 2), ("start", "<i4")])
 RESULT_DT = np.dtype([("makespan", "<i4"), ("makespan_phase2", "<i4"), ("alloc_index", "<i4"),
                       ("family_size", "<i4"), ("moves", "<i4"), ("swaps", "<i4"), ("iterations", "<i4"),
@@ -73,6 +75,9 @@ def lib():
             "far_solve_many": ([p, p, i64, i32, p, p, p, p, p], C.c_int),
             "far_solve_many_host": ([p, p, i64, i32, p, p, p, p], C.c_int),
             "far_concat_streams": ([p, p, i64, i32, i32, p, p, p, p, p, p, p], C.c_int),
+            "far_stage_timing": ([p, i32], C.c_int),
+            "far_stage_times": ([p, p], i32),
+            "far_launch_count": ([p], i64),
         }
         for name, (a, r) in sig.items():
             f = getattr(L, name)
@@ -132,6 +137,21 @@ class Far:
 
     def sync(self):
         self._check(lib().far_sync(self._h))
+
+    # -- diagnostics ------------------------------------------------------------------
+    def stage_timing(self, enable=True):
+        self._check(lib().far_stage_timing(self._h, 1 if enable else 0))
+
+    def stage_times(self):
+        """-> (number of timed launches, {stage: device ms summed over them}); resets the sums."""
+        ms = np.zeros(len(STAGES), np.float32)
+        k = lib().far_stage_times(self._h, _np_ptr(ms))
+        if k < 0:
+            raise FarError(5, lib().far_last_error(self._h).decode())
+        return k, {name: float(v) for name, v in zip(STAGES, ms)}
+
+    def launch_count(self):
+        return int(lib().far_launch_count(self._h))
 
     # -- single batch, host memory -------------------------------------------------
     def schedule_batch(self, times, **kw):
