@@ -63,6 +63,10 @@ struct KParams {
 enum { PIPE_NONE = 0, PIPE_PREP = 1 };  // far_solve_kernel template modes: fused / H0-H3 -> ws
 enum { WS_FLAG = 8, WS_K = 9 };  // ws_meta slots: flag 0 = phase 2 pending, 1 = finished or deferred
 
+// misc int slots (PIPE_PREP keeps only the first M_PREP_END: list offsets, node table, costs)
+enum { M_LOFF = 0, M_NINFO = 8, M_CR = 24, M_DE = 32, M_PREP_END = 40, M_NCNT = 40, M_NSUM = 56, M_SEND = 72,
+       M_BSEND = 80, M_LIFE = 88, M_MEMB = 184, M_END = 216 };
+
 // Per-warp shared-memory layout (bytes), identical on host and device.  kcap bounds the
 // family size K this layout holds (the per-size lists hold at most n + K - 1 entries).
 struct Layout {
@@ -94,16 +98,23 @@ __host__ __device__ inline Layout make_layout(int n, int NC, int S, int NN, int 
   if (pipe != 1 && 2 * NN * n + 4 * n + 4 > sc) sc = 2 * NN * n + 4 * n + 4;  // node lists + durations
   L.scratch = o;  o = al16(o + sc);
   L.scr = sc;
-  L.lstate = o;   o = al16(o + 4 * NC * 32);
-  L.start = o;    o = al16(o + 4 * n);
-  L.misc = o;     o = al16(o + 4 * 224);
+  L.lstate = o;   o = al16(o + (pipe == 1 ? 4 * kcap : 4 * NC * 32));  // PIPE_PREP: growth-step ranks only
+  L.start = o;    o = al16(o + (pipe == 1 ? 0 : 4 * n));
+  L.misc = o;     o = al16(o + 4 * (pipe == 1 ? (int)M_PREP_END : (int)M_END));
   L.bytes = o;
   return L;
 }
 
-// misc int slots
-enum { M_LOFF = 0, M_NCNT = 8, M_NSUM = 24, M_SEND = 40, M_BSEND = 48, M_LIFE = 56, M_MEMB = 152, M_NINFO = 184,
-       M_CR = 200, M_DE = 208 };
+// c += (v >= k) for unsigned v, k: the carry of v - k (no borrow) added in one pair
+__device__ __forceinline__ void count_ge(int& c, unsigned v, unsigned k) {
+  asm("{\n\t.reg .u32 t;\n\tsub.cc.u32 t, %1, %2;\n\taddc.u32 %0, %0, 0;\n\t}" : "+r"(c) : "r"(v), "r"(k));
+}
+
+// c += ((vhi, vlo) >= (khi, klo)) as unsigned 64-bit
+__device__ __forceinline__ void count_ge64(int& c, unsigned vlo, unsigned vhi, unsigned klo, unsigned khi) {
+  asm("{\n\t.reg .u32 t;\n\tsub.cc.u32 t, %1, %3;\n\tsubc.cc.u32 t, %2, %4;\n\taddc.u32 %0, %0, 0;\n\t}"
+      : "+r"(c) : "r"(vlo), "r"(vhi), "r"(klo), "r"(khi));
+}
 
 __device__ __forceinline__ long long warp_sum_ll(long long v) {
 #pragma unroll
@@ -719,11 +730,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   int* start = (int*)(wsm + L.start);
   int* misc = (int*)(wsm + L.misc);
   int* loff = misc + M_LOFF;
-  int* ncnt = misc + M_NCNT;
-  int* nsum = misc + M_NSUM;
-  int* send = misc + M_SEND;
   int* bsend = misc + M_BSEND;
-  int* life = misc + M_LIFE;
 
   // ---- H0: stage the runtime table (contiguous n*NC int32) into shared memory
   const int cntT = n * NC;
@@ -909,14 +916,16 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     }
     __syncwarp();
     // rank of each step: larger keys first; equal keys (same task) in chain order
+    // (64-bit compare of (key, 63 - pos): count the elements <= own, rank = Gn - that)
     for (int e = lane; e < Gn; e += 32) {
       const unsigned ke = (unsigned)G[e].x;
       const int pe = G[e].y >> 16;
-      int rk = 0;
+      int ge = 0;
       for (int f = 0; f < Gn; ++f) {
         const int2 g = G[f];
-        rk += ((unsigned)g.x > ke) || ((unsigned)g.x == ke && (g.y >> 16) < pe);
+        count_ge64(ge, 63u - (unsigned)pe, ke, 63u - ((unsigned)g.y >> 16), (unsigned)g.x);
       }
+      const int rk = Gn - ge;
       // step rk produces member rk + 1: longest task of member rk, deltas of member rk + 1
       const int j = G[e].y & 1023, cf = (G[e].y >> 10) & 7, ct = (G[e].y >> 13) & 7;
       lbh[rk] = (int)(ke >> 10);
@@ -963,12 +972,14 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     K = Gn + 1;
   } else {
     unsigned long long cp = c0pack;
-    uint32_t* ck = (uint32_t*)start;  // packed current key per task (start[] is free until H7)
+    // packed current key per task (start[] is free until H7; PIPE_PREP has no start[] and
+    // recomputes the keys)
+    uint32_t* ck = (uint32_t*)start;
     unsigned lk = 0;
     if (small) {
       for (int j = lane; j < n; j += 32) {
         const unsigned key = ((unsigned)T[j * NC + cur[j]] << 10) | (unsigned)(1023 - j);
-        ck[j] = key;
+        if (PIPE != PIPE_PREP) ck[j] = key;
         lk = max(lk, key);
       }
     }
@@ -1013,12 +1024,13 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         ivl[jj * NC + cj] = (ivl[jj * NC + cj] & 0xFFFFu) | ((uint32_t)K << 16);  // leaves size cj at member K
         ivl[jj * NC + best] = (uint32_t)K | 0xFFFF0000u;                          // enters size best at member K
         cnts[K] = cp;
-        if (small) ck[jj] = ((unsigned)T[jj * NC + best] << 10) | (unsigned)(1023 - jj);
+        if (small && PIPE != PIPE_PREP) ck[jj] = ((unsigned)T[jj * NC + best] << 10) | (unsigned)(1023 - jj);
       }
       __syncwarp();
       if (small && lane == (jj & 31)) {
         lk = 0;
-        for (int j = lane; j < n; j += 32) lk = max(lk, ck[j]);
+        for (int j = lane; j < n; j += 32)
+          lk = max(lk, PIPE == PIPE_PREP ? (((unsigned)T[j * NC + cur[j]] << 10) | (unsigned)(1023 - j)) : ck[j]);
       }
       ++K;
     }
@@ -1079,15 +1091,19 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
           yv[r] = i < m ? lent[b + i].y : 0;
           rk[r] = 0;
         }
+        // rk counts the keys >= own key (itself included) with one subtract-with-carry pair
+        // per comparison; the rank is then m - rk (keys are distinct)
         if (m <= 32) {
-          for (int f = 0; f < m; ++f) rk[0] += kk[f] < key[0];
+          for (int f = 0; f < m; ++f) count_ge(rk[0], kk[f], key[0]);
         } else {
           for (int f = 0; f < m; ++f) {
             const unsigned v = kk[f];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) rk[r] += v < key[r];
+            for (int r = 0; r < 4; ++r) count_ge(rk[r], v, key[r]);
           }
         }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) rk[r] = m - rk[r];
         __syncwarp();
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
