@@ -197,44 +197,61 @@ template <int S> struct Frontier {
 // durations.  The event loop pops keys in non-decreasing (time, first slice) order, so
 // both loops apply the same reconfiguration events in the same order and give identical
 // starts (a destroy charged after the last task started cannot delay any creation).  This
-// takes <= 2*#nodes heap steps on one lane instead of n + #nodes; task starts are then
-// prefix sums over each node list (one lane per node).  life[v*6] = {cs, ce, ds, de}.
-// ---------------------------------------------------------------------------
+// takes <= 2*#nodes heap steps instead of n + #nodes; task starts are then prefix sums
+// over each node list (one lane per node).  life[v*6] = {cs, ce, ds, de}.
+// The frontier is spread over the warp: lane s < S holds slot s's key
+// (end << 3 | s); the control state (rec, has, slot -> node map, live) is uniform, so every
+// lane follows the same path and a pop is one REDUX.MIN instead of an unrolled scan.
 template <int NC>
-__device__ int node_sim(const int* ncnt, const int* nsum, int* life, const uint32_t* ninfo, const int* cr,
-                        const int* de, int* Eout) {
-  constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
-  for (int v = 0; v < NN; ++v) life[v * 6] = -1;
-  Frontier<S> F;
-  F.init();
+__device__ int node_sim_warp(const int* ncnt, const int* nsum, int* life, const uint32_t* ninfo, const int* cr,
+                             const int* de, int lane, int& Eout) {
+  constexpr int NN = Tree<NC>::NN;
+  if (lane < NN) life[lane * 6] = -1;
+  unsigned e = lane == 0 ? 0u : 0xFFFFFFFFu;  // root in slot 0 at time 0
+  uint32_t slotnode = 0, live = 1, has = 0;
   int rec = 0, ms = 0, E = 0;
-  while (F.live) {
-    int bs, be;
-    F.pop(bs, be);
-    const int v = F.node(bs);
+  while (live) {
+    const unsigned m = __reduce_min_sync(FULL, e);
+    const int bs = (int)(m & 7u), be = (int)(m >> 3);
+    const int v = (int)((slotnode >> (4 * bs)) & 15u);
     const uint32_t w = ninfo[v];
-    if (!((F.has >> bs) & 1) && ncnt[v] > 0) {  // creation (lines 8-11), then all of v's tasks
+    if (!((has >> bs) & 1) && ncnt[v] > 0) {  // creation (lines 8-11), then all of v's tasks
       const int cs = max(rec, be);
       rec = cs + cr[nd_szi(w)];
-      life[v * 6 + 0] = cs;
-      life[v * 6 + 1] = rec;
+      if (lane == 0) {
+        life[v * 6 + 0] = cs;
+        life[v * 6 + 1] = rec;
+      }
       const int f = rec + nsum[v];
       ms = max(ms, f);
       E = max(E, f);
-      F.has |= 1u << bs;
-      F.set(bs, f);
-    } else {  // repartitioning (lines 17-24): destroy if it had tasks
-      if ((F.has >> bs) & 1) {
+      has |= 1u << bs;
+      if (lane == bs) e = ((unsigned)f << 3) | (unsigned)bs;
+    } else {  // repartitioning (lines 17-24): destroy if it had tasks, then split or drop
+      if ((has >> bs) & 1) {
         const int ds = max(rec, be);
         rec = ds + de[nd_szi(w)];
-        life[v * 6 + 2] = ds;
-        life[v * 6 + 3] = rec;
+        if (lane == 0) {
+          life[v * 6 + 2] = ds;
+          life[v * 6 + 3] = rec;
+        }
         E = max(E, rec);
       }
-      F.split(bs, be, w);
+      has &= ~(1u << bs);
+      const int ch1 = nd_ch1(w);
+      if (ch1 != LEAF) {  // children: slot bs (keeps its key) and slot ch2lo, both at be
+        const int s2 = nd_ch2lo(w);
+        slotnode = (slotnode & ~(15u << (4 * bs))) | ((uint32_t)ch1 << (4 * bs));
+        slotnode = (slotnode & ~(15u << (4 * s2))) | ((uint32_t)nd_ch2(w) << (4 * s2));
+        live |= 1u << s2;
+        if (lane == s2) e = ((unsigned)be << 3) | (unsigned)s2;
+      } else {
+        live &= ~(1u << bs);
+        if (lane == bs) e = 0xFFFFFFFFu;
+      }
     }
   }
-  *Eout = E;
+  Eout = E;
   return ms;
 }
 
@@ -261,10 +278,8 @@ __device__ int replay_warp(int n, const int* D, const uint16_t* nlist, const int
     nsum[lane] = acc;
   }
   __syncwarp();
-  int ms = 0, E = 0;
-  if (lane == 0) ms = node_sim<NC>(ncnt, nsum, life, ninfo, cr, de, &E);
-  ms = __shfl_sync(FULL, ms, 0);
-  E = __shfl_sync(FULL, E, 0);
+  int E = 0;
+  const int ms = node_sim_warp<NC>(ncnt, nsum, life, ninfo, cr, de, lane, E);
   __syncwarp();
   for (int j2 = lane; j2 < n; j2 += 32) start[j2] += life[onode[j2] * 6 + 1];
   __syncwarp();
@@ -279,6 +294,17 @@ __device__ int replay_warp(int n, const int* D, const uint16_t* nlist, const int
 template <int NC>
 __device__ void list_remove(uint16_t* lst, int* cnt, int j, int lane) {
   const int c = *cnt;
+  if (c <= 32) {  // one chunk: find by ballot, shift left by a shuffle
+    const int x = lane < c ? lst[lane] : -1;
+    const unsigned m = __ballot_sync(FULL, x == j);
+    const int q = __ffs(m) - 1;
+    const int y = __shfl_down_sync(FULL, x, 1);
+    __syncwarp();
+    if (lane >= q && lane < c - 1) lst[lane] = (uint16_t)y;
+    if (lane == 0) *cnt = c - 1;
+    __syncwarp();
+    return;
+  }
   int q = c;
   for (int b = 0; b < c; b += 32) {
     const unsigned m = __ballot_sync(FULL, b + lane < c && lst[b + lane] == j);
@@ -301,6 +327,21 @@ template <int NC>
 __device__ void list_insert(uint16_t* lst, int* cnt, int j, const int* D, int lane) {
   const int c = *cnt;
   const int dj = D[j];
+  if (c < 32) {  // one chunk: position by ballot, shift right by a shuffle
+    const int x = lane < c ? lst[lane] : 0;
+    bool before = false;
+    if (lane < c) {
+      const int dx = D[x];
+      before = dx > dj || (dx == dj && x < j);
+    }
+    const int pos = __popc(__ballot_sync(FULL, before));
+    const int y = __shfl_up_sync(FULL, x, 1);
+    __syncwarp();
+    if (lane <= c) lst[lane] = (uint16_t)(lane < pos ? x : (lane == pos ? j : y));
+    if (lane == 0) *cnt = c + 1;
+    __syncwarp();
+    return;
+  }
   int pos = 0;
   for (int b = 0; b < c; b += 32) {
     const int i = b + lane;
