@@ -95,6 +95,8 @@ static far_status ensure_device(far_ctx* ctx) {
                          (const void*)far_members_kernel<3>, (const void*)far_members_kernel<5>,
                          (const void*)far_winner_kernel<3>, (const void*)far_winner_kernel<5>};
   for (const void* f : pfns) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384));
+  CK(cudaFuncSetAttribute((const void*)far_member0_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
+  CK(cudaFuncSetAttribute((const void*)far_member0_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   CK(cudaFuncSetAttribute((const void*)far_finish_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   CK(cudaFuncSetAttribute((const void*)far_finish_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   for (const void* f : fns) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
@@ -254,7 +256,9 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     const size_t o_ent = 0, o_lb = o_ent + a256(I * ecap1 * 8), o_cnt = o_lb + a256(I * kfast * 4),
                  o_meta = o_cnt + a256(I * kfast * 8), o_best = o_meta + a256(I * 64), o_evt = o_best + a256(I * 8),
                  o_rec = o_evt + a256(I * 8), o_sl = o_rec + a256(I * P.n * 4), o_items = o_sl + a256(I * 32),
-                 o_end = o_items + a256(I * (size_t)(kfast - 1 > 0 ? kfast - 1 : 1) * 8);
+                 o_m0 = o_items + a256(I * (size_t)(kfast - 1 > 0 ? kfast - 1 : 1) * 8);
+    const int n4 = (P.n + 3) & ~3;
+    const size_t o_end = o_m0 + a256(I * (size_t)n4 * 4);
     const int r = ctx->launch_id & 1;
     if ((st = grow(ctx, &ctx->d_pws[r], &ctx->d_pws_bytes[r], o_end))) return st;
     char* w = ctx->d_pws[r];
@@ -268,6 +272,8 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     P.ws_sl = (int*)(w + o_sl);
     P.ws_ecap1 = ecap1;
     P.ws_kcap = kfast;
+    P.ws_m0 = (uint32_t*)(w + o_m0);
+    P.ws_n4 = n4;
     // ---- K1: H0-H3 per instance (warp)
     P.kcap = kfast;
     P.ovf_pass = 0;
@@ -287,6 +293,7 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     Q.ws_ent = P.ws_ent; Q.ws_lb = P.ws_lb; Q.ws_cnt = P.ws_cnt; Q.ws_meta = P.ws_meta;
     Q.ws_best = P.ws_best; Q.ws_evt = P.ws_evt; Q.ws_rec = P.ws_rec; Q.ws_sl = P.ws_sl;
     Q.ws_ecap1 = ecap1; Q.ws_kcap = kfast;
+    Q.ws_m0 = P.ws_m0; Q.ws_n4 = n4;
     Q.items = (int2*)(w + o_items);
     Q.nitems = ctx->d_counter + slot + 3;
     Q.counter = ctx->d_counter + slot + 4;
@@ -294,8 +301,18 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     const size_t psm = (size_t)4 * NC * tb + (size_t)2 * NN * tb;
     const int g_inst = (int)std::min<int64_t>((P.I + tb - 1) / tb, (int64_t)ctx->sms * 16);
     const int g_items = ctx->sms * 16;
-    if (a30) far_member0_kernel<3><<<g_inst, tb, psm, stream>>>(Q);
-    else far_member0_kernel<5><<<g_inst, tb, psm, stream>>>(Q);
+    {  // K2: per-thread shared-memory copy of member 0's lists -> block size by footprint
+      const size_t per_thread = (size_t)4 * NC + 2 * NN + 4 * (size_t)(n4 + 4);
+      const int tb0 = (int)std::min<size_t>(128, (size_t)ctx->smem_max / per_thread / 32 * 32);
+      if (tb0 < 32) return fail(ctx, FAR_E_TOO_LARGE, "member-0 lists do not fit in shared memory");
+      const size_t sm0 = per_thread * tb0;
+      const void* f0 = a30 ? (const void*)far_member0_kernel<3> : (const void*)far_member0_kernel<5>;
+      int per_sm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, tb0, sm0));
+      const int g0 = (int)std::max<int64_t>(1, std::min<int64_t>((P.I + tb0 - 1) / tb0, (int64_t)ctx->sms * std::max(1, per_sm)));
+      if (a30) far_member0_kernel<3><<<g0, tb0, sm0, stream>>>(Q);
+      else far_member0_kernel<5><<<g0, tb0, sm0, stream>>>(Q);
+    }
     CK(cudaGetLastError());
     if ((st = t_mark(ctx, tset, stream, FAR_STAGE_MEMBER0))) return st;
     if (a30) far_members_kernel<3><<<g_items, tb, psm, stream>>>(Q);
@@ -355,6 +372,11 @@ static void fill_params(far_ctx* ctx, const far_opts* o, KParams& P) {
   for (int c = 0; c < 8; ++c) {
     P.cr[c] = zero ? 0 : ctx->cr[c];
     P.de[c] = zero ? 0 : ctx->de[c];
+  }
+  P.rsum = 0;
+  for (int v = 0; v < ctx->nn; ++v) {
+    const int szi = nd_szi(ctx->nc == 3 ? Tree<3>::node[v] : Tree<5>::node[v]);
+    P.rsum += P.cr[szi] + P.de[szi];
   }
 }
 

@@ -19,6 +19,7 @@
 #pragma once
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "../../include/far.h"
 #include "far_tree.cuh"
@@ -59,6 +60,9 @@ struct KParams {
   uint32_t* ws_rec;             // [I][n]        k*'s placement: node | size idx << 4 | position << 7
   int* ws_sl;                   // [I][8]        k*'s slice ends
   int ws_ecap1, ws_kcap;
+  int rsum;                     // sum over tree nodes of create + destroy cost (integer-range check)
+  uint32_t* ws_m0;              // [I][ws_n4]    member 0's compact per-size LPT lists (t | task << 22)
+  int ws_n4;
 };
 enum { PIPE_NONE = 0, PIPE_PREP = 1 };  // far_solve_kernel template modes: fused / H0-H3 -> ws
 enum { WS_FLAG = 8, WS_K = 9 };  // ws_meta slots: flag 0 = phase 2 pending, 1 = finished or deferred
@@ -92,10 +96,17 @@ __host__ __device__ inline Layout make_layout(int n, int NC, int S, int NN, int 
   L.cur = o;      o = al16(o + n);
   L.su = o;       o = al16(o + n);
   L.bestnode = o; o = al16(o + n);
-  int sc = pipe == 1 ? 0 : 32 * n;             // phase-2 node record [n][32] (not in PIPE_PREP)
-  if (10 * Ecap > sc) sc = 10 * Ecap;           // list sort scratch
-  if (4 * n * NC > sc) sc = 4 * n * NC;         // phase-1 member intervals
-  if (pipe != 1 && 2 * NN * n + 4 * n + 4 > sc) sc = 2 * NN * n + 4 * n + 4;  // node lists + durations
+  int sc;
+  if (pipe == 1) {  // PIPE_PREP: u16 member intervals, the rank-sort keys, the long-list sort
+    sc = 2 * n * NC;
+    if (4 * n > sc) sc = 4 * n;
+    if (n > 128 && 10 * Ecap > sc) sc = 10 * Ecap;
+  } else {
+    sc = 32 * n;                                  // phase-2 node record [n][32]
+    if (10 * Ecap > sc) sc = 10 * Ecap;           // list sort scratch
+    if (4 * n * NC > sc) sc = 4 * n * NC;         // phase-1 member intervals
+    if (2 * NN * n + 4 * n + 4 > sc) sc = 2 * NN * n + 4 * n + 4;  // node lists + durations
+  }
   L.scratch = o;  o = al16(o + sc);
   L.scr = sc;
   L.lstate = o;   o = al16(o + (pipe == 1 ? 4 * kcap : 4 * NC * 32));  // PIPE_PREP: growth-step ranks only
@@ -813,9 +824,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     bad = __any_sync(FULL, bad);
     bsum = warp_sum_ll(bsum);
     tmax = __reduce_max_sync(FULL, tmax);
-    long long rsum = 0;
-    for (int v = 0; v < NN; ++v) rsum += cr[nd_szi(ninfo[v])] + de[nd_szi(ninfo[v])];
-    if (bad || bsum + rsum >= BOUND) {
+    if (bad || bsum + P.rsum >= BOUND) {
       if (lane == 0) {
         R.makespan = -1;
         R.status = FAR_E_BAD_TIME;
@@ -842,7 +851,12 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     return;
   }
   // ---- H1: first allocation a^1_i = argmin_s s*t_i(s), ties -> smallest s
-  uint32_t* ivl = (uint32_t*)scratch;  // [n][NC] member interval lo | hi<<16 (0xFFFF = absent/open)
+  // [n][NC] member interval lo | hi << IB (lo = IM: absent; hi = IM: open).  PIPE_PREP holds
+  // families of <= 64 members, so 8-bit bounds (half the shared memory) suffice there.
+  using IV = typename std::conditional<PIPE == PIPE_PREP, uint16_t, uint32_t>::type;
+  constexpr int IB = PIPE == PIPE_PREP ? 8 : 16;
+  constexpr uint32_t IM = (1u << IB) - 1u;
+  IV* ivl = (IV*)scratch;
   unsigned long long c0pack = 0;
   long long W = 0;  // total area sum_i a_i t_i(a_i) of the current member (uniform)
   bool mono = true;
@@ -851,12 +865,16 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     int cnt_c[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) cnt_c[c] = 0;
+    // (the checks above bound every t below 2^29, so size * t < 7 * 2^29 fits 32 bits unsigned)
     for (int j = lane; j < n; j += 32) {
+      unsigned tv[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) tv[c] = (unsigned)T[j * NC + c];
       int best = 0;
-      long long bw = (long long)size_of<NC>(0) * T[j * NC];
+      unsigned bw = (unsigned)size_of<NC>(0) * tv[0];
 #pragma unroll
       for (int c = 1; c < NC; ++c) {
-        const long long w = (long long)size_of<NC>(c) * T[j * NC + c];
+        const unsigned w = (unsigned)size_of<NC>(c) * tv[c];
         if (w < bw) { bw = w; best = c; }
       }
       cur[j] = (uint8_t)best;
@@ -865,29 +883,32 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       {
         unsigned packed = 0;
         int above = NC - 1;
-        long long wa = (long long)size_of<NC>(NC - 1) * T[j * NC + NC - 1];
+        unsigned wa = (unsigned)size_of<NC>(NC - 1) * tv[NC - 1];
 #pragma unroll
         for (int c = NC - 2; c >= 0; --c) {
           packed |= (unsigned)above << (3 * c);
-          const long long wc = (long long)size_of<NC>(c) * T[j * NC + c];
+          const unsigned wc = (unsigned)size_of<NC>(c) * tv[c];
           if (wc <= wa) { wa = wc; above = c; }
         }
         su[j] = (uint8_t)(packed & 0xFF);
         bestnode[j] = (uint8_t)(packed >> 8);
-        // growth chain a^1 -> nx -> ... -> max size: monotone (non-increasing t) chains allow
-        // the parallel phase-1 below
-        int c = best;
-        while (c != NC - 1) {
-          const int c2 = (int)((packed >> (3 * c)) & 7u);
-          mono = mono && T[j * NC + c2] <= T[j * NC + c];
-          c = c2;
-        }
-        tstar = max(tstar, ((unsigned)T[j * NC + NC - 1] << 10) | (unsigned)(1023 - j));
+        // growth chain a^1 -> nx -> ... -> max size (strictly increasing sizes, so one ascending
+        // scan): monotone (non-increasing t) chains allow the parallel phase-1 below
+        int nextc = best;
+        unsigned tprev = 0xFFFFFFFFu;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          if (c == nextc) {
+            mono = mono && tv[c] <= tprev;
+            tprev = tv[c];
+            nextc = c == NC - 1 ? NC : (int)((packed >> (3 * c)) & 7u);
+          }
+        tstar = max(tstar, (tv[NC - 1] << 10) | (unsigned)(1023 - j));
       }
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         cnt_c[c] += (c == best);
-        ivl[j * NC + c] = (c == best) ? 0xFFFF0000u : 0xFFFFFFFFu;
+        ivl[j * NC + c] = (IV)((c == best) ? (IM << IB) : ((IM << IB) | IM));
       }
     }
 #pragma unroll
@@ -971,7 +992,8 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       const int j = G[e].y & 1023, cf = (G[e].y >> 10) & 7, ct = (G[e].y >> 13) & 7;
       lbh[rk] = (int)(ke >> 10);
       cnts[rk + 1] = (1ull << (11 * ct)) - (1ull << (11 * cf));
-      lbw[rk + 1] = (long long)size_of<NC>(ct) * T[j * NC + ct] - (long long)size_of<NC>(cf) * T[j * NC + cf];
+      lbw[rk + 1] = (long long)((unsigned)size_of<NC>(ct) * (unsigned)T[j * NC + ct]) -
+                    (long long)((unsigned)size_of<NC>(cf) * (unsigned)T[j * NC + cf]);
       rnk[e] = rk;
     }
     __syncwarp();
@@ -980,8 +1002,8 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       const int y = G[e].y, j = y & 1023, cf = (y >> 10) & 7, ct = (y >> 13) & 7, pos = y >> 16;
       const int rk = rnk[e];
       const bool next = e + 1 < Gn && (G[e + 1].y & 1023) == j;
-      ivl[j * NC + ct] = (uint32_t)(rk + 1) | ((next ? (uint32_t)(rnk[e + 1] + 1) : 0xFFFFu) << 16);
-      if (pos == 0) ivl[j * NC + cf] = (uint32_t)(rk + 1) << 16;  // a^1 interval [0, rk + 1)
+      ivl[j * NC + ct] = (IV)((uint32_t)(rk + 1) | ((next ? (uint32_t)(rnk[e + 1] + 1) : IM) << IB));
+      if (pos == 0) ivl[j * NC + cf] = (IV)((uint32_t)(rk + 1) << IB);  // a^1 interval [0, rk + 1)
     }
     if (lane == 0) {
       lbh[Gn] = (int)(tstar >> 10);
@@ -1058,12 +1080,13 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       const unsigned nxp = (unsigned)su[jj] | ((unsigned)bestnode[jj] << 8);
       const int best = (int)((nxp >> (3 * cj)) & 7u);
       cp = cp - (1ull << (11 * cj)) + (1ull << (11 * best));
-      W += (long long)size_of<NC>(best) * T[jj * NC + best] - (long long)size_of<NC>(cj) * T[jj * NC + cj];
+      W += (long long)((unsigned)size_of<NC>(best) * (unsigned)T[jj * NC + best]) -
+           (long long)((unsigned)size_of<NC>(cj) * (unsigned)T[jj * NC + cj]);
       __syncwarp();
       if (lane == 0) {
         cur[jj] = (uint8_t)best;
-        ivl[jj * NC + cj] = (ivl[jj * NC + cj] & 0xFFFFu) | ((uint32_t)K << 16);  // leaves size cj at member K
-        ivl[jj * NC + best] = (uint32_t)K | 0xFFFF0000u;                          // enters size best at member K
+        ivl[jj * NC + cj] = (IV)((ivl[jj * NC + cj] & IM) | ((uint32_t)K << IB));  // leaves size cj at member K
+        ivl[jj * NC + best] = (IV)((uint32_t)K | (IM << IB));                     // enters size best at member K
         cnts[K] = cp;
         if (small && PIPE != PIPE_PREP) ck[jj] = ((unsigned)T[jj * NC + best] << 10) | (unsigned)(1023 - jj);
       }
@@ -1084,7 +1107,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     int acc = 0;
     for (int c = 0; c < NC; ++c) {
       int cnt = 0;
-      for (int j = lane; j < n; j += 32) cnt += ((ivl[j * NC + c] & 0xFFFFu) != 0xFFFFu);
+      for (int j = lane; j < n; j += 32) cnt += ((ivl[j * NC + c] & IM) != IM);
       cnt = __reduce_add_sync(FULL, cnt);
       if (lane == 0) loff[c] = acc;
       acc += cnt;
@@ -1096,15 +1119,15 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       int base = loff[c];
       for (int j0 = 0; j0 < n; j0 += 32) {
         const int j = j0 + lane;
-        uint32_t iv = 0xFFFFFFFFu;
+        uint32_t iv = (IM << IB) | IM;
         if (j < n) iv = ivl[j * NC + c];
-        const bool pres = (iv & 0xFFFFu) != 0xFFFFu;
+        const bool pres = (iv & IM) != IM;
         const unsigned bal = __ballot_sync(FULL, pres);
         if (pres) {
           const int pos = base + __popc(bal & ((1u << lane) - 1));
-          uint32_t hi = iv >> 16;
-          if (hi == 0xFFFFu) hi = (uint32_t)K;
-          lent[pos] = make_int2(T[j * NC + c], (int)((iv & 0xFFFFu) | (hi << 16)));
+          uint32_t hi = iv >> IB;
+          if (hi == IM) hi = (uint32_t)K;
+          lent[pos] = make_int2(T[j * NC + c], (int)((iv & IM) | (hi << 16)));
           ltask[pos] = (uint16_t)j;
         }
         base += __popc(bal);
@@ -1188,6 +1211,24 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     for (int k = lane; k < K; k += 32) {
       gl[k] = max(lbh[k], (int)((lbw[k] + S - 1) / S));  // max(h_k, ceil(W_k / #slices))
       gc[k] = cnts[k];
+    }
+    // member 0's entries (interval lo == 0: the a^1 sizes), compacted per size for K2
+    {
+      uint32_t* gm = P.ws_m0 + inst * (int64_t)P.ws_n4;
+      int base = 0;
+      for (int i0 = 0; i0 < E; i0 += 32) {
+        const int i = i0 + lane;
+        bool z = false;
+        uint32_t x = 0;
+        if (i < E) {
+          const int2 en = lent[i];
+          z = (en.y & 0xFFFF) == 0;
+          x = (uint32_t)en.x | ((uint32_t)ltask[i] << 22);
+        }
+        const unsigned bal = __ballot_sync(FULL, z);
+        if (z) gm[base + __popc(bal & ((1u << lane) - 1))] = x;
+        base += __popc(bal);
+      }
     }
     int* meta = P.ws_meta + inst * 16;
     if (lane <= NC) meta[lane] = loff[lane];

@@ -110,6 +110,79 @@ __device__ int sim_member(const int2* __restrict__ ent, const int* loff, unsigne
   return ms;
 }
 
+// Alg. 1 for member 0 from its compact per-size LPT lists: row = this thread's shared-memory
+// copy of the a^1 entries (t | task << 22), size c's list at offset sum_{c' < c} count_c'.
+// No other member's entries interleave, so every placement is one shared-memory load.
+template <int NC>
+__device__ int sim_member0(const uint32_t* row, unsigned long long cp, const uint32_t* ninfo, const int* cr,
+                           const int* de, uint32_t* st, uint16_t* npos, int bdim, uint32_t* rec, int* sl_out,
+                           int& pops) {
+  constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
+  int total = 0;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int r = (int)((cp >> (11 * c)) & 2047);
+    st[c * bdim] = ((uint32_t)r << 16) | (uint32_t)total;
+    total += r;
+  }
+  for (int v = 0; v < NN; ++v) npos[v * bdim] = 0;
+  Frontier<S> F;
+  F.init();
+  int rec_end = 0, ms = 0;
+  int sl[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) sl[s] = 0;
+  while (total > 0) {
+    int bs, be;
+    F.pop(bs, be);
+    const int v = F.node(bs);
+    const uint32_t w = ninfo[v];
+    int c = nd_c0(w);
+    uint32_t sv = st[c * bdim];
+    if (!(sv >> 16)) {
+      c = nd_c1(w);
+      sv = 0;
+      if (c != NONE) sv = st[c * bdim];
+    }
+    ++pops;
+    if (sv >> 16) {
+      if (!((F.has >> bs) & 1)) {
+        rec_end = max(rec_end, be) + cr[nd_szi(w)];
+        be = rec_end;
+        F.has |= 1u << bs;
+      }
+      const int p = (int)(sv & 0xFFFFu);
+      const uint32_t x = row[p];
+      const int task = (int)(x >> 22);
+      const int pos = npos[v * bdim];
+      npos[v * bdim] = (uint16_t)(pos + 1);
+      rec[task] = (uint32_t)v | ((uint32_t)c << 4) | ((uint32_t)pos << 7);
+      st[c * bdim] = sv - 0x10000u + 1u;
+      be += (int)(x & 0x3FFFFFu);
+      ms = max(ms, be);
+      --total;
+      F.set(bs, be);
+    } else {
+      if ((F.has >> bs) & 1) rec_end = max(rec_end, be) + de[nd_szi(w)];
+      if (!F.split(bs, be, w)) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) sl[s] = (s == bs) ? be : sl[s];
+      }
+    }
+  }
+  pops += __popc(F.live);
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+    if ((F.live >> s) & 1) {
+      const int sz = nd_sz(ninfo[F.node(s)]);
+#pragma unroll
+      for (int q = 0; q < S; ++q) sl[q] = (q >= s && q < s + sz) ? F.endv(s) : sl[q];
+    }
+#pragma unroll
+  for (int s = 0; s < S; ++s) sl_out[s] = sl[s];
+  return ms;
+}
+
 struct PParams {
   int64_t I;
   int n;
@@ -124,6 +197,8 @@ struct PParams {
   uint32_t* ws_rec;
   int* ws_sl;
   int ws_ecap1, ws_kcap;
+  const uint32_t* ws_m0;        // [I][n4] member 0's compact per-size LPT lists (t | task << 22)
+  int ws_n4;
   int2* items;                  // (instance, member) work items of K3
   unsigned long long* nitems;   // item counter
   unsigned long long* counter;  // K3 item scheduler
@@ -155,19 +230,22 @@ __global__ void __launch_bounds__(128) far_member0_kernel(PParams P) {
   const int bdim = blockDim.x, tid = threadIdx.x;
   uint32_t* st = (uint32_t*)dsm + tid;
   uint16_t* npos = (uint16_t*)(dsm + 4 * NC * bdim) + tid;
+  // this thread's copy of member 0's lists (row stride n4 + 4 words: 16 B aligned, banks shifted)
+  uint32_t* row = (uint32_t*)(dsm + (4 * NC + 2 * NN) * bdim) + (size_t)tid * (P.ws_n4 + 4);
   const bool exhaustive = (P.flags & FAR_EXHAUSTIVE) != 0;
   for (int64_t i = (int64_t)blockIdx.x * bdim + tid; i < P.I; i += (int64_t)gridDim.x * bdim) {
     const int* meta = P.ws_meta + i * 16;
     if (meta[WS_FLAG]) continue;
-    int loff[NC + 1];
-#pragma unroll
-    for (int c = 0; c <= NC; ++c) loff[c] = meta[c];
     const int K = meta[WS_K];
-    const int2* ent = P.ws_ent + i * (int64_t)P.ws_ecap1;
     const int* lb = P.ws_lb + i * (int64_t)P.ws_kcap;
+    {  // independent 16 B loads (many in flight), then every placement reads shared memory
+      const int4* src = (const int4*)(P.ws_m0 + i * (int64_t)P.ws_n4);
+      int4* dst = (int4*)row;
+      for (int q = 0; q < (P.ws_n4 >> 2); ++q) dst[q] = __ldcs(src + q);
+    }
     int pops = 0;
-    const int ms0 = sim_member<NC, true>(ent, loff, P.ws_cnt[i * (int64_t)P.ws_kcap], 0, sm.ninfo, sm.cr, sm.de, st,
-                                         npos, bdim, P.ws_rec + i * (int64_t)P.n, P.ws_sl + i * 8, pops);
+    const int ms0 = sim_member0<NC>(row, P.ws_cnt[i * (int64_t)P.ws_kcap], sm.ninfo, sm.cr, sm.de, st, npos, bdim,
+                                    P.ws_rec + i * (int64_t)P.n, P.ws_sl + i * 8, pops);
     const unsigned long long b0 = best_key(ms0, 0);
     P.ws_best[i] = b0;
     P.ws_evt[i] = (unsigned long long)pops;
