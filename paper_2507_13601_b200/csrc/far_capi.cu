@@ -12,6 +12,7 @@
 #include "far_kernel.cuh"
 #include "far_stream.cuh"
 #include "far_pipeline.cuh"
+#include "far_finish_lane.cuh"
 
 using namespace farb;
 
@@ -99,6 +100,8 @@ static far_status ensure_device(far_ctx* ctx) {
   CK(cudaFuncSetAttribute((const void*)far_member0_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   CK(cudaFuncSetAttribute((const void*)far_finish_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   CK(cudaFuncSetAttribute((const void*)far_finish_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
+  CK(cudaFuncSetAttribute((const void*)far_finish_lane_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
+  CK(cudaFuncSetAttribute((const void*)far_finish_lane_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   for (const void* f : fns) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   ctx->inited = true;
   return FAR_OK;
@@ -221,7 +224,9 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
   const bool a30 = ctx->nc == 3;
   const int NC = ctx->nc, NN = ctx->nn;
   const int kmax = 1 + P.n * (NC - 1);
-  int kfast = std::min(kmax, 64);  // M5: P(K > 64) ~ 0.4% -> those go to the overflow pass
+  int kcap_fast = 96;  // M5: P(K > 64) ~ 0.4%, P(K > 96) ~ 0: larger families go to the overflow pass
+  if (const char* e = getenv("FAR_DEBUG_KFAST")) kcap_fast = std::max(2, std::min(254, atoi(e)));  // experiments (8-bit intervals)
+  int kfast = std::min(kmax, kcap_fast);
   if (P.mode != MODE_SOLVE) kfast = 1;
   const bool pipe = P.mode == MODE_SOLVE && P.n > 0 && P.n <= 1023 && !getenv("FAR_FUSED_PHASE2");
   const bool need_ovf = P.mode == MODE_SOLVE && (kfast < kmax || pipe);
@@ -258,7 +263,8 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
                  o_rec = o_evt + a256(I * 8), o_sl = o_rec + a256(I * P.n * 4), o_items = o_sl + a256(I * 32),
                  o_m0 = o_items + a256(I * (size_t)(kfast - 1 > 0 ? kfast - 1 : 1) * 8);
     const int n4 = (P.n + 3) & ~3;
-    const size_t o_end = o_m0 + a256(I * (size_t)n4 * 4);
+    const size_t o_ncnt = o_m0 + a256(I * (size_t)n4 * 4);
+    const size_t o_end = o_ncnt + a256(I * 32);
     const int r = ctx->launch_id & 1;
     if ((st = grow(ctx, &ctx->d_pws[r], &ctx->d_pws_bytes[r], o_end))) return st;
     char* w = ctx->d_pws[r];
@@ -274,6 +280,7 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     P.ws_kcap = kfast;
     P.ws_m0 = (uint32_t*)(w + o_m0);
     P.ws_n4 = n4;
+    P.ws_ncnt = (uint16_t*)(w + o_ncnt);
     // ---- K1: H0-H3 per instance (warp)
     P.kcap = kfast;
     P.ovf_pass = 0;
@@ -293,7 +300,7 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     Q.ws_ent = P.ws_ent; Q.ws_lb = P.ws_lb; Q.ws_cnt = P.ws_cnt; Q.ws_meta = P.ws_meta;
     Q.ws_best = P.ws_best; Q.ws_evt = P.ws_evt; Q.ws_rec = P.ws_rec; Q.ws_sl = P.ws_sl;
     Q.ws_ecap1 = ecap1; Q.ws_kcap = kfast;
-    Q.ws_m0 = P.ws_m0; Q.ws_n4 = n4;
+    Q.ws_m0 = P.ws_m0; Q.ws_n4 = n4; Q.ws_ncnt = P.ws_ncnt;
     Q.items = (int2*)(w + o_items);
     Q.nitems = ctx->d_counter + slot + 3;
     Q.counter = ctx->d_counter + slot + 4;
@@ -324,9 +331,21 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     CK(cudaGetLastError());
     ctx->launches += 3;
     if ((st = t_mark(ctx, tset, stream, FAR_STAGE_WINNER))) return st;
-    // ---- K5: H6-H7 per instance (warp), compact layout
+    // ---- K5: H6-H7, one thread per instance (n <= 256), else one warp per instance
     P.counter = ctx->d_counter + slot + 5;
-    {
+    const LRow LR = make_lrow(P.n, NN);
+    const int tbl = (int)std::min<int64_t>(128, (int64_t)ctx->smem_max / LR.bytes / 32 * 32);
+    if (P.n <= 256 && tbl >= 32 && !getenv("FAR_DEBUG_WARP_FINISH")) {
+      const void* lfn = a30 ? (const void*)far_finish_lane_kernel<3> : (const void*)far_finish_lane_kernel<5>;
+      const size_t lsm = (size_t)tbl * LR.bytes;
+      int per_sm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lfn, tbl, lsm));
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((P.I + tbl - 1) / tbl, (int64_t)ctx->sms * std::max(1, per_sm)));
+      if (a30) far_finish_lane_kernel<3><<<grid, tbl, lsm, stream>>>(P);
+      else far_finish_lane_kernel<5><<<grid, tbl, lsm, stream>>>(P);
+      CK(cudaGetLastError());
+      ++ctx->launches;
+    } else {
       const FLayout FL = make_flayout(P.n, NN);
       const int fw = 4;
       int per_sm = 0;

@@ -1,0 +1,344 @@
+// far_finish_lane.cuh — H6/H7 (Alg. 2, line-26 replay P:557, keep-best guard P:812)
+// with ONE THREAD PER INSTANCE, for the pipelined solver (far_pipeline.cuh K5).
+//
+// Phase 3 on a realistic instance touches node lists of ~10-20 tasks: a warp spends most of
+// its issue slots on reductions, ballots and list shifts whose lanes are mostly idle.  Here
+// each thread runs Alg. 2 and the replay of its own instance sequentially, so a warp issues
+// one instruction for 32 instances.  The readings, tie-breaks and counters are those of
+// refine_warp / replay_warp (far_kernel.cuh); the two paths are bit-identical by construction
+// and both are checked against the oracle (tests/test_gpu_parity.py).
+//
+// Per-thread state in shared memory (one row per thread):
+//   ent[n]   u32  the node lists, concatenated in node-id order; entry = D << 10 | (1023 - task)
+//                 (D = duration at the task's size, < 2^22 on this path), so "ordered by
+//                 T.time, ties -> lower index" is the descending order of entries
+//   off[NN+1] u16 segment offsets of the node lists inside ent
+//   alt[n/32] u32 bit per task: the task runs at the second size its node hosts (A100 {S0..S3}
+//                 running a 3-slice task); such tasks never change node (no other 4-slice node)
+// Slice ends live in registers (7 slots, compile-time indexed).
+#pragma once
+#include "far_pipeline.cuh"
+
+namespace farb {
+
+struct LRow {
+  int ent, off, alt, bytes;  // byte offsets inside one thread's row
+};
+__host__ __device__ inline LRow make_lrow(int n, int NN) {
+  LRow r;
+  int o = 0;
+  r.ent = o; o += 4 * ((n + 3) & ~3);
+  r.alt = o; o += 4 * ((n + 31) / 32);
+  r.off = o; o += 2 * (NN + 1);
+  o = (o + 15) & ~15;
+  r.bytes = o + 16;  // +16 B: consecutive rows start in different banks
+  return r;
+}
+
+template <int NC>
+__device__ __forceinline__ uint32_t cnode(int u) {
+  return NC == 3 ? c_nodes3[u] : c_nodes5[u];
+}
+
+// max over the slices of node w of the slice ends
+template <int S>
+__device__ __forceinline__ int lane_end(uint32_t w, const int (&send)[S]) {
+  const int lo = nd_lo(w), hi = lo + nd_sz(w);
+  int e = 0;
+#pragma unroll
+  for (int s = 0; s < S; ++s) e = (s >= lo && s < hi) ? max(e, send[s]) : e;
+  return e;
+}
+
+// Move the entry x from node `from` to node `to` at its ordered position.
+template <int NN>
+__device__ __forceinline__ void lane_transfer(uint32_t* ent, uint16_t* off, int from, int to, uint32_t x) {
+  // index of x in from's segment
+  int g = off[from];
+  while (ent[g] != x) ++g;
+  // position in to's segment: entries ordered before x
+  int p = 0;
+  const int b = off[to], e = off[to + 1];
+  for (int q = b; q < e; ++q) p += ent[q] > x;
+  if (to > from) {  // segments (from, to] move left by one
+    const int tgt = e - 1 - (e - b - p);  // = off[to] - 1 + p
+    for (int q = g; q < tgt; ++q) ent[q] = ent[q + 1];
+    ent[tgt] = x;
+    for (int v = from + 1; v <= to; ++v) off[v] = (uint16_t)(off[v] - 1);
+  } else {  // segments (to, from] move right by one
+    const int tgt = b + p;
+    for (int q = g; q > tgt; --q) ent[q] = ent[q - 1];
+    ent[tgt] = x;
+    for (int v = to + 1; v <= from; ++v) off[v] = (uint16_t)(off[v] + 1);
+  }
+}
+
+// Alg. 2 on one thread; same readings as refine_warp.
+template <int NC>
+__device__ void refine_lane(uint32_t* ent, uint16_t* off, int (&send)[Tree<NC>::S], int max_it, int ppm, int& moves,
+                            int& swaps, int& iters, long long& evals) {
+  constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
+  int omega = 0;
+#pragma unroll
+  for (int s = 0; s < S; ++s) omega = max(omega, send[s]);
+  moves = swaps = iters = 0;
+  evals = 0;
+  bool stop = false;
+  while (!stop && iters < max_it) {
+    ++iters;
+    const int omega_prev = omega;
+    unsigned long long Q = 0;  // FIFO of node ids, 4 bits each
+    int qh = 0, qt = 0;
+    uint32_t opened = 0;
+    // line 5: leaves of the slices reaching omega, ascending slice order
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+      if (send[s] == omega) {
+        const int leaf = leaf_of<NC>(s);
+        Q |= (unsigned long long)leaf << (4 * qt++);
+        opened |= 1u << leaf;
+      }
+    while (qh < qt) {
+      const int I = (int)((Q >> (4 * qh++)) & 15);
+      if (I == 0) { stop = true; break; }
+      const uint32_t wI = cnode<NC>(I);
+      // alternative I^a: same size, != I, minimum (end, first slice)
+      int A = -1, eA = INT_MAX, loA = 15;
+#pragma unroll
+      for (int u = 0; u < NN; ++u) {
+        const uint32_t wu = cnode<NC>(u);
+        if (u != I && nd_sz(wu) == nd_sz(wI)) {  // argmin (end, first slice)
+          const int eu = lane_end<S>(wu, send);
+          if (eu < eA || (eu == eA && nd_lo(wu) < loA)) { eA = eu; A = u; loA = nd_lo(wu); }
+        }
+      }
+      bool done = false;
+      if (A >= 0) {
+        const int m = omega - eA;
+        const int bI = off[I], nI = off[I + 1] - bI;
+        evals += nI;
+        // move: argmin (|2t - m|, index) over t < m
+        unsigned bd = UINT_MAX;
+        int bj = INT_MAX;
+        uint32_t bx = 0;
+        for (int q = bI; q < bI + nI; ++q) {
+          const uint32_t x = ent[q];
+          const int t = (int)(x >> 10), j = 1023 - (int)(x & 1023u);
+          if (t < m) {
+            const unsigned d = (unsigned)abs(2 * t - m);
+            if (d < bd || (d == bd && j < bj)) { bd = d; bj = j; bx = x; }
+          }
+        }
+        if (bd != UINT_MAX) {
+          lane_transfer<NN>(ent, off, I, A, bx);
+          const int delta = (int)(bx >> 10);
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            if (s >= nd_lo(wI) && s < nd_lo(wI) + nd_sz(wI)) send[s] -= delta;
+          }
+          const uint32_t wA = cnode<NC>(A);
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            if (s >= nd_lo(wA) && s < nd_lo(wA) + nd_sz(wA)) send[s] += delta;
+          }
+          ++moves;
+          done = true;
+        } else {
+          const int bA = off[A], nA = off[A + 1] - bA;
+          evals += (long long)nI * nA;
+          // argmin over pairs of (|2(t_k - t_j) - m|, k, j), 0 < t_k - t_j < m.  Both lists are
+          // ordered by (t desc, task asc) (single-size nodes: LPT order of Alg. 1, kept by the
+          // ordered inserts; the two-size {S0..S3} node has no same-size alternative), so for
+          // t_k descending the best partners -- the first entry with 2 t_j <= 2 t_k - m and the
+          // first entry of the block of equal t just above it -- move monotonically: a
+          // two-pointer sweep instead of the |I| * |A| scan (same argmin, same tie-breaks).
+          unsigned bd2 = UINT_MAX, bkey = UINT_MAX;
+          uint32_t xk = 0, xj = 0;
+          int r = bA, bst = bA;  // r: first entry with 2t <= T; bst: start of the equal-t block before r
+          const int eAo = bA + nA;
+          for (int q = bI; q < bI + nI && m > 0; ++q) {
+            const uint32_t a = ent[q];
+            const int tk = (int)(a >> 10), k = 1023 - (int)(a & 1023u);
+            const int T = 2 * tk - m;
+            while (r < eAo && 2 * (int)(ent[r] >> 10) > T) {
+              if (r == bA || (ent[r] >> 10) != (ent[r - 1] >> 10)) bst = r;
+              ++r;
+            }
+            // below (or equal): entry r (first of its equal-t block); needs t_j > t_k - m
+            if (r < eAo) {
+              const uint32_t b = ent[r];
+              const int dl = tk - (int)(b >> 10);
+              if (dl < m) {  // dl > 0 since 2 t_j <= 2 t_k - m < 2 t_k
+                const unsigned d = (unsigned)abs(2 * dl - m);
+                const unsigned key = ((unsigned)k << 10) | (unsigned)(1023 - (int)(b & 1023u));
+                if (d < bd2 || (d == bd2 && key < bkey)) { bd2 = d; bkey = key; xk = a; xj = b; }
+              }
+            }
+            // above: first entry of the block before r; needs t_j < t_k
+            if (r > bA) {
+              const uint32_t b = ent[bst];
+              const int dl = tk - (int)(b >> 10);
+              if (dl > 0) {  // dl < m since 2 t_j > 2 t_k - m
+                const unsigned d = (unsigned)abs(2 * dl - m);
+                const unsigned key = ((unsigned)k << 10) | (unsigned)(1023 - (int)(b & 1023u));
+                if (d < bd2 || (d == bd2 && key < bkey)) { bd2 = d; bkey = key; xk = a; xj = b; }
+              }
+            }
+          }
+          if (bd2 != UINT_MAX) {  // K: I -> A, then J: A -> I (same final lists as the warp path)
+            lane_transfer<NN>(ent, off, I, A, xk);
+            lane_transfer<NN>(ent, off, A, I, xj);
+            const int delta = (int)(xk >> 10) - (int)(xj >> 10);
+            const uint32_t wA = cnode<NC>(A);
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+              if (s >= nd_lo(wI) && s < nd_lo(wI) + nd_sz(wI)) send[s] -= delta;
+              if (s >= nd_lo(wA) && s < nd_lo(wA) + nd_sz(wA)) send[s] += delta;
+            }
+            ++swaps;
+            done = true;
+          }
+        }
+      }
+      if (!done) {
+        const int par = nd_par(wI);
+        if (par != ROOTP && !((opened >> par) & 1)) {
+          opened |= 1u << par;
+          Q |= (unsigned long long)par << (4 * qt++);
+        }
+      }
+    }
+    omega = 0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) omega = max(omega, send[s]);
+    if (ppm > 0 && (long long)(omega_prev - omega) * 1000000LL < (long long)ppm * omega_prev) break;
+  }
+}
+
+// Node lists of k* from the phase-2 record (node | size index << 4 | position << 7 per task,
+// node list lengths in ncnt); fills ent/off/alt.
+template <int NC>
+__device__ void lane_lists(int n, const uint32_t* __restrict__ rec, const uint16_t* __restrict__ ncnt,
+                           const int32_t* __restrict__ t, uint32_t* ent, uint16_t* off, uint32_t* alt) {
+  constexpr int NN = Tree<NC>::NN;
+  for (int w = 0; w < (n + 31) / 32; ++w) alt[w] = 0;
+  int acc = 0;
+#pragma unroll
+  for (int v = 0; v < NN; ++v) {
+    off[v] = (uint16_t)acc;
+    acc += __ldg(ncnt + v);
+  }
+  off[NN] = (uint16_t)acc;
+#pragma unroll 4
+  for (int j = 0; j < n; ++j) {
+    const uint32_t r = __ldg(rec + j);
+    const int v = (int)(r & 15u), c = (int)((r >> 4) & 7u), pos = (int)(r >> 7);
+    const int d = __ldg(t + j * NC + c);
+    ent[off[v] + pos] = ((uint32_t)d << 10) | (uint32_t)(1023 - j);
+    if (c != nd_c0(cnode<NC>(v))) alt[j >> 5] |= 1u << (j & 31);
+  }
+}
+
+// Node-level replay (the frontier in registers of this thread); writes the schedule when
+// `out` is not null; returns the makespan.
+template <int NC>
+__device__ int lane_replay(const uint32_t* ent, const uint16_t* off, const uint32_t* alt, const int* cr,
+                           const int* de, far_task_slot* out) {
+  constexpr int S = Tree<NC>::S;
+  Frontier<S> F;
+  F.init();
+  int rec = 0, ms = 0;
+  while (F.live) {
+    int bs, be;
+    F.pop(bs, be);
+    const int v = F.node(bs);
+    const uint32_t w = cnode<NC>(v);
+    const int b = off[v], e = off[v + 1];
+    if (!((F.has >> bs) & 1) && e > b) {  // creation (lines 8-11), then all of v's tasks
+      rec = max(rec, be) + cr[nd_szi(w)];
+      int acc = rec;
+      for (int q = b; q < e; ++q) {
+        const uint32_t x = ent[q];
+        if (out) {
+          const int j = 1023 - (int)(x & 1023u);
+          const int c = ((alt[j >> 5] >> (j & 31)) & 1) ? nd_c1(w) : nd_c0(w);
+          const unsigned long long s = (unsigned long long)(unsigned)v |
+                                       ((unsigned long long)(unsigned)size_of<NC>(c) << 8) |
+                                       ((unsigned long long)(unsigned)acc << 32);
+          *(unsigned long long*)(out + j) = s;
+        }
+        acc += (int)(x >> 10);
+      }
+      ms = max(ms, acc);
+      F.has |= 1u << bs;
+      F.set(bs, acc);
+    } else {  // repartitioning (lines 17-24): destroy if it had tasks, then split or drop
+      if ((F.has >> bs) & 1) rec = max(rec, be) + de[nd_szi(w)];
+      F.split(bs, be, w);
+    }
+  }
+  return ms;
+}
+
+template <int NC>
+__global__ void __launch_bounds__(128) far_finish_lane_kernel(KParams P) {
+  constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ int s_cr[8], s_de[8];
+  if (threadIdx.x < 8) {
+    s_cr[threadIdx.x] = P.cr[threadIdx.x];
+    s_de[threadIdx.x] = P.de[threadIdx.x];
+  }
+  __syncthreads();
+  const int n = P.n;
+  const LRow L = make_lrow(n, NN);
+  unsigned char* row = dsm + (size_t)threadIdx.x * L.bytes;
+  uint32_t* ent = (uint32_t*)(row + L.ent);
+  uint16_t* off = (uint16_t*)(row + L.off);
+  uint32_t* alt = (uint32_t*)(row + L.alt);
+  const bool want_sched = P.sched != nullptr && !(P.flags & FAR_NO_SCHEDULE);
+  const bool refine = !(P.flags & FAR_NO_REFINE);
+  const bool need_replay = refine || want_sched;
+  for (int64_t inst = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; inst < P.I;
+       inst += (int64_t)gridDim.x * blockDim.x) {
+    const int* meta = P.ws_meta + inst * 16;
+    if (meta[WS_FLAG]) continue;  // error / empty (K1 wrote the outputs) / deferred to the overflow pass
+    const unsigned long long best = P.ws_best[inst];
+    const int ms2 = (int)(best >> 16), bestk = (int)(best & 0xFFFFu);
+    far_result R;
+    R.makespan = 0; R.makespan_phase2 = ms2; R.alloc_index = bestk; R.family_size = meta[WS_K];
+    R.moves = 0; R.swaps = 0; R.iterations = 0; R.reverted = 0; R.status = FAR_OK; R.reserved = 0;
+    R.evals = 0; R.events = (long long)P.ws_evt[inst];
+    const uint32_t* rec = P.ws_rec + inst * (int64_t)n;
+    const int32_t* t = P.times + inst * (int64_t)n * NC;
+    far_task_slot* out = want_sched ? P.sched + inst * (int64_t)n : nullptr;
+    int msF = ms2;
+    for (int pass = 0; pass < 2; ++pass) {
+      lane_lists<NC>(n, rec, P.ws_ncnt + inst * 16, t, ent, off, alt);
+      const bool ref = refine && pass == 0;
+      if (ref) {
+        int send[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) send[s] = P.ws_sl[inst * 8 + s];
+        int mv, sw, it;
+        long long ev;
+        refine_lane<NC>(ent, off, send, P.max_it, P.ppm, mv, sw, it, ev);
+        R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
+      }
+      if (!need_replay) break;
+      const int msR = lane_replay<NC>(ent, off, alt, s_cr, s_de, out);
+      if (ref && !(P.flags & FAR_NO_GUARD) && msR > ms2) {
+        R.reverted = 1;  // keep-best guard: return the phase-2 schedule (replayed in pass 1)
+        if (!want_sched) break;
+        continue;
+      }
+      if (ref) msF = msR;
+      break;
+    }
+    R.makespan = msF;
+    P.makespan[inst] = R.makespan;
+    if (P.res) P.res[inst] = R;
+  }
+}
+
+}  // namespace farb

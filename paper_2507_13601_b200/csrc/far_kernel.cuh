@@ -61,6 +61,7 @@ struct KParams {
   int* ws_sl;                   // [I][8]        k*'s slice ends
   int ws_ecap1, ws_kcap;
   int rsum;                     // sum over tree nodes of create + destroy cost (integer-range check)
+  uint16_t* ws_ncnt;            // [I][16]       k*'s node list lengths (lane-per-instance finish)
   uint32_t* ws_m0;              // [I][ws_n4]    member 0's compact per-size LPT lists (t | task << 22)
   int ws_n4;
 };
@@ -936,11 +937,12 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   // takes the largest current key, and a chain's later keys are never larger.  It stops at
   // the first terminal element (max size) on top, i.e. at T* = the largest terminal key, so
   // the growth steps are exactly the non-terminal chain elements with key >= T*, in that order.
-  mono = __all_sync(FULL, mono && small && P.kcap <= 64);  // (fast layout: <= 63 steps)
+  // (growth-step ranks live in lstate: PIPE_PREP sizes it by kcap, the fused layout holds 160)
+  mono = __all_sync(FULL, mono && small && (PIPE == PIPE_PREP || P.kcap <= 160));
   tstar = __reduce_max_sync(FULL, tstar);
   if (mono) {
     int2* G = lent;  // temporary (filled in H3): {key, task | from << 10 | to << 13 | pos << 16}
-    int* rnk = (int*)lstate;  // step rank per element (lstate is free until H4; <= 63 steps)
+    int* rnk = (int*)lstate;  // step rank per element (lstate is free until H4)
     int cntl = 0;
     for (int j = lane; j < n; j += 32) {
       const unsigned nxp = (unsigned)su[j] | ((unsigned)bestnode[j] << 8);

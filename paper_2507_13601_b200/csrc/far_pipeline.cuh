@@ -199,6 +199,7 @@ struct PParams {
   int ws_ecap1, ws_kcap;
   const uint32_t* ws_m0;        // [I][n4] member 0's compact per-size LPT lists (t | task << 22)
   int ws_n4;
+  uint16_t* ws_ncnt;            // [I][16] node list lengths of the recorded member
   int2* items;                  // (instance, member) work items of K3
   unsigned long long* nitems;   // item counter
   unsigned long long* counter;  // K3 item scheduler
@@ -246,6 +247,7 @@ __global__ void __launch_bounds__(128) far_member0_kernel(PParams P) {
     int pops = 0;
     const int ms0 = sim_member0<NC>(row, P.ws_cnt[i * (int64_t)P.ws_kcap], sm.ninfo, sm.cr, sm.de, st, npos, bdim,
                                     P.ws_rec + i * (int64_t)P.n, P.ws_sl + i * 8, pops);
+    for (int v = 0; v < NN; ++v) P.ws_ncnt[i * 16 + v] = npos[v * bdim];
     const unsigned long long b0 = best_key(ms0, 0);
     P.ws_best[i] = b0;
     P.ws_evt[i] = (unsigned long long)pops;
@@ -294,6 +296,7 @@ __global__ void __launch_bounds__(128) far_members_kernel(PParams P) {
 // K4: re-run the winner when it is not member 0, recording its placements.
 template <int NC>
 __global__ void __launch_bounds__(128) far_winner_kernel(PParams P) {
+  constexpr int NN = Tree<NC>::NN;
   __shared__ PipeSmem<NC> sm;
   extern __shared__ __align__(16) unsigned char dsm[];
   pipe_prologue<NC>(P, sm);
@@ -311,6 +314,7 @@ __global__ void __launch_bounds__(128) far_winner_kernel(PParams P) {
     int pops = 0;
     sim_member<NC, true>(P.ws_ent + i * (int64_t)P.ws_ecap1, loff, P.ws_cnt[i * (int64_t)P.ws_kcap + k], k,
                          sm.ninfo, sm.cr, sm.de, st, npos, bdim, P.ws_rec + i * (int64_t)P.n, P.ws_sl + i * 8, pops);
+    for (int v = 0; v < NN; ++v) P.ws_ncnt[i * 16 + v] = npos[v * bdim];
   }
 }
 
