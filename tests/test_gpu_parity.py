@@ -100,15 +100,38 @@ def test_options(O, torch_dev, flags, max_it, ppm):
     check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=flags, max_iterations=max_it, ppm=ppm)
 
 
-@pytest.mark.parametrize("n", [128, 256, 1024])
+@pytest.mark.parametrize("n", [128, 256, 257, 600, 1023, 1024])
 def test_large_n(O, torch_dev, n):
     profile = "A100"
     costs = inputs.reconfig_costs(profile)
-    tab = inputs.synthetic(profile, n, 24 if n < 1024 else 3, 31, times="narrow" if n == 1024 else "wide")
-    if n == 1024:
+    big = n > 512
+    tab = inputs.synthetic(profile, n, 24 if not big else 3, 31, times="narrow" if big else "wide")
+    if big:
         tab = np.minimum(tab, 900)  # keep the makespan bound < 2^29
     ms, slots, res = run_gpu(torch_dev, profile, costs, tab)
     check_against_oracle(O, profile, costs, tab, ms, slots, res)
+
+
+# The pipelined solver has three H6/H7 implementations: one thread per instance (n <= 256),
+# one warp per instance (the debug switch below, and 256 < n <= 1023), and the fused kernel
+# (FAR_FUSED_PHASE2; also the overflow pass and n = 1024).  All must agree with the oracle.
+@pytest.mark.parametrize("switch", [None, "FAR_DEBUG_WARP_FINISH", "FAR_FUSED_PHASE2"])
+@pytest.mark.parametrize("wname,gen", [("M5", "wide"), ("M3", "wide"), ("A30", "ties"), ("A100", "monoties")])
+def test_finish_paths_agree(O, torch_dev, monkeypatch, switch, wname, gen):
+    if switch:
+        monkeypatch.setenv(switch, "1")
+    if wname in ("M5", "M3"):
+        w = inputs.WORKLOADS[wname]
+        profile, costs, tab = w.profile, w.costs(), w.table(count=200)
+    elif gen == "ties":
+        profile = wname
+        costs, tab = inputs.reconfig_costs(profile), inputs.small_ties(profile, 40, 200, 8)
+    else:
+        profile = wname
+        costs, tab = inputs.reconfig_costs(profile), inputs.monotone_ties(profile, 40, 200, 9)
+    for flags in (0, far.NO_GUARD):
+        ms, slots, res = run_gpu(torch_dev, profile, costs, tab, flags=flags)
+        check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=flags)
 
 
 def test_input_errors_flagged(torch_dev):
