@@ -666,7 +666,8 @@ __device__ __noinline__ void solve_local(const KParams& P, int64_t inst, unsigne
 
 // Node lists of k* from the pipelined phase-2 record (node, size index, position per task).
 template <int NC>
-__device__ void lists_from_record(int n, const uint32_t* rec, uint16_t* nlist, int* ncnt, uint8_t* su, int lane) {
+__device__ void lists_from_record(int n, const uint32_t* rec, const int32_t* t, uint16_t* nlist, int* ncnt,
+                                  uint8_t* su, int* D, int lane) {
   constexpr int NN = Tree<NC>::NN;
   if (lane < NN) ncnt[lane] = 0;
   __syncwarp();
@@ -675,6 +676,7 @@ __device__ void lists_from_record(int n, const uint32_t* rec, uint16_t* nlist, i
     const int v = (int)(r & 15u);
     nlist[v * n + (int)(r >> 7)] = (uint16_t)j;
     su[j] = (uint8_t)((r >> 4) & 7u);
+    D[j] = __ldg(t + j * NC + su[j]);
     atomicAdd(&ncnt[v], 1);
   }
   __syncwarp();
@@ -702,9 +704,8 @@ __device__ void finish_core(const KParams& P, int64_t inst, uint16_t* nlist, int
   const bool need_replay = refine || want_sched;
   for (int pass = 0; pass < 2; ++pass) {
     if (FROM_REC) {
-      lists_from_record<NC>(n, P.ws_rec + inst * (int64_t)n, nlist, ncnt, su, lane);
-      const int32_t* gt = P.times + inst * (int64_t)n * NC;
-      for (int j = lane; j < n; j += 32) D[j] = __ldg(gt + j * NC + su[j]);
+      lists_from_record<NC>(n, P.ws_rec + inst * (int64_t)n, P.times + inst * (int64_t)n * NC, nlist, ncnt, su, D,
+                            lane);
     } else {
       build_node_lists<NC>(n, bestk, lent, ltask, loff, bestnode, nlist, ncnt, su, lane);
       for (int j = lane; j < n; j += 32) D[j] = T[j * NC + su[j]];

@@ -298,16 +298,18 @@ template <int NC>
 __global__ void __launch_bounds__(128) far_winner_kernel(PParams P) {
   constexpr int NN = Tree<NC>::NN;
   __shared__ PipeSmem<NC> sm;
+  __shared__ int64_t queue[4][64];  // per warp: instances whose winner is not member 0
   extern __shared__ __align__(16) unsigned char dsm[];
   pipe_prologue<NC>(P, sm);
-  const int bdim = blockDim.x, tid = threadIdx.x;
+  const int bdim = blockDim.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint32_t* st = (uint32_t*)dsm + tid;
   uint16_t* npos = (uint16_t*)(dsm + 4 * NC * bdim) + tid;
-  for (int64_t i = (int64_t)blockIdx.x * bdim + tid; i < P.I; i += (int64_t)gridDim.x * bdim) {
+  int64_t* q = queue[warp];
+  // ~10 % of the instances have k* != 0: each warp scans 32 instances at a time and compacts
+  // them into its queue, so that the re-simulations run with every lane busy
+  auto resim = [&](int64_t i) {
     const int* meta = P.ws_meta + i * 16;
-    if (meta[WS_FLAG]) continue;
     const int k = (int)(P.ws_best[i] & 0xFFFFu);
-    if (k == 0) continue;
     int loff[NC + 1];
 #pragma unroll
     for (int c = 0; c <= NC; ++c) loff[c] = meta[c];
@@ -315,7 +317,27 @@ __global__ void __launch_bounds__(128) far_winner_kernel(PParams P) {
     sim_member<NC, true>(P.ws_ent + i * (int64_t)P.ws_ecap1, loff, P.ws_cnt[i * (int64_t)P.ws_kcap + k], k,
                          sm.ninfo, sm.cr, sm.de, st, npos, bdim, P.ws_rec + i * (int64_t)P.n, P.ws_sl + i * 8, pops);
     for (int v = 0; v < NN; ++v) P.ws_ncnt[i * 16 + v] = npos[v * bdim];
+  };
+  int count = 0;
+  const int64_t nwarps = (int64_t)gridDim.x * (bdim >> 5);
+  for (int64_t base = ((int64_t)blockIdx.x * (bdim >> 5) + warp) * 32; base < P.I; base += nwarps * 32) {
+    const int64_t i = base + lane;
+    bool need = false;
+    if (i < P.I && !P.ws_meta[i * 16 + WS_FLAG]) need = (P.ws_best[i] & 0xFFFFu) != 0;
+    const unsigned bal = __ballot_sync(FULL, need);
+    if (need) q[count + __popc(bal & ((1u << lane) - 1))] = i;
+    count += __popc(bal);
+    __syncwarp();
+    if (count >= 32) {
+      resim(q[lane]);
+      const int64_t rest = lane + 32 < count ? q[lane + 32] : 0;
+      __syncwarp();
+      if (lane + 32 < count) q[lane] = rest;
+      count -= 32;
+      __syncwarp();
+    }
   }
+  if (lane < count) resim(q[lane]);
 }
 
 // ---------------------------------------------------------------------------
