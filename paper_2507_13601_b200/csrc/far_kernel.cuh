@@ -75,7 +75,7 @@ enum { M_LOFF = 0, M_NINFO = 8, M_CR = 24, M_DE = 32, M_PREP_END = 40, M_NCNT = 
 // Per-warp shared-memory layout (bytes), identical on host and device.  kcap bounds the
 // family size K this layout holds (the per-size lists hold at most n + K - 1 entries).
 struct Layout {
-  int times, lent, ltask, cnts, lbw, lbh, cur, su, bestnode, scratch, lstate, start, misc, bytes, ecap, scr;
+  int times, lent, ltask, cnts, lbs, lbh, cur, su, bestnode, scratch, lstate, start, misc, bytes, ecap, scr;
 };
 
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
@@ -92,7 +92,7 @@ __host__ __device__ inline Layout make_layout(int n, int NC, int S, int NN, int 
   L.lent = o;     o = al16(o + 8 * (Ecap + 1));
   L.ltask = o;    o = al16(o + 2 * (Ecap + 1));
   L.cnts = o;     o = al16(o + 8 * kcap);
-  L.lbw = o;      o = al16(o + 8 * kcap);
+  L.lbs = o;      o = al16(o + 4 * kcap);
   L.lbh = o;      o = al16(o + 4 * kcap);
   L.cur = o;      o = al16(o + n);
   L.su = o;       o = al16(o + n);
@@ -774,8 +774,10 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   int2* lent = (int2*)(wsm + L.lent);
   uint16_t* ltask = (uint16_t*)(wsm + L.ltask);
   unsigned long long* cnts = (unsigned long long*)(wsm + L.cnts);
-  long long* lbw = (long long*)(wsm + L.lbw);  // area of each member
-  int* lbh = (int*)(wsm + L.lbh);              // longest task of each member
+  // lower bound of each member's Alg. 1 makespan: its longest task h_k (lbh) and its area
+  // spread over all slices, ceil(W_k / #slices) (lbs) -- reconfiguration only adds idle time
+  int* lbs = (int*)(wsm + L.lbs);
+  int* lbh = (int*)(wsm + L.lbh);
   uint8_t* cur = wsm + L.cur;
   uint8_t* su = wsm + L.su;
   uint8_t* bestnode = wsm + L.bestnode;
@@ -860,7 +862,8 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   constexpr uint32_t IM = (1u << IB) - 1u;
   IV* ivl = (IV*)scratch;
   unsigned long long c0pack = 0;
-  long long W = 0;  // total area sum_i a_i t_i(a_i) of the current member (uniform)
+  // total area sum_i a_i t_i(a_i) of the current member (uniform); < 7 * 2^29 by the range check
+  unsigned W = 0;
   bool mono = true;
   unsigned tstar = 0;
   {
@@ -915,7 +918,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c) c0pack |= (unsigned long long)__reduce_add_sync(FULL, cnt_c[c]) << (11 * c);
-    W = warp_sum_ll(W);
+    W = __reduce_add_sync(FULL, W);
   }
   if (lane == 0) cnts[0] = c0pack;
   __syncwarp();
@@ -932,6 +935,9 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     return;
   }
   int K = 1;
+  // list entries per size (11-bit fields): member 0's sizes + one entry per growth step at the
+  // size it enters (a task enters each size at most once, so a field stays <= n)
+  unsigned long long entp = c0pack;
   // Parallel form for monotone chains (every task's t non-increasing along its growth chain;
   // property 1 of P:260-263 implies it).  With key(t, j) = t << 10 | (1023 - j) the growth
   // process is the merge of the per-task chains by (key desc, chain position asc): each step
@@ -968,6 +974,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       }
       return;
     }
+    unsigned long long myent = 0;
     for (int j = lane; j < n; j += 32) {
       const unsigned nxp = (unsigned)su[j] | ((unsigned)bestnode[j] << 8);
       int pos = 0;
@@ -976,9 +983,11 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         if (key < tstar) break;
         const int c2 = (int)((nxp >> (3 * c)) & 7u);
         G[excl++] = make_int2((int)key, j | (c << 10) | (c2 << 13) | (pos << 16));
+        myent += 1ull << (11 * c2);
         c = c2;
       }
     }
+    entp += (unsigned long long)warp_sum_ll((long long)myent);
     __syncwarp();
     // rank of each step: larger keys first; equal keys (same task) in chain order
     // (64-bit compare of (key, 63 - pos): count the elements <= own, rank = Gn - that)
@@ -995,8 +1004,9 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       const int j = G[e].y & 1023, cf = (G[e].y >> 10) & 7, ct = (G[e].y >> 13) & 7;
       lbh[rk] = (int)(ke >> 10);
       cnts[rk + 1] = (1ull << (11 * ct)) - (1ull << (11 * cf));
-      lbw[rk + 1] = (long long)((unsigned)size_of<NC>(ct) * (unsigned)T[j * NC + ct]) -
-                    (long long)((unsigned)size_of<NC>(cf) * (unsigned)T[j * NC + cf]);
+      // area delta (>= 0: work is non-decreasing along a growth chain, nx(c) minimises over c' > c)
+      lbs[rk + 1] = (int)((unsigned)size_of<NC>(ct) * (unsigned)T[j * NC + ct] -
+                          (unsigned)size_of<NC>(cf) * (unsigned)T[j * NC + cf]);
       rnk[e] = rk;
     }
     __syncwarp();
@@ -1011,25 +1021,25 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     if (lane == 0) {
       lbh[Gn] = (int)(tstar >> 10);
       cnts[0] = c0pack;
-      lbw[0] = W;
+      lbs[0] = (int)W;
     }
     __syncwarp();
-    // prefix sums over members of the packed size counts and of the area
+    // prefix sums over members of the packed size counts and of the area (W_k < 2^32 unsigned)
     unsigned long long cc = 0;
-    long long ww = 0;
+    unsigned ww = 0;
     for (int k0 = 0; k0 <= Gn; k0 += 32) {
       const int k = k0 + lane;
       unsigned long long dc = k <= Gn ? cnts[k] : 0;
-      long long dw = k <= Gn ? lbw[k] : 0;
+      unsigned dw = k <= Gn ? (unsigned)lbs[k] : 0u;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const unsigned long long yc = __shfl_up_sync(FULL, dc, o);
-        const long long yw = __shfl_up_sync(FULL, dw, o);
+        const unsigned yw = __shfl_up_sync(FULL, dw, o);
         if (lane >= o) { dc += yc; dw += yw; }
       }
       if (k <= Gn) {
         cnts[k] = cc + dc;
-        lbw[k] = ww + dw;
+        lbs[k] = (int)((ww + dw + (unsigned)(S - 1)) / (unsigned)S);  // ceil(W_k / #slices)
       }
       cc += __shfl_sync(FULL, dc, 31);
       ww += __shfl_sync(FULL, dw, 31);
@@ -1068,7 +1078,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       // over all slices (reconfiguration only adds idle time) -- used to prune phase 2
       if (lane == 0) {
         lbh[K - 1] = hmax;
-        lbw[K - 1] = W;
+        lbs[K - 1] = (int)((W + (unsigned)(S - 1)) / (unsigned)S);
       }
       const int cj = cur[jj];
       if (cj == NC - 1) break;
@@ -1083,8 +1093,9 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       const unsigned nxp = (unsigned)su[jj] | ((unsigned)bestnode[jj] << 8);
       const int best = (int)((nxp >> (3 * cj)) & 7u);
       cp = cp - (1ull << (11 * cj)) + (1ull << (11 * best));
-      W += (long long)((unsigned)size_of<NC>(best) * (unsigned)T[jj * NC + best]) -
-           (long long)((unsigned)size_of<NC>(cj) * (unsigned)T[jj * NC + cj]);
+      entp += 1ull << (11 * best);
+      W += (unsigned)size_of<NC>(best) * (unsigned)T[jj * NC + best] -
+           (unsigned)size_of<NC>(cj) * (unsigned)T[jj * NC + cj];
       __syncwarp();
       if (lane == 0) {
         cur[jj] = (uint8_t)best;
@@ -1108,12 +1119,10 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   //          member interval; order (-t(s), task) (Alg. 1 lines 1-2)
   {
     int acc = 0;
+#pragma unroll
     for (int c = 0; c < NC; ++c) {
-      int cnt = 0;
-      for (int j = lane; j < n; j += 32) cnt += ((ivl[j * NC + c] & IM) != IM);
-      cnt = __reduce_add_sync(FULL, cnt);
       if (lane == 0) loff[c] = acc;
-      acc += cnt;
+      acc += (int)((entp >> (11 * c)) & 2047u);
     }
     if (lane == 0) loff[NC] = acc;
     __syncwarp();
@@ -1162,6 +1171,12 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         // per comparison; the rank is then m - rk (keys are distinct)
         if (m <= 32) {
           for (int f = 0; f < m; ++f) count_ge(rk[0], kk[f], key[0]);
+        } else if (m <= 64) {
+          for (int f = 0; f < m; ++f) {
+            const unsigned v = kk[f];
+            count_ge(rk[0], v, key[0]);
+            count_ge(rk[1], v, key[1]);
+          }
         } else {
           for (int f = 0; f < m; ++f) {
             const unsigned v = kk[f];
@@ -1212,7 +1227,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     int* gl = P.ws_lb + inst * (int64_t)P.ws_kcap;
     unsigned long long* gc = P.ws_cnt + inst * (int64_t)P.ws_kcap;
     for (int k = lane; k < K; k += 32) {
-      gl[k] = max(lbh[k], (int)((lbw[k] + S - 1) / S));  // max(h_k, ceil(W_k / #slices))
+      gl[k] = max(lbh[k], lbs[k]);  // max(h_k, ceil(W_k / #slices))
       gc[k] = cnts[k];
     }
     // member 0's entries (interval lo == 0: the a^1 sizes), compacted per size for K2
@@ -1256,8 +1271,8 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     int got = 0;
     while (got < 32 && nextk < K) {
       const int cand = nextk + lane;
-      // prune iff max(h_k, ceil(W_k / S)) >= bestms  <=>  h_k >= bestms || W_k > S*(bestms-1)
-      const bool ok = cand < K && (!prune || (lbh[cand] < bestms && lbw[cand] <= (long long)S * (bestms - 1)));
+      // prune iff max(h_k, ceil(W_k / S)) >= bestms
+      const bool ok = cand < K && (!prune || (lbh[cand] < bestms && lbs[cand] < bestms));
       const unsigned bal = __ballot_sync(FULL, ok);
       const int pos = __popc(bal & ((1u << lane) - 1));
       const int need = 32 - got;
