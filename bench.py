@@ -155,6 +155,16 @@ def secondary(far, torch, dev, reps=5):
     F.sync()
     out["M3_instances_per_s"] = d.shape[0] / (ms / 1000.0)
     out["M3_ms"] = ms
+    # schedule export + feasibility check of the M3 outputs (far_schedule_events,
+    # far_validate_schedules)
+    ev, nev, ems = F.schedule_events(d, bufs[1], stream=st)
+    msv = timed(lambda: F.schedule_events(d, bufs[1], stream=st))
+    ms_chk = timed(lambda: F.validate_schedules(d, bufs[1], ev, nev, stream=st))
+    viol = F.validate_schedules(d, bufs[1], ev, nev, stream=st)
+    F.sync()
+    out["M3_events_instances_per_s"] = d.shape[0] / (msv / 1000.0)
+    out["M3_validate_instances_per_s"] = d.shape[0] / (ms_chk / 1000.0)
+    out["M3_infeasible_outputs"] = int((viol != 0).sum().item())
     for prof in ("A30", "A100"):
         w = inputs.WORKLOADS["M4_" + prof]
         S = 1024

@@ -169,6 +169,46 @@ far_status far_concat_streams(far_ctx *ctx, const int32_t *d_times, int64_t S, i
                               const far_opts *opts, int64_t *d_stream_makespan, int64_t *d_offsets,
                               far_task_slot *d_sched, far_result *d_batch_res, int32_t *d_seam, void *cuda_stream);
 
+/* ---- Checking and export of schedules.
+ *
+ * A reconfiguration event: kind 0 = create, 1 = destroy; node id; start and duration in
+ * ticks (the create/destroy cost of the node's size, Table 2 / the ctx costs). */
+typedef struct {
+  int32_t kind;
+  int32_t node;
+  int32_t start;
+  int32_t dur;
+} far_event;
+
+/* Reconfiguration events of I schedules (device memory, async on cuda_stream).  For each
+ * instance the node lists are rebuilt from d_sched[I][n] (a task belongs to its node's list,
+ * ordered by (start, task)) and the line-26 replay (Alg. 1's event loop taking each node's
+ * tasks from its list) is run; its create events and the destroy events
+ * issued while tasks remain unscheduled (Alg. 1 l.17-20) are written to
+ * d_events[I][2 * far_num_nodes(ctx)] in start order (events are disjoint in time: sequential
+ * reconfiguration), d_nev[I] = their number, d_makespan[I] (optional) = the
+ * replay's makespan.  For a schedule returned by far_solve_many the replay reproduces its
+ * starts (fixpoint), so these are exactly the schedule's reconfigurations.  An instance whose
+ * slot names a node that does not host its size gets d_nev = -1.  Costs: the ctx's, or zero
+ * with FAR_ZERO_RECONFIG in opts->flags. */
+far_status far_schedule_events(far_ctx *ctx, const int32_t *d_times, int64_t I, int32_t n,
+                               const far_task_slot *d_sched, const far_opts *opts, far_event *d_events,
+                               int32_t *d_nev, int32_t *d_makespan, void *cuda_stream);
+
+/* Feasibility check of I schedules with their events (device memory, async): d_violations[I]
+ * = the number of violated conditions, 0 for a feasible schedule: (0) every slot names a node
+ * hosting its size with start >= 0 (if not, only these are counted); (1) tasks on instances
+ * sharing a slice never overlap in time; (2) at every task start the running
+ * instances are pairwise disjoint tree nodes, i.e. a valid partition; (3) events
+ * have the node's create/destroy duration, are pairwise disjoint in time, every
+ * node with tasks is created exactly once before its first task and destroyed at most once
+ * after its last, nodes without tasks have no events, and of two nodes sharing a slice the
+ * earlier-created one is destroyed before the other is created.  d_events/d_nev as written
+ * by far_schedule_events (nev <= 2 * far_num_nodes). */
+far_status far_validate_schedules(far_ctx *ctx, const int32_t *d_times, int64_t I, int32_t n,
+                                  const far_task_slot *d_sched, const far_opts *opts, const far_event *d_events,
+                                  const int32_t *d_nev, int32_t *d_violations, void *cuda_stream);
+
 /* ---- Diagnostics (no compute; for bench.py and profiling).
  * Kernel stages of far_solve_many / far_concat_streams:
  *   PREP     H0-H3 (input checks, phase-1 family, per-size LPT lists), warp per instance
@@ -178,9 +218,10 @@ far_status far_concat_streams(far_ctx *ctx, const int32_t *d_times, int64_t S, i
  *   FINISH   H6-H7 (phase 3, line-26 replay, guard, output), warp per instance
  *   OVERFLOW fused H0-H7 for the instances PREP deferred (family > 64 members), warp per instance
  *   FUSED    fused H0-H7 (far_schedule_batch, far_local_search, n = 1024), warp per instance
- *   STREAM   multi-batch fold of far_concat_streams, warp per stream */
+ *   STREAM   multi-batch fold of far_concat_streams, warp per stream
+ *   CHECK    far_schedule_events / far_validate_schedules, warp per instance */
 enum { FAR_STAGE_PREP = 0, FAR_STAGE_MEMBER0, FAR_STAGE_MEMBERS, FAR_STAGE_WINNER, FAR_STAGE_FINISH,
-       FAR_STAGE_OVERFLOW, FAR_STAGE_FUSED, FAR_STAGE_STREAM, FAR_NUM_STAGES };
+       FAR_STAGE_OVERFLOW, FAR_STAGE_FUSED, FAR_STAGE_STREAM, FAR_STAGE_CHECK, FAR_NUM_STAGES };
 /* enable != 0: from now on every launch of the context is bracketed by CUDA events recorded
  * on the caller's stream (one event per stage boundary; the events add no synchronisation). */
 far_status far_stage_timing(far_ctx *ctx, int32_t enable);

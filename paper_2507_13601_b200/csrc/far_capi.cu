@@ -13,6 +13,7 @@
 #include "far_stream.cuh"
 #include "far_pipeline.cuh"
 #include "far_finish_lane.cuh"
+#include "far_check.cuh"
 
 using namespace farb;
 
@@ -102,6 +103,11 @@ static far_status ensure_device(far_ctx* ctx) {
   CK(cudaFuncSetAttribute((const void*)far_finish_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   CK(cudaFuncSetAttribute((const void*)far_finish_lane_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   CK(cudaFuncSetAttribute((const void*)far_finish_lane_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
+  {
+    const void* cf[4] = {(const void*)far_events_kernel<3>, (const void*)far_events_kernel<5>,
+                         (const void*)far_validate_kernel<3>, (const void*)far_validate_kernel<5>};
+    for (const void* f : cf) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
+  }
   for (const void* f : fns) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   ctx->inited = true;
   return FAR_OK;
@@ -716,3 +722,87 @@ extern "C" far_status far_concat_streams(far_ctx* ctx, const int32_t* d_times, i
   ++ctx->launches;
   return t_mark(ctx, tset, stream, FAR_STAGE_STREAM);
 }
+
+// ---- schedule events and validation (far_check.cuh), one warp per instance
+static far_status launch_check(far_ctx* ctx, CParams& Q, int64_t I, int n, bool validate, cudaStream_t stream) {
+  const bool a30 = ctx->nc == 3;
+  const int bytes = validate ? make_vlayout(n, ctx->nn).bytes : make_elayout(n, ctx->nn).bytes;
+  const void* fn = validate ? (a30 ? (const void*)far_validate_kernel<3> : (const void*)far_validate_kernel<5>)
+                            : (a30 ? (const void*)far_events_kernel<3> : (const void*)far_events_kernel<5>);
+  int warps = 0, per_sm = 0;
+  far_status st = pick_shape(ctx, fn, bytes, warps, per_sm);
+  if (st) return st;
+  const int slot = (ctx->launch_id++ % (RING / 8)) * 8;
+  CK(cudaMemsetAsync(ctx->d_counter + slot, 0, sizeof(unsigned long long), stream));
+  Q.counter = ctx->d_counter + slot;
+  far_ctx::EvSet* tset = nullptr;
+  if ((st = t_begin(ctx, stream, tset))) return st;
+  const size_t smem = (size_t)warps * bytes;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((I + warps - 1) / warps, (int64_t)ctx->sms * per_sm));
+  if (validate) {
+    if (a30) far_validate_kernel<3><<<grid, warps * 32, smem, stream>>>(Q);
+    else far_validate_kernel<5><<<grid, warps * 32, smem, stream>>>(Q);
+  } else {
+    if (a30) far_events_kernel<3><<<grid, warps * 32, smem, stream>>>(Q);
+    else far_events_kernel<5><<<grid, warps * 32, smem, stream>>>(Q);
+  }
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  return t_mark(ctx, tset, stream, FAR_STAGE_CHECK);
+}
+
+static far_status check_args(far_ctx* ctx, const int32_t* d_times, int64_t I, int32_t n, const far_task_slot* d_sched,
+                             const far_opts* opts, CParams& Q) {
+  if (I < 0 || n < 0) return fail(ctx, FAR_E_INVALID_ARG, "negative I or n");
+  if (n > MAXN) return fail(ctx, FAR_E_TOO_LARGE, "n > 1024");
+  if (I > 0 && n > 0 && (!d_times || !d_sched)) return fail(ctx, FAR_E_INVALID_ARG, "null device pointer");
+  far_status st = check_opts(ctx, opts);
+  if (st) return st;
+  if ((st = ensure_device(ctx))) return st;
+  KParams P;
+  fill_params(ctx, opts, P);
+  memset(&Q, 0, sizeof(Q));
+  Q.times = d_times;
+  Q.sched = d_sched;
+  Q.I = I;
+  Q.n = n;
+  for (int c = 0; c < 8; ++c) {
+    Q.cr[c] = P.cr[c];
+    Q.de[c] = P.de[c];
+  }
+  return FAR_OK;
+}
+
+extern "C" {
+
+far_status far_schedule_events(far_ctx* ctx, const int32_t* d_times, int64_t I, int32_t n,
+                               const far_task_slot* d_sched, const far_opts* opts, far_event* d_events,
+                               int32_t* d_nev, int32_t* d_makespan, void* cuda_stream) {
+  if (!ctx) return FAR_E_INVALID_ARG;
+  CParams Q;
+  far_status st = check_args(ctx, d_times, I, n, d_sched, opts, Q);
+  if (st) return st;
+  if (I > 0 && (!d_events || !d_nev)) return fail(ctx, FAR_E_INVALID_ARG, "null device pointer");
+  if (I == 0) return FAR_OK;
+  Q.events = d_events;
+  Q.nev = d_nev;
+  Q.makespan = d_makespan;
+  return launch_check(ctx, Q, I, n, false, (cudaStream_t)cuda_stream);
+}
+
+far_status far_validate_schedules(far_ctx* ctx, const int32_t* d_times, int64_t I, int32_t n,
+                                  const far_task_slot* d_sched, const far_opts* opts, const far_event* d_events,
+                                  const int32_t* d_nev, int32_t* d_violations, void* cuda_stream) {
+  if (!ctx) return FAR_E_INVALID_ARG;
+  CParams Q;
+  far_status st = check_args(ctx, d_times, I, n, d_sched, opts, Q);
+  if (st) return st;
+  if (I > 0 && (!d_events || !d_nev || !d_violations)) return fail(ctx, FAR_E_INVALID_ARG, "null device pointer");
+  if (I == 0) return FAR_OK;
+  Q.events_in = d_events;
+  Q.nev_in = d_nev;
+  Q.violations = d_violations;
+  return launch_check(ctx, Q, I, n, true, (cudaStream_t)cuda_stream);
+}
+
+}  // extern "C"

@@ -210,7 +210,7 @@ template <int S> struct Frontier {
 // both loops apply the same reconfiguration events in the same order and give identical
 // starts (a destroy charged after the last task started cannot delay any creation).  This
 // takes <= 2*#nodes heap steps instead of n + #nodes; task starts are then prefix sums
-// over each node list (one lane per node).  life[v*6] = {cs, ce, ds, de}.
+// over each node list (one lane per node).  life[v*6] = {cs, ce, ds, de, creation pop time, end}.
 // The frontier is spread over the warp: lane s < S holds slot s's key
 // (end << 3 | s); the control state (rec, has, slot -> node map, live) is uniform, so every
 // lane follows the same path and a pop is one REDUX.MIN instead of an unrolled scan.
@@ -218,7 +218,10 @@ template <int NC>
 __device__ int node_sim_warp(const int* ncnt, const int* nsum, int* life, const uint32_t* ninfo, const int* cr,
                              const int* de, int lane, int& Eout) {
   constexpr int NN = Tree<NC>::NN;
-  if (lane < NN) life[lane * 6] = -1;
+  if (lane < NN) {
+    life[lane * 6 + 0] = -1;  // not created
+    life[lane * 6 + 2] = -1;  // not destroyed
+  }
   unsigned e = lane == 0 ? 0u : 0xFFFFFFFFu;  // root in slot 0 at time 0
   uint32_t slotnode = 0, live = 1, has = 0;
   int rec = 0, ms = 0, E = 0;
@@ -230,11 +233,13 @@ __device__ int node_sim_warp(const int* ncnt, const int* nsum, int* life, const 
     if (!((has >> bs) & 1) && ncnt[v] > 0) {  // creation (lines 8-11), then all of v's tasks
       const int cs = max(rec, be);
       rec = cs + cr[nd_szi(w)];
+      const int f = rec + nsum[v];
       if (lane == 0) {
         life[v * 6 + 0] = cs;
         life[v * 6 + 1] = rec;
+        life[v * 6 + 4] = be;  // pop time of the creation (= first task's placement pop)
+        life[v * 6 + 5] = f;   // end of the node's tasks (its split / destroy pop)
       }
-      const int f = rec + nsum[v];
       ms = max(ms, f);
       E = max(E, f);
       has |= 1u << bs;

@@ -23,14 +23,15 @@ NO_REFINE, NO_GUARD, ZERO_RECONFIG, NO_SCHEDULE, EXHAUSTIVE = 1, 2, 4, 8, 16
 STATUS = {0: "FAR_OK", 1: "FAR_E_INVALID_ARG", 2: "FAR_E_UNSUPPORTED_PROFILE", 3: "FAR_E_BAD_TIME",
           4: "FAR_E_TOO_LARGE", 5: "FAR_E_CUDA", 6: "FAR_E_OOM"}
 
-STAGES = ("prep", "member0", "members", "winner", "finish", "overflow", "fused", "stream")  # FAR_STAGE_*
+STAGES = ("prep", "member0", "members", "winner", "finish", "overflow", "fused", "stream", "check")  # FAR_STAGE_*
 
 SLOT_DT = np.dtype([("node", "u1"), ("size_used", "u1"), ("pad", "u1", 2), ("start", "<i4")])
 RESULT_DT = np.dtype([("makespan", "<i4"), ("makespan_phase2", "<i4"), ("alloc_index", "<i4"),
                       ("family_size", "<i4"), ("moves", "<i4"), ("swaps", "<i4"), ("iterations", "<i4"),
                       ("reverted", "<i4"), ("status", "<i4"), ("reserved", "<i4"), ("evals", "<i8"),
                       ("events", "<i8")])
-assert SLOT_DT.itemsize == 8 and RESULT_DT.itemsize == 56
+EVENT_DT = np.dtype([("kind", "<i4"), ("node", "<i4"), ("start", "<i4"), ("dur", "<i4")])  # far_event
+assert SLOT_DT.itemsize == 8 and RESULT_DT.itemsize == 56 and EVENT_DT.itemsize == 16
 
 
 class FarError(RuntimeError):
@@ -75,6 +76,8 @@ def lib():
             "far_solve_many": ([p, p, i64, i32, p, p, p, p, p], C.c_int),
             "far_solve_many_host": ([p, p, i64, i32, p, p, p, p], C.c_int),
             "far_concat_streams": ([p, p, i64, i32, i32, p, p, p, p, p, p, p], C.c_int),
+            "far_schedule_events": ([p, p, i64, i32, p, p, p, p, p, p], C.c_int),
+            "far_validate_schedules": ([p, p, i64, i32, p, p, p, p, p, p], C.c_int),
             "far_stage_timing": ([p, i32], C.c_int),
             "far_stage_times": ([p, p], i32),
             "far_launch_count": ([p], i64),
@@ -230,6 +233,44 @@ class Far:
                                              _t_ptr(off), _t_ptr(sd), _t_ptr(br), _t_ptr(se),
                                              C.c_void_p(st.cuda_stream)))
         return sm, off, sd, br, se
+
+
+    # -- schedule export and checking (device memory) ----------------------------------
+    def schedule_events(self, d_times, d_sched, *, stream=None, flags=0):
+        """Reconfiguration events of schedules (include/far.h far_schedule_events).
+        d_times int32 [I][n][nsizes], d_sched uint8 [I][n][8] (far_task_slot) CUDA tensors ->
+        (events uint8 [I][2*nnodes][16] viewable as EVENT_DT, nev int32 [I], makespan int32 [I])."""
+        import torch
+        I, n = d_times.shape[0], d_times.shape[1]
+        dev = d_times.device
+        ev = torch.empty((I, 2 * self.nnodes, 16), dtype=torch.uint8, device=dev)
+        nev = torch.empty(I, dtype=torch.int32, device=dev)
+        ms = torch.empty(I, dtype=torch.int32, device=dev)
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        o = _opts(flags=flags)
+        self._check(lib().far_schedule_events(self._h, _t_ptr(d_times), I, n, _t_ptr(d_sched), C.byref(o), _t_ptr(ev),
+                                              _t_ptr(nev), _t_ptr(ms), C.c_void_p(st.cuda_stream)))
+        return ev, nev, ms
+
+    def validate_schedules(self, d_times, d_sched, d_events, d_nev, *, stream=None, flags=0):
+        """Violation count per schedule (include/far.h far_validate_schedules) -> int32 [I]."""
+        import torch
+        I, n = d_times.shape[0], d_times.shape[1]
+        dev = d_times.device
+        viol = torch.empty(I, dtype=torch.int32, device=dev)
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        o = _opts(flags=flags)
+        self._check(lib().far_validate_schedules(self._h, _t_ptr(d_times), I, n, _t_ptr(d_sched), C.byref(o),
+                                                 _t_ptr(d_events), _t_ptr(d_nev), _t_ptr(viol),
+                                                 C.c_void_p(st.cuda_stream)))
+        return viol
+
+
+def events_np(ev_tensor, nev_tensor):
+    """-> list of EVENT_DT arrays, one per instance."""
+    ev = ev_tensor.cpu().numpy().view(EVENT_DT)[..., 0]
+    nev = nev_tensor.cpu().numpy()
+    return [ev[i, :max(int(nev[i]), 0)].copy() for i in range(ev.shape[0])]
 
 
 def slots_np(sd_tensor):
