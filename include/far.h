@@ -209,6 +209,13 @@ far_status far_validate_schedules(far_ctx *ctx, const int32_t *d_times, int64_t 
                                   const far_task_slot *d_sched, const far_opts *opts, const far_event *d_events,
                                   const int32_t *d_nev, int32_t *d_violations, void *cuda_stream);
 
+/* Lower bound of the optimal makespan of I instances (device memory, async):
+ * d_sum_min_work[I] = sum_i min_s s * t_i(s) (the paper's baseline is this / #slices, and
+ * rho = makespan / baseline, Tables 4 and 9) and d_max_min_time[I] (or NULL) = max_i min_s t_i(s).
+ * Both bound every schedule's makespan with or without reconfiguration. */
+far_status far_lower_bounds(far_ctx *ctx, const int32_t *d_times, int64_t I, int32_t n, int64_t *d_sum_min_work,
+                            int32_t *d_max_min_time, void *cuda_stream);
+
 /* ---- Diagnostics (no compute; for bench.py and profiling).
  * Kernel stages of far_solve_many / far_concat_streams:
  *   PREP     H0-H3 (input checks, phase-1 family, per-size LPT lists), warp per instance

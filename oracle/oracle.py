@@ -253,3 +253,26 @@ def stream(profile, costs, times, max_iterations=100, min_improvement_ppm=0, fla
                             flags, _ptr(out2), _ptr(offs), _ptr(seam), _ptr(slots), _ptr(res), _ptr(viol)))
     return {"makespan": int(out2[0]), "trivial": int(out2[1]), "offsets": offs, "seam": seam, "slots": slots,
             "results": res, "violations": int(viol[0])}
+
+
+def table_stats(profile, costs, tables, max_iterations=100, min_improvement_ppm=0, flags=0):
+    """The evaluation statistics of PAPER.md §6 as exact fractions over a set of instances:
+      rho   = omega / baseline, baseline = sum_i min_s s * t_i(s) / #slices   (Table 4)
+      p_ref = (omega_no_ref / omega_ref - 1) * 100                             (Table 6)
+    with omega_no_ref = FAR without phase 3 = the phase-2 makespan (R13), and the mean numbers of
+    moves and swaps (Table 6).  Returns {"rho", "p_ref", "moves", "swaps", "count"} (Fractions)."""
+    from fractions import Fraction
+    t = np.asarray(tables, dtype=np.int32)
+    ms, res = far_many(profile, costs, t, max_iterations=max_iterations, min_improvement_ppm=min_improvement_ppm,
+                       flags=flags)
+    S = lib().orc_num_slices(pid(profile))
+    I = t.shape[0]
+    rho = Fraction(0)
+    pref = Fraction(0)
+    for i in range(I):
+        w, _ = lower_bound(profile, t[i])
+        rho += Fraction(int(ms[i]) * S, w)
+        pref += (Fraction(int(res["makespan_phase2"][i]), int(ms[i])) - 1) * 100
+    return {"rho": rho / I, "p_ref": pref / I, "moves": Fraction(int(res["moves"].sum()), I),
+            "swaps": Fraction(int(res["swaps"].sum()), I), "count": I}
+

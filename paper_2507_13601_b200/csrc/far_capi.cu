@@ -805,4 +805,23 @@ far_status far_validate_schedules(far_ctx* ctx, const int32_t* d_times, int64_t 
   return launch_check(ctx, Q, I, n, true, (cudaStream_t)cuda_stream);
 }
 
+far_status far_lower_bounds(far_ctx* ctx, const int32_t* d_times, int64_t I, int32_t n, int64_t* d_sum_min_work,
+                            int32_t* d_max_min_time, void* cuda_stream) {
+  if (!ctx) return FAR_E_INVALID_ARG;
+  if (I < 0 || n < 0) return fail(ctx, FAR_E_INVALID_ARG, "negative I or n");
+  if (I > 0 && (!d_sum_min_work || (n > 0 && !d_times))) return fail(ctx, FAR_E_INVALID_ARG, "null device pointer");
+  far_status st = ensure_device(ctx);
+  if (st) return st;
+  if (I == 0) return FAR_OK;
+  cudaStream_t stream = (cudaStream_t)cuda_stream;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((I + 255) / 256, (int64_t)ctx->sms * 8));
+  if (ctx->nc == 3)
+    far_lower_bound_kernel<3><<<grid, 256, 0, stream>>>(d_times, I, n, (long long*)d_sum_min_work, d_max_min_time);
+  else
+    far_lower_bound_kernel<5><<<grid, 256, 0, stream>>>(d_times, I, n, (long long*)d_sum_min_work, d_max_min_time);
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  return FAR_OK;
+}
+
 }  // extern "C"

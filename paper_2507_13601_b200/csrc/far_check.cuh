@@ -330,4 +330,33 @@ __global__ void __launch_bounds__(128) far_validate_kernel(CParams P) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Lower bound of the optimal makespan: baseline = sum_i min_s s * t_i(s) / #slices
+// and max_i min_s t_i(s); one thread per instance (the evaluation metric rho = omega / baseline of
+// Tables 4 and 9).
+// ---------------------------------------------------------------------------
+template <int NC>
+__global__ void __launch_bounds__(256) far_lower_bound_kernel(const int32_t* __restrict__ times, int64_t I, int n,
+                                                              long long* sum_min_work, int32_t* max_min_time) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < I; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t* t = times + i * (int64_t)n * NC;
+    long long W = 0;
+    int H = 0;
+    for (int j = 0; j < n; ++j) {
+      long long w = LLONG_MAX;
+      int h = INT_MAX;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int x = __ldg(t + j * NC + c);
+        w = min(w, (long long)size_of<NC>(c) * x);
+        h = min(h, x);
+      }
+      W += w;
+      H = max(H, h);
+    }
+    sum_min_work[i] = W;
+    if (max_min_time) max_min_time[i] = H;
+  }
+}
+
 }  // namespace farb

@@ -78,6 +78,7 @@ def lib():
             "far_concat_streams": ([p, p, i64, i32, i32, p, p, p, p, p, p, p], C.c_int),
             "far_schedule_events": ([p, p, i64, i32, p, p, p, p, p, p], C.c_int),
             "far_validate_schedules": ([p, p, i64, i32, p, p, p, p, p, p], C.c_int),
+            "far_lower_bounds": ([p, p, i64, i32, p, p, p], C.c_int),
             "far_stage_timing": ([p, i32], C.c_int),
             "far_stage_times": ([p, p], i32),
             "far_launch_count": ([p], i64),
@@ -264,6 +265,18 @@ class Far:
                                                  _t_ptr(d_events), _t_ptr(d_nev), _t_ptr(viol),
                                                  C.c_void_p(st.cuda_stream)))
         return viol
+
+    def lower_bounds(self, d_times, *, stream=None):
+        """-> (sum_min_work int64 [I], max_min_time int32 [I]) CUDA tensors (far_lower_bounds)."""
+        import torch
+        I, n = d_times.shape[0], d_times.shape[1]
+        dev = d_times.device
+        w = torch.empty(I, dtype=torch.int64, device=dev)
+        h = torch.empty(I, dtype=torch.int32, device=dev)
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        self._check(lib().far_lower_bounds(self._h, _t_ptr(d_times), I, n, _t_ptr(w), _t_ptr(h),
+                                           C.c_void_p(st.cuda_stream)))
+        return w, h
 
 
 def events_np(ev_tensor, nev_tensor):
