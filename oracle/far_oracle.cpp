@@ -308,7 +308,7 @@ void insert_ordered(const Problem& P, const Sched& S, std::vector<int>& lst, int
   lst.insert(it, j);
 }
 
-RefineStats refine(const Problem& P, Sched& S, int max_iterations, int ppm) {
+RefineStats refine(const Problem& P, Sched& S, int max_iterations, int ppm, bool nonempty_alt) {
   const Model& m = P.m;
   const int N = (int)m.node.size();
   RefineStats st;
@@ -349,6 +349,7 @@ RefineStats refine(const Problem& P, Sched& S, int max_iterations, int ppm) {
       i64 eA = 0;
       for (int u = 0; u < N; ++u) {
         if (u == I || m.node[u].size() != m.node[I].size()) continue;
+        if (nonempty_alt && S.list[u].empty()) continue;  // variant ORC_NONEMPTY_ALT
         i64 e = end_of(u);
         if (A < 0 || e < eA || (e == eA && m.node[u].lo < m.node[A].lo)) { A = u; eA = e; }
       }
@@ -427,7 +428,7 @@ void write_events(const Sched& S, orc_event* ev, int32_t* nev) {
 Sched refine_and_replay(const Problem& P, const Sched& S2, i64 ms2, int max_it, int ppm, uint32_t flags,
                         orc_result* res) {
   Sched S = S2;
-  RefineStats st = refine(P, S, max_it, ppm);
+  RefineStats st = refine(P, S, max_it, ppm, (flags & ORC_NONEMPTY_ALT) != 0);
   Sched R = replay(P, S);
   res->moves = st.moves;
   res->swaps = st.swaps;

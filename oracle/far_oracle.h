@@ -32,7 +32,9 @@ typedef struct {
   int32_t alloc_index, family_size, moves, swaps, reverted, iterations;
 } orc_result;
 
-enum { ORC_NO_REFINE = 1u, ORC_NO_GUARD = 2u, ORC_ZERO_RECONFIG = 4u };
+/* ORC_NONEMPTY_ALT: reading variant -- Alg. 2's alternative I^a
+ * must hold at least one task (default: any same-size node, P:524 literally). */
+enum { ORC_NO_REFINE = 1u, ORC_NO_GUARD = 2u, ORC_ZERO_RECONFIG = 4u, ORC_NONEMPTY_ALT = 32u };
 
 int orc_num_sizes(int profile);
 int orc_num_nodes(int profile);

@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "liboracle.so")
 SOURCES = ["far_oracle.cpp"]
 
 PROFILES = {"A30": 0, "A100": 1, "H100": 2}
-NO_REFINE, NO_GUARD, ZERO_RECONFIG = 1, 2, 4
+NO_REFINE, NO_GUARD, ZERO_RECONFIG, NONEMPTY_ALT = 1, 2, 4, 32
 
 
 def build(force: bool = False) -> str:

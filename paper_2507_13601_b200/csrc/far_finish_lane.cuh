@@ -75,8 +75,8 @@ __device__ __forceinline__ void lane_transfer(uint32_t* ent, uint16_t* off, int 
 
 // Alg. 2 on one thread; same readings as refine_warp.
 template <int NC>
-__device__ void refine_lane(uint32_t* ent, uint16_t* off, int (&send)[Tree<NC>::S], int max_it, int ppm, int& moves,
-                            int& swaps, int& iters, long long& evals) {
+__device__ void refine_lane(uint32_t* ent, uint16_t* off, int (&send)[Tree<NC>::S], int max_it, int ppm,
+                            bool nonempty_alt, int& moves, int& swaps, int& iters, long long& evals) {
   constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
   int omega = 0;
 #pragma unroll
@@ -107,7 +107,7 @@ __device__ void refine_lane(uint32_t* ent, uint16_t* off, int (&send)[Tree<NC>::
 #pragma unroll
       for (int u = 0; u < NN; ++u) {
         const uint32_t wu = cnode<NC>(u);
-        if (u != I && nd_sz(wu) == nd_sz(wI)) {  // argmin (end, first slice)
+        if (u != I && nd_sz(wu) == nd_sz(wI) && (!nonempty_alt || off[u + 1] > off[u])) {  // argmin (end, lo)
           const int eu = lane_end<S>(wu, send);
           if (eu < eA || (eu == eA && nd_lo(wu) < loA)) { eA = eu; A = u; loA = nd_lo(wu); }
         }
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(128) far_finish_lane_kernel(KParams P) {
         for (int s = 0; s < S; ++s) send[s] = P.ws_sl[inst * 8 + s];
         int mv, sw, it;
         long long ev;
-        refine_lane<NC>(ent, off, send, P.max_it, P.ppm, mv, sw, it, ev);
+        refine_lane<NC>(ent, off, send, P.max_it, P.ppm, (P.flags & FAR_NONEMPTY_ALT) != 0, mv, sw, it, ev);
         R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
       }
       if (!need_replay) break;

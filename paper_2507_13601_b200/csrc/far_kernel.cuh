@@ -386,8 +386,8 @@ __device__ void list_insert(uint16_t* lst, int* cnt, int j, const int* D, int la
 
 template <int NC>
 __device__ void refine_warp(int n, const int* D, uint16_t* nlist, int* ncnt, int* send,
-                            const uint32_t* ninfo, int max_it, int ppm, int lane, int& moves, int& swaps, int& iters,
-                            long long& evals) {
+                            const uint32_t* ninfo, int max_it, int ppm, bool nonempty_alt, int lane, int& moves,
+                            int& swaps, int& iters, long long& evals) {
   constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
   auto end_of = [&](uint32_t w) {
     int e = 0;
@@ -423,7 +423,7 @@ __device__ void refine_warp(int n, const int* D, uint16_t* nlist, int* ncnt, int
       // alternative I^a: same size, != I, minimum (end, first slice) -- lanes over nodes
       bool valid = false;
       int eu = INT_MAX, lou = 15;
-      if (lane < NN && lane != I && nd_sz(ninfo[lane]) == nd_sz(wI)) {
+      if (lane < NN && lane != I && nd_sz(ninfo[lane]) == nd_sz(wI) && (!nonempty_alt || ncnt[lane] > 0)) {
         valid = true;
         eu = end_of(ninfo[lane]);
         lou = nd_lo(ninfo[lane]);
@@ -636,7 +636,8 @@ __device__ __noinline__ void solve_local(const KParams& P, int64_t inst, unsigne
       int* D = (int*)(scratch + ((2 * NN * n + 3) & ~3));  // durations at the tasks' sizes
       for (int j = lane; j < n; j += 32) D[j] = T[j * NC + su[j]];
       __syncwarp();
-      refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
+      refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, (P.flags & FAR_NONEMPTY_ALT) != 0, lane, mv,
+                      sw, it, ev);
       R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
       const int msR = replay_warp<NC>(n, D, nlist, ncnt, nsum, life, start, bestnode, ninfo, cr, de, lane);
       if (!(P.flags & FAR_NO_GUARD) && msR > ms2) {
@@ -722,7 +723,8 @@ __device__ void finish_core(const KParams& P, int64_t inst, uint16_t* nlist, int
       __syncwarp();
       int mv, sw, it;
       long long ev;
-      refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
+      refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, (P.flags & FAR_NONEMPTY_ALT) != 0, lane, mv,
+                      sw, it, ev);
       R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
     }
     if (!need_replay) break;

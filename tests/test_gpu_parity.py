@@ -30,7 +30,7 @@ def run_gpu(torch_dev, profile, costs, tab, **kw):
 
 
 def check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=0, max_iterations=100, ppm=0, full=True):
-    oflags = flags & (O.NO_REFINE | O.NO_GUARD | O.ZERO_RECONFIG)
+    oflags = flags & (O.NO_REFINE | O.NO_GUARD | O.ZERO_RECONFIG | O.NONEMPTY_ALT)
     oms, ores = O.far_many(profile, costs, tab, max_iterations=max_iterations, min_improvement_ppm=ppm, flags=oflags)
     bad = np.nonzero(ms != oms)[0]
     assert len(bad) == 0, f"makespan mismatch at {bad[:10]}: gpu {ms[bad[:5]]} oracle {oms[bad[:5]]}"
@@ -129,9 +129,21 @@ def test_finish_paths_agree(O, torch_dev, monkeypatch, switch, wname, gen):
     else:
         profile = wname
         costs, tab = inputs.reconfig_costs(profile), inputs.monotone_ties(profile, 40, 200, 9)
-    for flags in (0, far.NO_GUARD):
+    for flags in (0, far.NO_GUARD, far.NONEMPTY_ALT):
         ms, slots, res = run_gpu(torch_dev, profile, costs, tab, flags=flags)
         check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=flags)
+
+
+@pytest.mark.parametrize("profile,n", [("A100", 10), ("A100", 16), ("A30", 8)])
+def test_nonempty_alt_variant(O, torch_dev, profile, n):
+    # the NEXT-3 reading variant (FAR_NONEMPTY_ALT) against the oracle on small batches, where
+    # empty same-size nodes are common, and non-vacuous: it changes some outcomes
+    costs = inputs.reconfig_costs(profile)
+    tab = inputs.synthetic(profile, n, 300, 41)
+    ms0, _, r0 = run_gpu(torch_dev, profile, costs, tab)
+    ms1, s1, r1 = run_gpu(torch_dev, profile, costs, tab, flags=far.NONEMPTY_ALT)
+    check_against_oracle(O, profile, costs, tab, ms1, s1, r1, flags=far.NONEMPTY_ALT)
+    assert (r0["evals"] != r1["evals"]).any() and (ms0 != ms1).any()
 
 
 def test_input_errors_flagged(torch_dev):
