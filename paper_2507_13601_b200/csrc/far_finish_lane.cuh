@@ -83,6 +83,16 @@ __device__ void refine_lane(uint32_t* ent, uint16_t* off, int (&send)[Tree<NC>::
   for (int s = 0; s < S; ++s) omega = max(omega, send[s]);
   moves = swaps = iters = 0;
   evals = 0;
+  // candidate nodes for I^a: all, or (FAR_NONEMPTY_ALT) those holding a task -- a bit mask kept
+  // up to date by the transfers
+  uint32_t cand = 0xFFFFu;
+  if (nonempty_alt) {
+    cand = 0;
+    for (int v = 0; v < NN; ++v) cand |= (uint32_t)(off[v + 1] > off[v]) << v;
+  }
+  auto upd = [&](int v) {
+    if (nonempty_alt) cand = (cand & ~(1u << v)) | ((uint32_t)(off[v + 1] > off[v]) << v);
+  };
   bool stop = false;
   while (!stop && iters < max_it) {
     ++iters;
@@ -107,7 +117,7 @@ __device__ void refine_lane(uint32_t* ent, uint16_t* off, int (&send)[Tree<NC>::
 #pragma unroll
       for (int u = 0; u < NN; ++u) {
         const uint32_t wu = cnode<NC>(u);
-        if (u != I && nd_sz(wu) == nd_sz(wI) && (!nonempty_alt || off[u + 1] > off[u])) {  // argmin (end, lo)
+        if (u != I && nd_sz(wu) == nd_sz(wI) && ((cand >> u) & 1)) {  // argmin (end, first slice)
           const int eu = lane_end<S>(wu, send);
           if (eu < eA || (eu == eA && nd_lo(wu) < loA)) { eA = eu; A = u; loA = nd_lo(wu); }
         }
@@ -131,6 +141,8 @@ __device__ void refine_lane(uint32_t* ent, uint16_t* off, int (&send)[Tree<NC>::
         }
         if (bd != UINT_MAX) {
           lane_transfer<NN>(ent, off, I, A, bx);
+          upd(I);
+          upd(A);
           const int delta = (int)(bx >> 10);
 #pragma unroll
           for (int s = 0; s < S; ++s) {
@@ -281,7 +293,7 @@ __device__ int lane_replay(const uint32_t* ent, const uint16_t* off, const uint3
 }
 
 template <int NC>
-__global__ void __launch_bounds__(128) far_finish_lane_kernel(KParams P) {
+__global__ void __launch_bounds__(128, 3) far_finish_lane_kernel(KParams P) {
   constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ int s_cr[8], s_de[8];
