@@ -1401,7 +1401,7 @@ __constant__ uint32_t c_nodes5[13] = {
     Tree<5>::node[10], Tree<5>::node[11], Tree<5>::node[12]};
 
 template <int NC, int PIPE>
-__global__ void __launch_bounds__(128) far_solve_kernel(KParams P) {
+__global__ void __launch_bounds__(128, PIPE == PIPE_PREP ? 5 : 1) far_solve_kernel(KParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t ninfo[16];
   __shared__ int cr[8], de[8];
