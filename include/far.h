@@ -69,8 +69,10 @@ enum {
   FAR_ZERO_RECONFIG = 4u, /* ignore the ctx's create/destroy costs (all zero) */
   FAR_NO_SCHEDULE = 8u,   /* solve_many: do not write per-task slots (makespans/results only) */
   FAR_EXHAUSTIVE = 16u,   /* run Alg. 1 on every family member (disable the exact lower-bound skip) */
-  FAR_NONEMPTY_ALT = 32u  /* reading variant (R16): Alg. 2's alternative I^a must
+  FAR_NONEMPTY_ALT = 32u, /* reading variant (R16): Alg. 2's alternative I^a must
                              already hold a task (default: any same-size node, P:524 literally) */
+  FAR_NO_SEAM_MOVES = 64u /* far_concat_streams: reversal + seam offset only, no seam move/swap
+                             (Table 7's p_rev) */
 };
 
 typedef struct {

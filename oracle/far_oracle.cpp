@@ -1107,7 +1107,7 @@ extern "C" int orc_stream(int profile, const int32_t* costs, const int32_t* time
     const bool rev = (k % 2) == 1;
     Sched S = fin[k];
     SeamStats ss;
-    if (rev && k > 0) ss = seam_refine(Pb[k], S, st, max_iterations);
+    if (rev && k > 0 && !(flags & ORC_NO_SEAM_MOVES)) ss = seam_refine(Pb[k], S, st, max_iterations);
     Timeline T = batch_timeline(Pb[k], S, rev);
     SeamEval ev = seam_offset(mm, st, T);
     int reused = 0;

@@ -34,7 +34,8 @@ typedef struct {
 
 /* ORC_NONEMPTY_ALT: reading variant -- Alg. 2's alternative I^a
  * must hold at least one task (default: any same-size node, P:524 literally). */
-enum { ORC_NO_REFINE = 1u, ORC_NO_GUARD = 2u, ORC_ZERO_RECONFIG = 4u, ORC_NONEMPTY_ALT = 32u };
+/* ORC_NO_SEAM_MOVES: concatenation with reversal and seam offset only (Table 7's p_rev). */
+enum { ORC_NO_REFINE = 1u, ORC_NO_GUARD = 2u, ORC_ZERO_RECONFIG = 4u, ORC_NONEMPTY_ALT = 32u, ORC_NO_SEAM_MOVES = 64u };
 
 int orc_num_sizes(int profile);
 int orc_num_nodes(int profile);

@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "liboracle.so")
 SOURCES = ["far_oracle.cpp"]
 
 PROFILES = {"A30": 0, "A100": 1, "H100": 2}
-NO_REFINE, NO_GUARD, ZERO_RECONFIG, NONEMPTY_ALT = 1, 2, 4, 32
+NO_REFINE, NO_GUARD, ZERO_RECONFIG, NONEMPTY_ALT, NO_SEAM_MOVES = 1, 2, 4, 32, 64
 
 
 def build(force: bool = False) -> str:
@@ -276,3 +276,35 @@ def table_stats(profile, costs, tables, max_iterations=100, min_improvement_ppm=
     return {"rho": rho / I, "p_ref": pref / I, "moves": Fraction(int(res["moves"].sum()), I),
             "swaps": Fraction(int(res["swaps"].sum()), I), "count": I}
 
+
+
+def concat_stats(profile, costs, streams, max_iterations=100):
+    """Tables 7 and 8: over streams of batches [S][B][n][|C|], the means of
+      p_rev      = (omega_trivial / omega_rev - 1) * 100        reversal + seam offset only
+      p_move/swap = (omega_trivial / omega_move/swap - 1) * 100  + seam moves and swaps
+    and of the seam moves and swaps per stream, as exact Fractions."""
+    from fractions import Fraction
+    t = np.asarray(streams, dtype=np.int32)
+    S = t.shape[0]
+    prev = pms = Fraction(0)
+    mv = sw = 0
+    for s in range(S):
+        full = stream(profile, costs, t[s], max_iterations=max_iterations)
+        rev = stream(profile, costs, t[s], max_iterations=max_iterations, flags=NO_SEAM_MOVES)
+        assert rev["trivial"] == full["trivial"]
+        prev += (Fraction(full["trivial"], rev["makespan"]) - 1) * 100
+        pms += (Fraction(full["trivial"], full["makespan"]) - 1) * 100
+        mv += int(full["seam"][:, 1].sum())
+        sw += int(full["seam"][:, 2].sum())
+    return {"p_rev": prev / S, "p_move_swap": pms / S, "moves": Fraction(mv, S), "swaps": Fraction(sw, S), "count": S}
+
+
+def multi_batch_p(profile, costs, batches, max_iterations=100):
+    """Table 9: p_multi = (omega_multi / baseline_multi - 1) * 100 for one stream
+    [B][n][|C|], baseline_multi = sum over all tasks of min_s s * t(s) / #slices (exact Fraction)."""
+    from fractions import Fraction
+    t = np.asarray(batches, dtype=np.int32)
+    o = stream(profile, costs, t, max_iterations=max_iterations)
+    W = sum(lower_bound(profile, t[k])[0] for k in range(t.shape[0]))
+    S = lib().orc_num_slices(pid(profile))
+    return (Fraction(o["makespan"] * S, W) - 1) * 100

@@ -701,6 +701,7 @@ extern "C" far_status far_concat_streams(far_ctx* ctx, const int32_t* d_times, i
     Q.de[c] = P.de[c];
   }
   Q.max_it = P.max_it;
+  Q.seam_moves = (P.flags & FAR_NO_SEAM_MOVES) ? 0 : 1;
   Q.stream_ms = d_stream_makespan;
   Q.offsets = d_offsets;
   Q.out_sched = d_sched;

@@ -27,6 +27,7 @@ struct SParams {
   int B, n;
   int cr[8], de[8];
   int max_it;
+  int seam_moves;                // 0: FAR_NO_SEAM_MOVES
   int64_t* stream_ms;            // [S][2]
   int64_t* offsets;              // [S][B]
   far_task_slot* out_sched;      // [S][B][n] or null
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
     const bool rev = (k & 1) == 1;
     int moves = 0, swaps = 0;
     // ---- seam move/swap on reversed batches (R24)
-    if (rev && k > 0) {
+    if (rev && k > 0 && P.seam_moves) {
       SeamRes cur = eval_seam<NC>(n, T, su, D, nl, ncnt, nsum, onode, start, life, ninfo, cr, de, true, st, win, lane);
       for (int it = 0; it < P.max_it; ++it) {
         unsigned long long Q = 0;

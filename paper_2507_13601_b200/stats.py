@@ -34,3 +34,30 @@ def solve_and_measure(F, d_times, **kw) -> dict:
     res = far.results_np(rs)
     return table_means(F.nslices, ms.cpu().numpy(), res["makespan_phase2"], res["moves"], res["swaps"],
                        w.cpu().numpy())
+
+
+def concat_means(F, d_streams, **kw) -> dict:
+    """Tables 7 and 8 from far_concat_streams on device-resident streams
+    [S][B][n][|C|]: means over streams of p_rev (reversal + seam offset only, FAR_NO_SEAM_MOVES),
+    p_move/swap (the full fold) against the trivial concatenation, and of the seam moves / swaps."""
+    from . import far
+    flags = kw.pop("flags", 0)
+    sm, _, _, _, se = F.concat_streams(d_streams, sched=False, batch_res=False, flags=flags, **kw)
+    sr, _, _, _, _ = F.concat_streams(d_streams, sched=False, batch_res=False, seam=False,
+                                      flags=flags | far.NO_SEAM_MOVES, **kw)
+    sm, sr, se = sm.cpu().numpy(), sr.cpu().numpy(), se.cpu().numpy()
+    S = sm.shape[0]
+    assert (sm[:, 1] == sr[:, 1]).all()
+    prev = sum(((Fraction(int(a), int(b)) - 1) * 100 for a, b in zip(sm[:, 1], sr[:, 0])), Fraction(0))
+    pms = sum(((Fraction(int(a), int(b)) - 1) * 100 for a, b in zip(sm[:, 1], sm[:, 0])), Fraction(0))
+    return {"p_rev": prev / S, "p_move_swap": pms / S, "moves": Fraction(int(se[:, :, 1].sum()), S),
+            "swaps": Fraction(int(se[:, :, 2].sum()), S), "count": S}
+
+
+def multi_batch_p(F, d_batches, **kw) -> Fraction:
+    """Table 9: p_multi = (omega_multi / baseline_multi - 1) * 100 of one stream
+    [B][n][|C|] (far_concat_streams + far_lower_bounds, exact)."""
+    sm, _, _, _, _ = F.concat_streams(d_batches[None].contiguous(), sched=False, batch_res=False, seam=False, **kw)
+    w, _ = F.lower_bounds(d_batches)
+    W = int(w.sum().item())
+    return (Fraction(int(sm[0, 0].item()) * F.nslices, W) - 1) * 100

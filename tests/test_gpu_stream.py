@@ -71,3 +71,28 @@ def test_stream_edge_inputs(O, torch_dev, gen):
     check(O, profile, costs, tab, out)
     out = run_streams(torch_dev, profile, costs, tab, max_iterations=2)
     check(O, profile, costs, tab, out, max_iterations=2)
+
+
+@pytest.mark.parametrize("profile", ["A30", "A100"])
+def test_no_seam_moves_flag(O, torch_dev, profile):
+    # FAR_NO_SEAM_MOVES (reversal + seam offset only; Table 7's p_rev) against the oracle
+    tab = inputs.synthetic(profile, 10, 8 * 6, 77).reshape(8, 6, 10, -1)
+    costs = inputs.reconfig_costs(profile)
+    out = run_streams(torch_dev, profile, costs, tab, flags=far.NO_SEAM_MOVES)
+    check(O, profile, costs, tab, out, flags=O.NO_SEAM_MOVES)
+    assert (out[4][:, :, 1:3] == 0).all()
+
+
+@pytest.mark.parametrize("scaling,times", [("poor", "narrow"), ("mixed", "wide"), ("good", "narrow")])
+def test_concat_and_multibatch_statistics(O, torch_dev, scaling, times):
+    # Tables 7-9 statistics from the CUDA path equal the oracle's exact means
+    from paper_2507_13601_b200 import stats
+    torch, dev = torch_dev
+    costs = inputs.reconfig_costs("A100")
+    F = far.Far("A100", costs)
+    two = inputs.synthetic("A100", 10, 2 * 60, 300, scaling=scaling, times=times).reshape(60, 2, 10, -1)
+    got = stats.concat_means(F, torch.from_numpy(two).to(dev))
+    assert got == O.concat_stats("A100", costs, two)
+    long = inputs.synthetic("A100", 12, 101, 301, scaling=scaling, times=times)
+    assert stats.multi_batch_p(F, torch.from_numpy(long).to(dev)) == O.multi_batch_p("A100", costs, long)
+    F.sync()

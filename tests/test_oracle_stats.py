@@ -49,3 +49,19 @@ def test_statistics_bounds_and_mean(O):
         w, _ = O.lower_bound("A100", small[i])
         opt = O.bruteforce("A100", small[i])
         assert Fraction(opt * 7, w) <= r <= 2 * Fraction(opt * 7, w)
+
+
+def test_concat_statistics_closed_forms(O):
+    # two perfectly balanced batches (seven identical size-1 tasks each, zero reconfiguration):
+    # every slice is busy until T in both, so no reversal or seam move can overlap them and every
+    # concatenation gives 2T: p_rev = p_move/swap = 0
+    zero = inputs.reconfig_costs("A100", zero=True)
+    task = [700, 350, 700 // 3 + 1, 175, 100]
+    two = np.array([[[task] * 7, [task] * 7]], dtype=np.int32)
+    st = O.concat_stats("A100", zero, two)
+    assert st["p_rev"] == 0 and st["p_move_swap"] == 0 and st["moves"] == 0 and st["swaps"] == 0
+    assert O.multi_batch_p("A100", zero, two[0]) == 0  # omega = 1400 = baseline (2 * 7 * 700 / 7)
+    # a one-batch stream: p_multi = (rho - 1) * 100 of that batch (Tables 4 and 9 share the baseline)
+    costs = inputs.reconfig_costs("A100")
+    one = inputs.synthetic("A100", 15, 1, 92)
+    assert O.multi_batch_p("A100", costs, one) == (O.table_stats("A100", costs, one)["rho"] - 1) * 100

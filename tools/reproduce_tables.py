@@ -1,4 +1,4 @@
-"""Statistical reproduction of PAPER.md Tables 4 and 6 and the large-n scheduler-time workload on
+"""Statistical reproduction of PAPER.md Tables 4, 6, 7, 8, 9 and the large-n scheduler-time workload on
 the GPU, side by side with the values the paper prints
 (tests/golden/paper_tables.json).  The inputs come from this repo's §6.3 generator,
 not the paper's, so agreement is a plausibility signal for the readings, not a parity claim; the
@@ -35,7 +35,8 @@ def main():
     if args.oracle:
         from oracle import oracle as O
         O.build()
-    out = {"count": args.count, "table4": {}, "table6": {}, "large_n": {}, "oracle_checked": bool(args.oracle)}
+    out = {"count": args.count, "table4": {}, "table6": {}, "table7_8": {}, "table9": {}, "large_n": {},
+           "oracle_checked": bool(args.oracle)}
 
     def cell(n, scaling, times, seed):
         tab = inputs.synthetic("A100", n, args.count, seed, scaling=scaling, times=times)
@@ -61,6 +62,35 @@ def main():
                 rows.append({"n": n, "p_ref": float(g["p_ref"]), "moves": float(g["moves"]), "swaps": float(g["swaps"]),
                              "paper": paper})
             out["table6"][f"{sc}_{tm}"] = rows
+    # Tables 7 and 8: concatenations of two FAR schedules (the second reversed; the paper reports
+    # both orders together and finds them alike), count pairs per cell
+    t7, t8 = gold["table7_concat_A100"], gold["table8_concat_moves_swaps_A100"]
+    for sc in ("poor", "mixed", "good"):
+        for tm in ("narrow", "wide"):
+            rows = []
+            for q, n in enumerate(t7["n"]):
+                tab = inputs.synthetic("A100", n, 2 * args.count, 7000 + n, scaling=sc, times=tm).reshape(
+                    args.count, 2, n, -1)
+                g = stats.concat_means(F, torch.from_numpy(tab).to(dev))
+                F.sync()
+                if O is not None:
+                    assert g == O.concat_stats("A100", costs, tab), (n, sc, tm)
+                rows.append({"n": n, "p_rev": float(g["p_rev"]), "p_move_swap": float(g["p_move_swap"]),
+                             "moves": float(g["moves"]), "swaps": float(g["swaps"]),
+                             "paper7": t7[f"{sc}_{tm}"][q], "paper8": t8[f"{sc}_{tm}"][q]})
+            out["table7_8"][f"{sc}_{tm}"] = rows
+    # Table 9: one stream of 1001 batches per cell, WideTimes
+    t9 = gold["table9_multibatch_A100_wide"]
+    for sc in ("poor", "mixed", "good"):
+        rows = []
+        for n, paper in zip(t9["n"], t9[sc]):
+            tab = inputs.synthetic("A100", n, 1001, 9100 + n, scaling=sc, times="wide")
+            g = stats.multi_batch_p(F, torch.from_numpy(tab).to(dev))
+            F.sync()
+            if O is not None:
+                assert g == O.multi_batch_p("A100", costs, tab), (n, sc)
+            rows.append({"n": n, "p_multi": float(g), "paper": paper})
+        out["table9"][sc] = rows
     # the paper's scheduler-time workload: 1000 instances, MixedScaling, n = 100 / 500 / 1000
     ln = gold["large_n_cpu_ms"]
     for n, paper_ms in zip(ln["n"], ln["ms"]):
@@ -95,6 +125,19 @@ def main():
         lines.append(f"| {k} | " + " | ".join(
             f"{r['p_ref']:.2f}, {r['moves']:.2f}, {r['swaps']:.2f} / {r['paper'][0]:.2f}, {r['paper'][1]:.2f}, "
             f"{r['paper'][2]:.2f}" for r in rows) + " |")
+    lines += ["", "## Tables 7 and 8: concatenation of two FAR schedules, p_rev / p_move/swap (%) and seam moves, swaps "
+              "(ours / paper)", "",
+              "| workload | " + " | ".join(f"n={r['n']}" for r in out["table7_8"]["poor_narrow"]) + " |",
+              "|---|" + "---|" * len(out["table7_8"]["poor_narrow"])]
+    for k, rows in out["table7_8"].items():
+        lines.append(f"| {k} | " + " | ".join(
+            f"{r['p_rev']:.2f}, {r['p_move_swap']:.2f}; {r['moves']:.2f}, {r['swaps']:.2f} / "
+            f"{r['paper7'][0]:.2f}, {r['paper7'][1]:.2f}; {r['paper8'][0]:.2f}, {r['paper8'][1]:.2f}" for r in rows) + " |")
+    lines += ["", "## Table 9: p_multi-batch (%), 1001 batches, WideTimes (ours / paper)", "",
+              "| scaling | " + " | ".join(f"n={r['n']}" for r in out["table9"]["poor"]) + " |",
+              "|---|" + "---|" * len(out["table9"]["poor"])]
+    for sc, rows in out["table9"].items():
+        lines.append(f"| {sc} | " + " | ".join(f"{r['p_multi']:.2f} / {r['paper']:.2f}" for r in rows) + " |")
     lines += ["", "## Scheduler time at large n (MixedScaling; paper: C++ on a Ryzen 5 4600H, one batch at a time)", "",
               "| n | GPU, all instances (ms) | GPU per instance (us) | paper per instance (ms) |", "|---|---|---|---|"]
     for n, r in out["large_n"].items():
