@@ -71,8 +71,11 @@ enum {
   FAR_EXHAUSTIVE = 16u,   /* run Alg. 1 on every family member (disable the exact lower-bound skip) */
   FAR_NONEMPTY_ALT = 32u, /* reading variant (R16): Alg. 2's alternative I^a must
                              already hold a task (default: any same-size node, P:524 literally) */
-  FAR_NO_SEAM_MOVES = 64u /* far_concat_streams: reversal + seam offset only, no seam move/swap
+  FAR_NO_SEAM_MOVES = 64u,/* far_concat_streams: reversal + seam offset only, no seam move/swap
                              (Table 7's p_rev) */
+  FAR_GROW_TIES = 128u    /* reading variant (R2): phase 1 grows every task tied for the
+                             longest time in one step, as the formula of P:349 (default: one task,
+                             the lowest index) */
 };
 
 typedef struct {

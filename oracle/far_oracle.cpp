@@ -130,7 +130,7 @@ int load_problem(int profile, const int32_t* costs, const int32_t* times, int n,
 // ---------------------------------------------------------------------------
 // Phase 1: Turek family of allocations.  Allocations hold size VALUES.
 // ---------------------------------------------------------------------------
-std::vector<std::vector<int>> allocation_family(const Problem& P) {
+std::vector<std::vector<int>> allocation_family(const Problem& P, bool grow_ties) {
   const Model& m = P.m;
   std::vector<std::vector<int>> fam;
   if (P.n == 0) return fam;
@@ -148,11 +148,9 @@ std::vector<std::vector<int>> allocation_family(const Problem& P) {
   fam.push_back(a);
   // a^{k+1} from a^k: grow the longest task (ties -> lowest index, Q2)
   // to argmin_{s > a_j} s * t_j(s) (ties -> smallest s, Q3); stop when it cannot grow (Q4).
-  for (;;) {
-    int j = 0;
-    for (int i = 1; i < P.n; ++i)
-      if (P.time(i, a[i]) > P.time(j, a[j])) j = i;
-    if (a[j] == m.sizes.back()) break;
+  // Variant ORC_GROW_TIES (the formula of P:349 literally): every task whose time equals the
+  // maximum grows in the same step; the family ends when one of them cannot grow.
+  auto next_size = [&](int j) {
     int best = -1;
     i64 bw = 0;
     for (int s : m.sizes) {
@@ -160,7 +158,25 @@ std::vector<std::vector<int>> allocation_family(const Problem& P) {
       i64 w = (i64)s * P.time(j, s);
       if (best < 0 || w < bw) { best = s; bw = w; }
     }
-    a[j] = best;
+    return best;
+  };
+  for (;;) {
+    int j = 0;
+    for (int i = 1; i < P.n; ++i)
+      if (P.time(i, a[i]) > P.time(j, a[j])) j = i;
+    if (!grow_ties) {
+      if (a[j] == m.sizes.back()) break;
+      a[j] = next_size(j);
+    } else {
+      const i64 h = P.time(j, a[j]);
+      bool stuck = false;
+      for (int i = 0; i < P.n; ++i) stuck |= (P.time(i, a[i]) == h && a[i] == m.sizes.back());
+      if (stuck) break;
+      std::vector<int> grow;
+      for (int i = 0; i < P.n; ++i)
+        if (P.time(i, a[i]) == h) grow.push_back(i);
+      for (int i : grow) a[i] = next_size(i);
+    }
     fam.push_back(a);
   }
   return fam;
@@ -813,10 +829,14 @@ int orc_partitions(int profile, int32_t* out, int32_t* counts, int maxparts, int
 }
 
 int orc_family(int profile, const int32_t* times, int n, int32_t* out, int maxK) {
+  return orc_family_flags(profile, times, n, 0u, out, maxK);
+}
+
+int orc_family_flags(int profile, const int32_t* times, int n, uint32_t flags, int32_t* out, int maxK) {
   Problem P;
   int rc = load_problem(profile, nullptr, times, n, true, P);
   if (rc) return rc;
-  auto fam = allocation_family(P);
+  auto fam = allocation_family(P, (flags & ORC_GROW_TIES) != 0);
   for (size_t k = 0; k < fam.size() && (int)k < maxK; ++k)
     for (int i = 0; i < n; ++i) out[k * n + i] = fam[k][i];
   return (int)fam.size();
@@ -845,7 +865,7 @@ int orc_far(int profile, const int32_t* costs, const int32_t* times, int n, int3
   if (rc) return rc;
   orc_result r{};
   // Phase 1 + phase 2 on every member; k* = argmin (makespan_k, k)  (Q13)
-  auto fam = allocation_family(P);
+  auto fam = allocation_family(P, (flags & ORC_GROW_TIES) != 0);
   r.family_size = (int)fam.size();
   Sched best;
   int kbest = -1;
@@ -1070,7 +1090,7 @@ extern "C" int orc_stream(int profile, const int32_t* costs, const int32_t* time
     if (rc) return rc;
     const Problem& P = Pb[k];
     orc_result r{};
-    auto fam = allocation_family(P);
+    auto fam = allocation_family(P, (flags & ORC_GROW_TIES) != 0);
     r.family_size = (int)fam.size();
     Sched best;
     int kbest = -1;

@@ -35,7 +35,10 @@ typedef struct {
 /* ORC_NONEMPTY_ALT: reading variant -- Alg. 2's alternative I^a
  * must hold at least one task (default: any same-size node, P:524 literally). */
 /* ORC_NO_SEAM_MOVES: concatenation with reversal and seam offset only (Table 7's p_rev). */
-enum { ORC_NO_REFINE = 1u, ORC_NO_GUARD = 2u, ORC_ZERO_RECONFIG = 4u, ORC_NONEMPTY_ALT = 32u, ORC_NO_SEAM_MOVES = 64u };
+/* ORC_GROW_TIES: reading variant: phase 1 grows every task tied for the
+ * longest time in one step, as the formula of P:349 does (default: the lowest index only). */
+enum { ORC_NO_REFINE = 1u, ORC_NO_GUARD = 2u, ORC_ZERO_RECONFIG = 4u, ORC_NONEMPTY_ALT = 32u, ORC_NO_SEAM_MOVES = 64u,
+       ORC_GROW_TIES = 128u };
 
 int orc_num_sizes(int profile);
 int orc_num_nodes(int profile);
@@ -47,6 +50,7 @@ int orc_nodes(int profile, int32_t *lo, int32_t *hi, int32_t *parent);
 int orc_partitions(int profile, int32_t *out, int32_t *counts, int maxparts, int maxinst);
 /* Phase 1 family: out[k][n] = size VALUES; returns K. */
 int orc_family(int profile, const int32_t *times, int n, int32_t *out, int maxK);
+int orc_family_flags(int profile, const int32_t *times, int n, uint32_t flags, int32_t *out, int maxK);
 /* Alg. 1 on one allocation (size VALUES).  ev may be NULL. */
 int orc_schedule_allocation(int profile, const int32_t *costs, const int32_t *times, int n,
                             const int32_t *alloc, orc_slot *slots, orc_event *ev, int32_t *nev,

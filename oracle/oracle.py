@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "liboracle.so")
 SOURCES = ["far_oracle.cpp"]
 
 PROFILES = {"A30": 0, "A100": 1, "H100": 2}
-NO_REFINE, NO_GUARD, ZERO_RECONFIG, NONEMPTY_ALT, NO_SEAM_MOVES = 1, 2, 4, 32, 64
+NO_REFINE, NO_GUARD, ZERO_RECONFIG, NONEMPTY_ALT, NO_SEAM_MOVES, GROW_TIES = 1, 2, 4, 32, 64, 128
 
 
 def build(force: bool = False) -> str:
@@ -126,13 +126,13 @@ def partitions(profile):
     return [[tuple(map(int, out[j, q])) for q in range(cnt[j])] for j in range(k)]
 
 
-def family(profile, times):
+def family(profile, times, flags=0):
     t = _times(times)
     n = t.shape[0]
     nc = lib().orc_num_sizes(pid(profile))
     maxK = 1 + n * (nc - 1) + 1
     out = np.zeros((maxK, n), np.int32)
-    K = lib().orc_family(pid(profile), _ptr(t), n, _ptr(out), maxK)
+    K = lib().orc_family_flags(pid(profile), _ptr(t), n, C.c_uint32(flags), _ptr(out), maxK)
     if K < 0:
         raise OracleError(K)
     return out[:K].copy()

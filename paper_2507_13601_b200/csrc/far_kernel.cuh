@@ -952,7 +952,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   // the first terminal element (max size) on top, i.e. at T* = the largest terminal key, so
   // the growth steps are exactly the non-terminal chain elements with key >= T*, in that order.
   // (growth-step ranks live in lstate: PIPE_PREP sizes it by kcap, the fused layout holds 160)
-  mono = __all_sync(FULL, mono && small && (PIPE == PIPE_PREP || P.kcap <= 160));
+  mono = __all_sync(FULL, mono && small && (PIPE == PIPE_PREP || P.kcap <= 160) && !(P.flags & FAR_GROW_TIES));
   tstar = __reduce_max_sync(FULL, tstar);
   if (mono) {
     int2* G = lent;  // temporary (filled in H3): {key, task | from << 10 | to << 13 | pos << 16}
@@ -1088,6 +1088,49 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         lbs[K - 1] = (int)((W + (unsigned)(S - 1)) / (unsigned)S);
       }
       const int cj = cur[jj];
+      if (P.flags & FAR_GROW_TIES) {
+        // variant (the formula of P:349): every task tied for the longest time grows in this
+        // step; the family ends when one of them is already at the largest size
+        bool stuck = false;
+        for (int j = lane; j < n; j += 32) stuck |= cur[j] == NC - 1 && T[j * NC + cur[j]] == hmax;
+        if (__any_sync(FULL, stuck)) break;
+        if (K >= P.kcap) {
+          if (lane == 0) {
+            atomicOr(P.ovf + (inst >> 5), 1u << (inst & 31));
+            atomicAdd(P.ovf_count, 1ull);
+            if (PIPE == PIPE_PREP) P.ws_meta[inst * 16 + WS_FLAG] = 1;
+          }
+          return;
+        }
+        unsigned long long dcp = 0, dent = 0;
+        unsigned dW = 0;
+        __syncwarp();
+        for (int j = lane; j < n; j += 32) {
+          const int c = cur[j];
+          if (T[j * NC + c] != hmax) continue;
+          const unsigned nx = (unsigned)su[j] | ((unsigned)bestnode[j] << 8);
+          const int b = (int)((nx >> (3 * c)) & 7u);
+          dcp += (1ull << (11 * b)) - (1ull << (11 * c));
+          dent += 1ull << (11 * b);
+          dW += (unsigned)size_of<NC>(b) * (unsigned)T[j * NC + b] - (unsigned)size_of<NC>(c) * (unsigned)T[j * NC + c];
+          cur[j] = (uint8_t)b;
+          ivl[j * NC + c] = (IV)((ivl[j * NC + c] & IM) | ((uint32_t)K << IB));
+          ivl[j * NC + b] = (IV)((uint32_t)K | (IM << IB));
+          if (small && PIPE != PIPE_PREP) ck[j] = ((unsigned)T[j * NC + b] << 10) | (unsigned)(1023 - j);
+        }
+        cp += (unsigned long long)warp_sum_ll((long long)dcp);
+        entp += (unsigned long long)warp_sum_ll((long long)dent);
+        W += __reduce_add_sync(FULL, dW);
+        if (lane == 0) cnts[K] = cp;
+        __syncwarp();
+        if (small) {
+          lk = 0;
+          for (int j = lane; j < n; j += 32)
+            lk = max(lk, PIPE == PIPE_PREP ? (((unsigned)T[j * NC + cur[j]] << 10) | (unsigned)(1023 - j)) : ck[j]);
+        }
+        ++K;
+        continue;
+      }
       if (cj == NC - 1) break;
       if (K >= P.kcap) {  // family larger than this layout holds: defer to the overflow pass
         if (lane == 0) {

@@ -30,7 +30,7 @@ def run_gpu(torch_dev, profile, costs, tab, **kw):
 
 
 def check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=0, max_iterations=100, ppm=0, full=True):
-    oflags = flags & (O.NO_REFINE | O.NO_GUARD | O.ZERO_RECONFIG | O.NONEMPTY_ALT)
+    oflags = flags & (O.NO_REFINE | O.NO_GUARD | O.ZERO_RECONFIG | O.NONEMPTY_ALT | O.GROW_TIES)
     oms, ores = O.far_many(profile, costs, tab, max_iterations=max_iterations, min_improvement_ppm=ppm, flags=oflags)
     bad = np.nonzero(ms != oms)[0]
     assert len(bad) == 0, f"makespan mismatch at {bad[:10]}: gpu {ms[bad[:5]]} oracle {oms[bad[:5]]}"
@@ -132,6 +132,25 @@ def test_finish_paths_agree(O, torch_dev, monkeypatch, switch, wname, gen):
     for flags in (0, far.NO_GUARD, far.NONEMPTY_ALT):
         ms, slots, res = run_gpu(torch_dev, profile, costs, tab, flags=flags)
         check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=flags)
+
+
+@pytest.mark.parametrize("profile,gen", [("A30", "ties"), ("A100", "ties"), ("A100", "monoties"), ("H100", "mixed")])
+def test_grow_ties_variant(O, torch_dev, profile, gen):
+    # the NEXT-3 reading variant FAR_GROW_TIES (phase 1 grows all tied longest tasks)
+    # against the oracle, and non-vacuous on tie-heavy inputs
+    costs = inputs.reconfig_costs(profile)
+    if gen == "ties":
+        tab = inputs.small_ties(profile, 20, 300, 44)
+    elif gen == "monoties":
+        tab = inputs.monotone_ties(profile, 24, 300, 45)
+    else:
+        tab = inputs.synthetic(profile, 32, 300, 46)
+    ms0, _, r0 = run_gpu(torch_dev, profile, costs, tab)
+    for flags in (far.GROW_TIES, far.GROW_TIES | far.EXHAUSTIVE, far.GROW_TIES | far.NONEMPTY_ALT):
+        ms1, s1, r1 = run_gpu(torch_dev, profile, costs, tab, flags=flags)
+        check_against_oracle(O, profile, costs, tab, ms1, s1, r1, flags=flags)
+    if gen != "mixed":
+        assert (r0["family_size"] != r1["family_size"]).any()
 
 
 @pytest.mark.parametrize("profile,n", [("A100", 10), ("A100", 16), ("A30", 8)])

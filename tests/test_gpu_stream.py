@@ -96,3 +96,10 @@ def test_concat_and_multibatch_statistics(O, torch_dev, scaling, times):
     long = inputs.synthetic("A100", 12, 101, 301, scaling=scaling, times=times)
     assert stats.multi_batch_p(F, torch.from_numpy(long).to(dev)) == O.multi_batch_p("A100", costs, long)
     F.sync()
+
+
+def test_grow_ties_streams(O, torch_dev):
+    tab = inputs.small_ties("A100", 12, 6 * 5, 78).reshape(6, 5, 12, -1)
+    costs = inputs.reconfig_costs("A100")
+    out = run_streams(torch_dev, "A100", costs, tab, flags=far.GROW_TIES)
+    check(O, "A100", costs, tab, out, flags=O.GROW_TIES)

@@ -231,3 +231,16 @@ def test_input_errors(O):
         O.far("A30", None, np.full((3, 3), 1 << 29, np.int32))     # makespan bound
     with pytest.raises(O.OracleError):
         O.far(7, None, np.ones((1, 3), np.int32))                  # unknown profile
+
+
+def test_grow_ties_variant_family(O):
+    # two identical perfectly-scaling A30 tasks (work 4 at every size): the literal reading (R2)
+    # grows one tied task per step (lowest index), the P:349 formula (FAR_GROW_TIES) grows both
+    t = np.array([[4, 2, 1], [4, 2, 1]], dtype=np.int32)
+    assert O.family("A30", t).tolist() == [[1, 1], [2, 1], [2, 2], [4, 2], [4, 4]]
+    assert O.family("A30", t, flags=O.GROW_TIES).tolist() == [[1, 1], [2, 2], [4, 4]]
+    # a tie, then a single longest task that ends the family at the largest size (hand-traced):
+    # works of task 2 are 3, 6, 12 -> a^1 = 1; it grows 1 -> 2 -> 4 with t = 3 throughout
+    u = np.array([[4, 2, 1], [4, 2, 1], [3, 3, 3]], dtype=np.int32)
+    assert O.family("A30", u, flags=O.GROW_TIES).tolist() == [[1, 1, 1], [2, 2, 1], [2, 2, 2], [2, 2, 4]]
+    assert O.family("A30", u).tolist() == [[1, 1, 1], [2, 1, 1], [2, 2, 1], [2, 2, 2], [2, 2, 4]]
