@@ -135,7 +135,8 @@ def secondary(far, torch, dev, reps=5):
     st = torch.cuda.current_stream(dev)
 
     def timed(fn):
-        fn()
+        for _ in range(3):  # warm-up (first-call and clock ramp effects)
+            fn()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)

@@ -75,7 +75,13 @@ enum {
                              (Table 7's p_rev) */
   FAR_GROW_TIES = 128u    /* reading variant (R2): phase 1 grows every task tied for the
                              longest time in one step, as the formula of P:349 (default: one task,
-                             the lowest index) */
+                             the lowest index) */,
+  FAR_BEST_IMPROVEMENT = 256u /* reading variant (R30; the north star's "evaluates every task
+                             move and swap, recomputes the makespan and takes an argmin"): phase 3
+                             scores every move to a same-size node and every swap pair on two
+                             same-size nodes by (max slice end, #slices at it) and applies the
+                             argmin while it improves; evals = candidates scored (default: Alg. 2,
+                             P:495-560, FAR_NONEMPTY_ALT ignored) */
 };
 
 typedef struct {

@@ -20,6 +20,7 @@
 #include <functional>
 #include <limits>
 #include <queue>
+#include <tuple>
 #include <vector>
 
 namespace {
@@ -429,6 +430,95 @@ RefineStats refine(const Problem& P, Sched& S, int max_iterations, int ppm, bool
   return st;
 }
 
+// ---------------------------------------------------------------------------
+// Variant ORC_BEST_IMPROVEMENT (R30; SURVEY.md §0 discrepancy 2 / NEXT-3): the
+// north star's literal phase 3, "evaluates every task move and swap, recomputes the
+// makespan and takes an argmin".  Same node lists, same time model as Alg. 2 (slice ends
+// from the phase-2 finishes, moved by +-t; reconfiguration recomputed by the
+// line-26 replay), same neighbourhood shape as Alg. 2 (a task only changes to a node of
+// the same size, |I^a| = |I|), but every candidate is scored:
+//   moves : task T on node I to every node u != I with |u| = |I|
+//   swaps : every task pair k < j on two different nodes of the same size
+//   score : (w', c') = (max slice end after the operation, #slices reaching w')
+//   pick  : argmin (w', c', kind [move 0 < swap 1], first id, second id) where (first,
+//           second) = (T, u) for a move and (k, j) for a swap
+// The best candidate is applied if (w', c') < (w, c) lexicographically, else the search
+// stops (a strict decrease of a well-founded key: it terminates).  evals = number of
+// candidates scored.  max_iterations and min-improvement (ppm on w) as in Alg. 2.
+// ---------------------------------------------------------------------------
+RefineStats refine_best(const Problem& P, Sched& S, int max_iterations, int ppm) {
+  const Model& m = P.m;
+  const int N = (int)m.node.size();
+  RefineStats st;
+  std::vector<i64> send(m.slices, 0);
+  for (int j = 0; j < P.n; ++j) {
+    const TreeNode& nd = m.node[S.node[j]];
+    for (int s = nd.lo; s < nd.hi; ++s) send[s] = std::max(send[s], S.start[j] + dur(P, S, j));
+  }
+  // score of the slice ends after moving d ticks of work from node a to node b
+  auto score = [&](int a, int b, i64 d) {
+    std::vector<i64> e = send;
+    for (int s = m.node[a].lo; s < m.node[a].hi; ++s) e[s] -= d;
+    for (int s = m.node[b].lo; s < m.node[b].hi; ++s) e[s] += d;
+    const i64 w = *std::max_element(e.begin(), e.end());
+    const i64 c = std::count(e.begin(), e.end(), w);
+    return std::make_pair(w, c);
+  };
+  auto cur = score(0, 0, 0);
+  while (st.iterations < max_iterations) {
+    st.iterations++;
+    const i64 omega_prev = cur.first;
+    // (w', c', kind, first, second)
+    std::tuple<i64, i64, int, int, int> best{std::numeric_limits<i64>::max(), 0, 0, 0, 0};
+    bool found = false;
+    for (int T = 0; T < P.n; ++T) {  // every move
+      const int I = S.node[T];
+      for (int u = 0; u < N; ++u) {
+        if (u == I || m.node[u].size() != m.node[I].size()) continue;
+        st.evals++;
+        auto sc = score(I, u, dur(P, S, T));
+        std::tuple<i64, i64, int, int, int> key{sc.first, sc.second, 0, T, u};
+        if (!found || key < best) { best = key; found = true; }
+      }
+    }
+    for (int k = 0; k < P.n; ++k)  // every swap
+      for (int j = k + 1; j < P.n; ++j) {
+        const int a = S.node[k], b = S.node[j];
+        if (a == b || m.node[a].size() != m.node[b].size()) continue;
+        st.evals++;
+        auto sc = score(a, b, dur(P, S, k) - dur(P, S, j));
+        std::tuple<i64, i64, int, int, int> key{sc.first, sc.second, 1, k, j};
+        if (!found || key < best) { best = key; found = true; }
+      }
+    if (!found || std::make_pair(std::get<0>(best), std::get<1>(best)) >= cur) break;
+    const int kind = std::get<2>(best), x = std::get<3>(best), y = std::get<4>(best);
+    if (kind == 0) {  // move x to node y
+      const int I = S.node[x];
+      S.list[I].erase(std::find(S.list[I].begin(), S.list[I].end(), x));
+      S.node[x] = y;
+      insert_ordered(P, S, S.list[y], x);
+      for (int s = m.node[I].lo; s < m.node[I].hi; ++s) send[s] -= dur(P, S, x);
+      for (int s = m.node[y].lo; s < m.node[y].hi; ++s) send[s] += dur(P, S, x);
+      st.moves++;
+    } else {  // swap x (node a) with y (node b)
+      const int a = S.node[x], b = S.node[y];
+      const i64 d = dur(P, S, x) - dur(P, S, y);
+      S.list[a].erase(std::find(S.list[a].begin(), S.list[a].end(), x));
+      S.list[b].erase(std::find(S.list[b].begin(), S.list[b].end(), y));
+      S.node[x] = b;
+      S.node[y] = a;
+      insert_ordered(P, S, S.list[b], x);
+      insert_ordered(P, S, S.list[a], y);
+      for (int s = m.node[a].lo; s < m.node[a].hi; ++s) send[s] -= d;
+      for (int s = m.node[b].lo; s < m.node[b].hi; ++s) send[s] += d;
+      st.swaps++;
+    }
+    cur = score(0, 0, 0);
+    if (ppm > 0 && (omega_prev - cur.first) * 1000000 < (i64)ppm * omega_prev) break;
+  }
+  return st;
+}
+
 void write_slots(const Sched& S, int n, orc_slot* slots) {
   if (!slots) return;
   for (int j = 0; j < n; ++j) slots[j] = {S.node[j], S.size_used[j], S.start[j]};
@@ -444,7 +534,8 @@ void write_events(const Sched& S, orc_event* ev, int32_t* nev) {
 Sched refine_and_replay(const Problem& P, const Sched& S2, i64 ms2, int max_it, int ppm, uint32_t flags,
                         orc_result* res) {
   Sched S = S2;
-  RefineStats st = refine(P, S, max_it, ppm, (flags & ORC_NONEMPTY_ALT) != 0);
+  RefineStats st = (flags & ORC_BEST_IMPROVEMENT) ? refine_best(P, S, max_it, ppm)
+                                                  : refine(P, S, max_it, ppm, (flags & ORC_NONEMPTY_ALT) != 0);
   Sched R = replay(P, S);
   res->moves = st.moves;
   res->swaps = st.swaps;

@@ -37,8 +37,11 @@ typedef struct {
 /* ORC_NO_SEAM_MOVES: concatenation with reversal and seam offset only (Table 7's p_rev). */
 /* ORC_GROW_TIES: reading variant: phase 1 grows every task tied for the
  * longest time in one step, as the formula of P:349 does (default: the lowest index only). */
+/* ORC_BEST_IMPROVEMENT: reading variant (SURVEY.md §0 discrepancy 2 / NEXT-3, R30): phase 3
+ * scores every same-size move and every swap pair by the resulting (makespan, #critical slices) and
+ * applies the argmin while it improves (default: Alg. 2). */
 enum { ORC_NO_REFINE = 1u, ORC_NO_GUARD = 2u, ORC_ZERO_RECONFIG = 4u, ORC_NONEMPTY_ALT = 32u, ORC_NO_SEAM_MOVES = 64u,
-       ORC_GROW_TIES = 128u };
+       ORC_GROW_TIES = 128u, ORC_BEST_IMPROVEMENT = 256u };
 
 int orc_num_sizes(int profile);
 int orc_num_nodes(int profile);

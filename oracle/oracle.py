@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "liboracle.so")
 SOURCES = ["far_oracle.cpp"]
 
 PROFILES = {"A30": 0, "A100": 1, "H100": 2}
-NO_REFINE, NO_GUARD, ZERO_RECONFIG, NONEMPTY_ALT, NO_SEAM_MOVES, GROW_TIES = 1, 2, 4, 32, 64, 128
+NO_REFINE, NO_GUARD, ZERO_RECONFIG, NONEMPTY_ALT, NO_SEAM_MOVES, GROW_TIES, BEST_IMPROVEMENT = 1, 2, 4, 32, 64, 128, 256
 
 
 def build(force: bool = False) -> str:

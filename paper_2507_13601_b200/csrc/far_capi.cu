@@ -337,11 +337,12 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     CK(cudaGetLastError());
     ctx->launches += 3;
     if ((st = t_mark(ctx, tset, stream, FAR_STAGE_WINNER))) return st;
-    // ---- K5: H6-H7, one thread per instance (n <= 256), else one warp per instance
+    // ---- K5: H6-H7, one thread per instance (n <= 256), else (and for FAR_BEST_IMPROVEMENT) one warp
+    //      per instance
     P.counter = ctx->d_counter + slot + 5;
     const LRow LR = make_lrow(P.n, NN);
     const int tbl = (int)std::min<int64_t>(128, (int64_t)ctx->smem_max / LR.bytes / 32 * 32);
-    if (P.n <= 256 && tbl >= 32 && !getenv("FAR_DEBUG_WARP_FINISH")) {
+    if (P.n <= 256 && tbl >= 32 && !(P.flags & FAR_BEST_IMPROVEMENT) && !getenv("FAR_DEBUG_WARP_FINISH")) {
       const void* lfn = a30 ? (const void*)far_finish_lane_kernel<3> : (const void*)far_finish_lane_kernel<5>;
       const size_t lsm = (size_t)tbl * LR.bytes;
       int per_sm = 0;

@@ -512,6 +512,143 @@ __device__ void refine_warp(int n, const int* D, uint16_t* nlist, int* ncnt, int
   }
 }
 
+// ---------------------------------------------------------------------------
+// Phase-3 variant FAR_BEST_IMPROVEMENT (R30; the north star's literal "evaluates
+// every task move and swap, recomputes the makespan and takes an argmin"): each iteration
+// scores EVERY move of a task to another node of the same size and EVERY swap of two tasks
+// on different same-size nodes by (w', c') = (max slice end after the operation, #slices at
+// w') under Alg. 2's time model (slice ends +-t), and applies the argmin of
+// (w', c', kind, first, second) if it lowers (w, c).  Same-size nodes form contiguous id
+// ranges in both trees (A30: {1,2}, {3..6}; A100: {3,4,5}, {6..12}).  Candidates are spread
+// over the lanes: moves as a flat (list entry, alternative) index, swaps as (entry, lanes
+// over the entries of later nodes of the class); one 64-bit packed key per lane, REDUX
+// min.  evals = candidates scored (closed form per class: m(|V|-1) + (m^2 - sum cnt^2)/2).
+// ---------------------------------------------------------------------------
+template <int NC>
+__device__ __noinline__ void refine_best_warp(int n, const int* D, uint16_t* nlist, int* ncnt, int* send,
+                                              const uint32_t* ninfo, int max_it, int ppm, int lane, int& moves,
+                                              int& swaps, int& iters, long long& evals) {
+  constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
+  // classes of >= 2 same-size nodes: contiguous id runs [cf, cl)
+  int cf[2] = {0, 0}, cl[2] = {0, 0}, ncls = 0;
+  for (int v = 1; v <= NN; ++v) {
+    const bool brk = v == NN || nd_sz(ninfo[v]) != nd_sz(ninfo[v - 1]);
+    if (brk) {
+      int f = v - 1;
+      while (f > 0 && nd_sz(ninfo[f - 1]) == nd_sz(ninfo[v - 1])) --f;
+      if (v - f >= 2 && ncls < 2) { cf[ncls] = f; cl[ncls] = v; ++ncls; }
+    }
+  }
+  auto mask_of = [&](int v) {
+    const uint32_t w = ninfo[v];
+    return ((1u << nd_sz(w)) - 1u) << nd_lo(w);
+  };
+  moves = swaps = iters = 0;
+  evals = 0;
+  while (iters < max_it) {
+    ++iters;
+    int e[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) e[s] = send[s];
+    // score of moving d ticks of work from the slices of mask mf to those of mask mt
+    auto score = [&](unsigned mf, unsigned mt, int d) {
+      int w = -1, c = 0;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int x = e[s] + (((mt >> s) & 1u) ? d : 0) - (((mf >> s) & 1u) ? d : 0);
+        if (x > w) { w = x; c = 1; } else if (x == w) { ++c; }
+      }
+      return ((unsigned long long)(unsigned)w << 24) | ((unsigned long long)c << 21);
+    };
+    const unsigned long long cur = score(0u, 0u, 0);
+    const int omega_prev = (int)(cur >> 24);
+    unsigned long long best = ~0ull;
+    for (int g = 0; g < ncls; ++g) {
+      const int f = cf[g], V = cl[g] - f, A = V - 1;
+      int m = 0, sq = 0;
+      for (int v = f; v < f + V; ++v) { m += ncnt[v]; sq += ncnt[v] * ncnt[v]; }
+      evals += (long long)m * A + (long long)(m * m - sq) / 2;
+      // entry index -> (node, position): scan of the class's node counts
+      auto locate = [&](int idx, int& v, int& pos) {
+        v = f;
+        pos = idx;
+        while (pos >= ncnt[v]) { pos -= ncnt[v]; ++v; }
+      };
+      // moves: flat p = idx * A + r, r-th alternative of the entry's node
+      for (int p = lane; p < m * A; p += 32) {
+        const int idx = p / A, r = p - idx * A;
+        int v, pos;
+        locate(idx, v, pos);
+        const int u = f + r + (f + r >= v ? 1 : 0);
+        const int T = nlist[v * n + pos];
+        const unsigned long long k = score(mask_of(v), mask_of(u), D[T]) | ((unsigned long long)T << 10) | (unsigned)u;
+        best = k < best ? k : best;
+      }
+      // swaps: entry x (uniform) with every entry y of a later node of the class
+      int vx = f, px = 0;
+      for (int x = 0; x < m; ++x) {
+        while (px >= ncnt[vx]) { px -= ncnt[vx]; ++vx; }
+        const int tx = nlist[vx * n + px];
+        ++px;
+        int before = 0;
+        for (int v = f; v <= vx; ++v) before += ncnt[v];
+        for (int y = before + lane; y < m; y += 32) {
+          int vy, py;
+          locate(y, vy, py);
+          const int ty = nlist[vy * n + py];
+          const int k = min(tx, ty), j = max(tx, ty);
+          const int a = tx < ty ? vx : vy, b = tx < ty ? vy : vx;
+          const unsigned long long key =
+              score(mask_of(a), mask_of(b), D[k] - D[j]) | (1ull << 20) | ((unsigned long long)k << 10) | (unsigned)j;
+          best = key < best ? key : best;
+        }
+      }
+    }
+    // warp argmin of the packed keys
+    const unsigned hi = __reduce_min_sync(FULL, (unsigned)(best >> 32));
+    const unsigned lo = __reduce_min_sync(FULL, (unsigned)(best >> 32) == hi ? (unsigned)best : ~0u);
+    best = ((unsigned long long)hi << 32) | lo;
+    if ((best >> 21) >= (cur >> 21)) break;  // no candidate lowers (w, c)
+    const int x = (int)((best >> 10) & 1023), y = (int)(best & 1023);
+    int from, to, tk0, tk1 = -1, d;
+    if (!((best >> 20) & 1)) {  // move x to node y
+      tk0 = x;
+      to = y;
+      from = -1;
+      for (int v = 0; v < NN; ++v)
+        for (int q = lane; q < ncnt[v]; q += 32)
+          if (nlist[v * n + q] == x) from = v;
+      from = __reduce_max_sync(FULL, from);
+      d = D[x];
+      ++moves;
+    } else {  // swap x (its node) with y (its node)
+      int vx = -1, vy = -1;
+      for (int v = 0; v < NN; ++v)
+        for (int q = lane; q < ncnt[v]; q += 32) {
+          const int t = nlist[v * n + q];
+          if (t == x) vx = v;
+          if (t == y) vy = v;
+        }
+      from = __reduce_max_sync(FULL, vx);
+      to = __reduce_max_sync(FULL, vy);
+      tk0 = x;
+      tk1 = y;
+      d = D[x] - D[y];
+      ++swaps;
+    }
+    // the oracle's order: remove both, then insert each into the other node's list
+    list_remove<NC>(nlist + from * n, &ncnt[from], tk0, lane);
+    if (tk1 >= 0) list_remove<NC>(nlist + to * n, &ncnt[to], tk1, lane);
+    list_insert<NC>(nlist + to * n, &ncnt[to], tk0, D, lane);
+    if (tk1 >= 0) list_insert<NC>(nlist + from * n, &ncnt[from], tk1, D, lane);
+    const unsigned mf = mask_of(from), mt = mask_of(to);
+    if (lane < S) send[lane] += (((mt >> lane) & 1u) ? d : 0) - (((mf >> lane) & 1u) ? d : 0);
+    __syncwarp();
+    int om = __reduce_max_sync(FULL, lane < S ? send[lane] : 0);
+    if (ppm > 0 && (long long)(omega_prev - om) * 1000000LL < (long long)ppm * omega_prev) break;
+  }
+}
+
 // Build per-node ordered lists of member k from the per-size LPT lists: sizes in
 // decreasing order so the A100 {S0..S3} node lists its size-4 tasks before its size-3
 // tasks.  Lanes over list entries; __match_any_sync ranks entries per node.
@@ -636,8 +773,11 @@ __device__ __noinline__ void solve_local(const KParams& P, int64_t inst, unsigne
       int* D = (int*)(scratch + ((2 * NN * n + 3) & ~3));  // durations at the tasks' sizes
       for (int j = lane; j < n; j += 32) D[j] = T[j * NC + su[j]];
       __syncwarp();
-      refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, (P.flags & FAR_NONEMPTY_ALT) != 0, lane, mv,
-                      sw, it, ev);
+      if (P.flags & FAR_BEST_IMPROVEMENT)
+        refine_best_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
+      else
+        refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, (P.flags & FAR_NONEMPTY_ALT) != 0, lane, mv,
+                        sw, it, ev);
       R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
       const int msR = replay_warp<NC>(n, D, nlist, ncnt, nsum, life, start, bestnode, ninfo, cr, de, lane);
       if (!(P.flags & FAR_NO_GUARD) && msR > ms2) {
@@ -723,8 +863,11 @@ __device__ void finish_core(const KParams& P, int64_t inst, uint16_t* nlist, int
       __syncwarp();
       int mv, sw, it;
       long long ev;
-      refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, (P.flags & FAR_NONEMPTY_ALT) != 0, lane, mv,
-                      sw, it, ev);
+      if (P.flags & FAR_BEST_IMPROVEMENT)
+        refine_best_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
+      else
+        refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, (P.flags & FAR_NONEMPTY_ALT) != 0, lane, mv,
+                        sw, it, ev);
       R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
     }
     if (!need_replay) break;

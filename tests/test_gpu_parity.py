@@ -30,7 +30,7 @@ def run_gpu(torch_dev, profile, costs, tab, **kw):
 
 
 def check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=0, max_iterations=100, ppm=0, full=True):
-    oflags = flags & (O.NO_REFINE | O.NO_GUARD | O.ZERO_RECONFIG | O.NONEMPTY_ALT | O.GROW_TIES)
+    oflags = flags & (O.NO_REFINE | O.NO_GUARD | O.ZERO_RECONFIG | O.NONEMPTY_ALT | O.GROW_TIES | O.BEST_IMPROVEMENT)
     oms, ores = O.far_many(profile, costs, tab, max_iterations=max_iterations, min_improvement_ppm=ppm, flags=oflags)
     bad = np.nonzero(ms != oms)[0]
     assert len(bad) == 0, f"makespan mismatch at {bad[:10]}: gpu {ms[bad[:5]]} oracle {oms[bad[:5]]}"
@@ -297,3 +297,58 @@ def test_local_search_rejects_bad_schedules(torch_dev):
         F.local_search(t, bad)
     assert e.value.status == 1
     F.sync()
+
+
+@pytest.mark.parametrize("profile,gen,n", [("A30", "mixed", 8), ("A30", "ties", 20), ("A100", "mixed", 16),
+                                           ("A100", "ties", 24), ("A100", "uniform", 33), ("H100", "mixed", 70),
+                                           ("A100", "mixed", 128), ("A100", "mixed", 300)])
+def test_best_improvement_variant(O, torch_dev, profile, gen, n):
+    """The NEXT-3 variant FAR_BEST_IMPROVEMENT (R30: every same-size move and every swap
+    pair scored by the resulting makespan, argmin applied) against the oracle, bit-exact on every
+    field incl. evals; non-vacuous (it changes some refinements)."""
+    costs = inputs.reconfig_costs(profile)
+    count = 40 if n >= 128 else 200
+    if gen == "ties":
+        tab = inputs.small_ties(profile, n, count, 61)
+    elif gen == "uniform":
+        tab = inputs.uniform_random(profile, n, count, 62)
+    else:
+        tab = inputs.synthetic(profile, n, count, 63 + n)
+    BI = far.BEST_IMPROVEMENT
+    _, _, r0 = run_gpu(torch_dev, profile, costs, tab)
+    for flags in (BI, BI | far.NO_GUARD, BI | far.ZERO_RECONFIG, BI | far.EXHAUSTIVE | far.GROW_TIES):
+        ms, slots, res = run_gpu(torch_dev, profile, costs, tab, flags=flags)
+        check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=flags, full=n <= 128)
+        if flags == BI:
+            assert (res["evals"] != r0["evals"]).any()
+    # max_iterations = 1 and a min-improvement threshold
+    for kw in ({"max_iterations": 1}, {"min_improvement_ppm": 20000}):
+        ms, slots, res = run_gpu(torch_dev, profile, costs, tab, flags=BI, **kw)
+        check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=BI,
+                             max_iterations=kw.get("max_iterations", 100), ppm=kw.get("min_improvement_ppm", 0),
+                             full=False)
+
+
+def test_best_improvement_local_search(O, torch_dev):
+    """far_local_search with FAR_BEST_IMPROVEMENT on phase-2 schedules == the oracle's refine."""
+    for profile in ("A30", "A100"):
+        costs = inputs.reconfig_costs(profile)
+        F = far.Far(profile, costs)
+        for t in inputs.synthetic(profile, 18, 40, 57):
+            s, r = F.schedule_batch(t)
+            s2, r2 = F.local_search(t, s, makespan_phase2=int(r["makespan"]), flags=far.BEST_IMPROVEMENT)
+            oslots = np.zeros(len(s), O.SLOT_DT)
+            oslots["node"], oslots["size_used"], oslots["start"] = s["node"], s["size_used"], s["start"]
+            q = O.refine(profile, costs, t, oslots, int(r["makespan"]), flags=O.BEST_IMPROVEMENT)
+            for k in ("makespan", "moves", "swaps", "evals", "iterations", "reverted"):
+                assert r2[k] == q["result"][k], k
+            assert (s2["node"] == q["slots"]["node"]).all() and (s2["start"] == q["slots"]["start"]).all()
+
+
+@pytest.mark.parametrize("profile", ["A30", "A100"])
+def test_best_improvement_fused_path(O, torch_dev, monkeypatch, profile):
+    monkeypatch.setenv("FAR_FUSED_PHASE2", "1")
+    costs = inputs.reconfig_costs(profile)
+    tab = inputs.synthetic(profile, 40, 100, 64)
+    ms, slots, res = run_gpu(torch_dev, profile, costs, tab, flags=far.BEST_IMPROVEMENT)
+    check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=far.BEST_IMPROVEMENT)

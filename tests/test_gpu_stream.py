@@ -103,3 +103,10 @@ def test_grow_ties_streams(O, torch_dev):
     costs = inputs.reconfig_costs("A100")
     out = run_streams(torch_dev, "A100", costs, tab, flags=far.GROW_TIES)
     check(O, "A100", costs, tab, out, flags=O.GROW_TIES)
+
+
+def test_best_improvement_streams(O, torch_dev):
+    tab = inputs.synthetic("A30", 16, 4 * 6, 79).reshape(4, 6, 16, -1)
+    costs = inputs.reconfig_costs("A30")
+    out = run_streams(torch_dev, "A30", costs, tab, flags=far.BEST_IMPROVEMENT)
+    check(O, "A30", costs, tab, out, flags=O.BEST_IMPROVEMENT)

@@ -244,3 +244,76 @@ def test_grow_ties_variant_family(O):
     u = np.array([[4, 2, 1], [4, 2, 1], [3, 3, 3]], dtype=np.int32)
     assert O.family("A30", u, flags=O.GROW_TIES).tolist() == [[1, 1, 1], [2, 2, 1], [2, 2, 2], [2, 2, 4]]
     assert O.family("A30", u).tolist() == [[1, 1, 1], [2, 1, 1], [2, 2, 1], [2, 2, 2], [2, 2, 4]]
+
+
+# ----------------------------------------------------------------- best-improvement variant (R30)
+@pytest.mark.parametrize("case", GOLD["refine_best"], ids=lambda c: c["example"])
+def test_best_improvement_examples(O, case):
+    """Hand traces of the north star's literal phase 3 (R30) on the two Alg. 2 examples."""
+    base = next(c for c in GOLD["refine"] if case["example"] in c["cite"])
+    t = _t(base["times"], base["profile"])
+    p2 = O.schedule_allocation(base["profile"], None, t, base["alloc"])
+    r = O.refine(base["profile"], None, t, p2["slots"], p2["makespan"], flags=O.BEST_IMPROVEMENT)
+    res = r["result"]
+    got = (res["makespan"], res["moves"], res["swaps"], res["evals"], res["iterations"])
+    assert got == (case["makespan"], case["moves"], case["swaps"], case["evals"], case["iterations"])
+    assert r["slots"]["node"].tolist() == case["nodes"]
+    assert O.validate(base["profile"], None, t, r["slots"], r["events"]) == 0
+
+
+def _laminar_key(lo, hi, S, load):
+    """(makespan, #slices reaching it) of a zero-reconfiguration node assignment by the laminar
+    closed form (slice end = sum of the loads of the nodes covering the slice),
+    computed from scratch -- independent of the oracle's incremental +-t slice ends."""
+    e = [sum(load[v] for v in range(len(lo)) if lo[v] <= s < hi[v]) for s in range(S)]
+    w = max(e)
+    return w, e.count(w)
+
+
+@pytest.mark.parametrize("profile", ["A30", "A100"])
+def test_best_improvement_local_optimum(O, profile):
+    """With zero reconfiguration the variant ends in a local optimum of its neighbourhood: no
+    same-size move and no swap lowers (makespan, #critical slices), and the replayed makespan is
+    the closed-form one."""
+    lo, hi, _ = O.nodes(profile)
+    lo, hi = lo.tolist(), hi.tolist()
+    S = SLICES[profile]
+    tabs = [inputs.synthetic(profile, n, 6, 90 + n) for n in (3, 9, 17)] + [inputs.small_ties(profile, 8, 6, 5)]
+    for tab in tabs:
+        for t in tab:
+            r = O.far(profile, None, t, max_iterations=10000, flags=O.BEST_IMPROVEMENT)
+            res, sl = r["result"], r["slots"]
+            assert res["reverted"] == 0 and res["iterations"] < 10000
+            node = sl["node"].tolist()
+            dur = [int(t[j][inputs.SIZES[profile].index(int(sl["size_used"][j]))]) for j in range(len(t))]
+
+            def key(nd):
+                load = [0] * len(lo)
+                for j, v in enumerate(nd):
+                    load[v] += dur[j]
+                return _laminar_key(lo, hi, S, load)
+
+            cur = key(node)
+            assert cur[0] == res["makespan"]
+            size = [hi[v] - lo[v] for v in range(len(lo))]
+            for j in range(len(t)):
+                for u in range(len(lo)):
+                    if u != node[j] and size[u] == size[node[j]]:
+                        nd = list(node); nd[j] = u
+                        assert key(nd) >= cur
+                for k in range(j + 1, len(t)):
+                    if node[k] != node[j] and size[node[k]] == size[node[j]]:
+                        nd = list(node); nd[j], nd[k] = node[k], node[j]
+                        assert key(nd) >= cur
+
+
+@pytest.mark.parametrize("profile", ["A30", "A100"])
+def test_best_improvement_feasible_and_guarded(O, profile):
+    costs = inputs.reconfig_costs(profile)
+    for t in list(inputs.synthetic(profile, 14, 12, 31)) + list(inputs.uniform_random(profile, 10, 8, 3)):
+        r = O.far(profile, costs, t, flags=O.BEST_IMPROVEMENT)
+        res = r["result"]
+        assert O.validate(profile, costs, t, r["slots"], r["events"]) == 0
+        assert res["makespan"] <= res["makespan_phase2"]
+        z = O.far(profile, costs, t, max_iterations=0, flags=O.BEST_IMPROVEMENT)
+        assert z["result"]["makespan"] == res["makespan_phase2"] and z["result"]["evals"] == 0
