@@ -166,6 +166,22 @@ def secondary(far, torch, dev, reps=5):
     out["M3_events_instances_per_s"] = d.shape[0] / (msv / 1000.0)
     out["M3_validate_instances_per_s"] = d.shape[0] / (ms_chk / 1000.0)
     out["M3_infeasible_outputs"] = int((viol != 0).sum().item())
+    # phase-3 variant FAR_BEST_IMPROVEMENT (R30: the north star's literal neighbourhood,
+    # every same-size move and every swap pair scored) on the first 100k M5 instances
+    w = inputs.WORKLOADS["M5"]
+    d = torch.from_numpy(w.table(count=100_000, parallel=True)).to(dev)
+    F = far.Far(w.profile, w.costs())
+    bufs = (torch.empty(d.shape[0], dtype=torch.int32, device=dev),
+            torch.empty((d.shape[0], w.n, 8), dtype=torch.uint8, device=dev),
+            torch.empty((d.shape[0], 56), dtype=torch.uint8, device=dev))
+    ms = timed(lambda: F.solve_many(d, out=bufs, stream=st, flags=far.BEST_IMPROVEMENT))
+    F.sync()
+    r = far.results_np(bufs[2])
+    out["M5_best_improvement_100k_ms"] = ms
+    out["M5_best_improvement_instances_per_s"] = d.shape[0] / (ms / 1000.0)
+    out["M5_best_improvement_evals_per_s"] = float(r["evals"].sum()) / (ms / 1000.0)
+    out["M5_best_improvement_moves_swaps_per_instance"] = float((r["moves"] + r["swaps"]).mean())
+    del d, bufs
     for prof in ("A30", "A100"):
         w = inputs.WORKLOADS["M4_" + prof]
         S = 1024

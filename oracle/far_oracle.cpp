@@ -48,7 +48,34 @@ struct Model {
   bool ok = false;
 };
 
+// Multi-target FAR: "as many trees as GPUs, and initially, there is one
+// node for the root of each tree to start repartitioning on".  profile = base | (g << 8) with
+// g in [2, 8] GPUs: tree t's node v gets id t*NN + v and slices t*S + [lo, hi); every other
+// step of FAR is unchanged (one heap, one reconfig_end, R31).
+Model make_model_one(int profile);
 Model make_model(int profile) {
+  const int g = profile >> 8;
+  Model one = make_model_one(profile & 255);
+  if (g == 0 || g == 1 || !one.ok) return one;
+  Model m;
+  if (g < 0 || g > 8) return m;
+  m.sizes = one.sizes;
+  m.slices = g * one.slices;
+  const int NN = (int)one.node.size();
+  for (int t = 0; t < g; ++t)
+    for (const TreeNode& v : one.node) {
+      TreeNode w = v;
+      w.lo += t * one.slices;
+      w.hi += t * one.slices;
+      for (int& c : w.children) c += t * NN;
+      w.parent = v.parent < 0 ? -1 : v.parent + t * NN;
+      m.node.push_back(w);
+    }
+  m.ok = true;
+  return m;
+}
+
+Model make_model_one(int profile) {
   Model m;
   if (profile == 0) {  // A30: 4 -> {2,2} -> 4 leaves
     m.slices = 4;
@@ -243,7 +270,8 @@ Sched run_event_loop(const Problem& P, const std::vector<int>* alloc,
   using Key = std::pair<i64, int>;  // (end, lo) ; node recovered from lo via map below
   auto cmp = [](const std::pair<Key, int>& a, const std::pair<Key, int>& b) { return a.first > b.first; };
   std::priority_queue<std::pair<Key, int>, std::vector<std::pair<Key, int>>, decltype(cmp)> heap(cmp);
-  heap.push({{0, m.node[0].lo}, 0});  // root, R.end = 0, R.tasks = []
+  for (int v = 0; v < N; ++v)  // the root (of every tree), R.end = 0, R.tasks = []
+    if (m.node[v].parent < 0) heap.push({{0, m.node[v].lo}, v});
 
   while (!heap.empty()) {  // line 5
     const int v = heap.top().second;  // line 6: pop the first instance to end
@@ -360,7 +388,7 @@ RefineStats refine(const Problem& P, Sched& S, int max_iterations, int ppm, bool
     while (!Q.empty()) {  // line 6
       const int I = Q.front();  // line 7
       Q.pop_front();
-      if (I == 0) { stop = true; break; }  // lines 8-10: root opened
+      if (m.node[I].parent < 0) { stop = true; break; }  // lines 8-10: root opened
       // line 11: alternative I^a, same size, != I, minimum end (ties -> lower slice, Q16)
       int A = -1;
       i64 eA = 0;
@@ -761,7 +789,7 @@ SeamStats seam_refine(const Problem& P, Sched& S, const StreamState& st, int max
     while (!Q.empty() && !accepted) {
       const int I = Q.front();
       Q.pop_front();
-      if (I == 0) { stop = true; break; }
+      if (m.node[I].parent < 0) { stop = true; break; }
       auto slack = [&](int u) {
         i64 g = std::numeric_limits<i64>::max();
         for (int s = m.node[u].lo; s < m.node[u].hi; ++s) g = std::min(g, cur.gap[s]);

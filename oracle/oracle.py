@@ -108,7 +108,11 @@ def _check(rc):
 
 
 def pid(profile):
-    return PROFILES[profile] if isinstance(profile, str) else int(profile)
+    """'A30' / 'A100' / 'H100', or 'A30x2' ... 'A100x8' for multi-target FAR (g trees)."""
+    if isinstance(profile, str):
+        base, _, g = profile.partition("x")
+        return PROFILES[base] | (int(g) << 8 if g else 0)
+    return int(profile)
 
 
 def nodes(profile):

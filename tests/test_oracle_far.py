@@ -317,3 +317,69 @@ def test_best_improvement_feasible_and_guarded(O, profile):
         assert res["makespan"] <= res["makespan_phase2"]
         z = O.far(profile, costs, t, max_iterations=0, flags=O.BEST_IMPROVEMENT)
         assert z["result"]["makespan"] == res["makespan_phase2"] and z["result"]["evals"] == 0
+
+
+# ----------------------------------------------------------------- multi-target FAR (NEXT-2, R31)
+def test_multi_gpu_forest_model(O):
+    """as many trees as GPUs; node ids t*NN + v, slices t*S + [lo, hi)."""
+    for base, S, NN in (("A30", 4, 7), ("A100", 7, 13)):
+        lo1, hi1, par1 = O.nodes(base)
+        for g in (2, 3, 8):
+            lo, hi, par = O.nodes(f"{base}x{g}")
+            assert len(lo) == g * NN and (par < 0).sum() == g
+            for t in range(g):
+                assert (lo[t * NN:(t + 1) * NN] == lo1 + t * S).all() and (hi[t * NN:(t + 1) * NN] == hi1 + t * S).all()
+    with pytest.raises(O.OracleError):
+        O.far("A30x9", None, np.ones((2, 3), np.int32))
+
+
+def test_multi_gpu_hand_trace(O):
+    """Hand trace (A30 x 2, zero reconfiguration): two perfectly scaling tasks t = (4, 2, 1).
+    Family [1,1] [2,1] [2,2] [4,2] [4,4]; Alg. 1 with both roots at time 0 gives 4, 4, 2, 2, 1
+    (member [4,4] runs each task on its own GPU's root); one A30 gives 4, 4, 2, 3, 2."""
+    t = np.array([[4, 2, 1], [4, 2, 1]], np.int32)
+    fam = O.family("A30x2", t)
+    assert fam.tolist() == [[1, 1], [2, 1], [2, 2], [4, 2], [4, 4]]
+    assert [O.schedule_allocation("A30x2", None, t, a)["makespan"] for a in fam] == [4, 4, 2, 2, 1]
+    assert [O.schedule_allocation("A30", None, t, a)["makespan"] for a in fam] == [4, 4, 2, 3, 2]
+    r = O.far("A30x2", None, t)
+    assert r["result"]["makespan"] == 1 and r["result"]["alloc_index"] == 4
+    assert r["slots"]["node"].tolist() == [0, 7]
+
+
+@pytest.mark.parametrize("g", [2, 3])
+def test_multi_gpu_a30_bounds(O, g):
+    """with g A30s the A30 argument gives, per allocation, 4g*w <= W + (4g-1)*h (zero
+    reconfiguration), hence w_FAR <= (8g-1)/(4g) * w*; and LB <= w* <= w_FAR."""
+    prof = f"A30x{g}"
+    for t in list(inputs.synthetic("A30", 12, 40, 300 + g)) + list(inputs.small_ties("A30", 9, 30, 7)):
+        for a in O.family(prof, t):
+            ms = O.schedule_allocation(prof, None, t, a)["makespan"]
+            W = sum(int(s) * int(t[i][inputs.SIZES["A30"].index(int(s))]) for i, s in enumerate(a))
+            h = max(int(t[i][inputs.SIZES["A30"].index(int(s))]) for i, s in enumerate(a))
+            assert 4 * g * ms <= W + (4 * g - 1) * h
+    for t in inputs.synthetic("A30", 5, 12, 310 + g):
+        opt = O.bruteforce(prof, t)
+        w = O.far(prof, None, t)["result"]["makespan"]
+        Wm, H = O.lower_bound(prof, t)
+        assert opt <= w and 4 * g * w <= (8 * g - 1) * opt
+        assert 4 * g * opt >= Wm and opt >= H
+
+
+@pytest.mark.parametrize("prof", ["A30x2", "A100x2", "A100x3", "H100x4"])
+def test_multi_gpu_feasible_and_bounded(O, prof):
+    base, g = prof.split("x")
+    g = int(g)
+    costs = inputs.reconfig_costs(base)
+    for t in list(inputs.synthetic(base, 20, 12, 320 + g)) + list(inputs.uniform_random(base, 9, 8, 5)):
+        for flags in (0, O.BEST_IMPROVEMENT):
+            r = O.far(prof, costs, t, flags=flags)
+            res = r["result"]
+            assert O.validate(prof, costs, t, r["slots"], r["events"]) == 0
+            assert res["makespan"] <= res["makespan_phase2"]
+            W, H = O.lower_bound(prof, t)
+            assert g * SLICES[base] * res["makespan"] >= W and res["makespan"] >= H
+    # n <= g identical property-1 tasks, zero reconfiguration: each gets a whole GPU (the last
+    # family member), so w_FAR = t(largest size) = the lower bound max_i min_s t_i(s)
+    t = np.tile(inputs.synthetic(base, 1, 1, 9)[0], (g, 1))
+    assert O.far(prof, None, t)["result"]["makespan"] == int(t[0].min())
