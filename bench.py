@@ -182,6 +182,17 @@ def secondary(far, torch, dev, reps=5):
     out["M5_best_improvement_evals_per_s"] = float(r["evals"].sum()) / (ms / 1000.0)
     out["M5_best_improvement_moves_swaps_per_instance"] = float((r["moves"] + r["swaps"]).mean())
     del d, bufs
+    # multi-target FAR (NEXT-2): 100k batches of 64 tasks scheduled on 4 A100s at once
+    F = far.Far("A100x4", inputs.reconfig_costs("A100"))
+    d = torch.from_numpy(inputs.synthetic_parallel("A100", 64, 100_000, 6)).to(dev)
+    fb = (torch.empty(d.shape[0], dtype=torch.int32, device=dev),
+          torch.empty((d.shape[0], 64, 8), dtype=torch.uint8, device=dev),
+          torch.empty((d.shape[0], 56), dtype=torch.uint8, device=dev))
+    ms = timed(lambda: F.solve_many(d, out=fb, stream=st))
+    F.sync()
+    out["A100x4_n64_100k_ms"] = ms
+    out["A100x4_n64_instances_per_s"] = d.shape[0] / (ms / 1000.0)
+    del d, fb
     for prof in ("A30", "A100"):
         w = inputs.WORKLOADS["M4_" + prof]
         S = 1024

@@ -121,12 +121,25 @@ typedef struct {
  * {create[], destroy[]} in the profile's size order, each >= 0 (all zero = no
  * reconfiguration cost).  Unknown profile -> FAR_E_UNSUPPORTED_PROFILE. */
 far_status far_create(far_profile profile, const int32_t *reconfig_cost, far_ctx **out);
+/* Multi-target FAR (R31): one context schedules each instance on num_gpus
+ * MIG GPUs of the profile at once -- "as many trees as GPUs, and initially, there is one node for
+ * the root of each tree to start repartitioning on"; one Alg. 1 heap and one reconfig_end over the
+ * forest, Alg. 2 alternatives among the same-size nodes of every tree.  Node ids: tree t's node v
+ * is t*NN + v (NN = 7 A30, 13 A100/H100), its slices t*S + [lo, hi).  num_gpus in [1, 8]
+ * (else FAR_E_INVALID_ARG); far_create(p, c, out) == far_create_multi(p, 1, c, out).  With
+ * num_gpus > 1: far_solve_many / far_solve_many_host / far_schedule_batch / far_local_search /
+ * far_lower_bounds take n <= 256 (else FAR_E_TOO_LARGE) and every flag except
+ * FAR_BEST_IMPROVEMENT (FAR_E_INVALID_ARG); far_concat_streams, far_schedule_events and
+ * far_validate_schedules return FAR_E_UNSUPPORTED_PROFILE. */
+far_status far_create_multi(far_profile profile, int32_t num_gpus, const int32_t *reconfig_cost, far_ctx **out);
+int32_t far_num_gpus(const far_ctx *ctx);
 void far_destroy(far_ctx *ctx);
 int32_t far_num_sizes(const far_ctx *ctx);
 const int32_t *far_sizes(const far_ctx *ctx);          /* nsizes values, host memory owned by ctx */
-int32_t far_num_nodes(const far_ctx *ctx);
-int32_t far_num_slices(const far_ctx *ctx);
-/* Tree node table (host): lo[v], hi[v] slice interval [lo,hi), parent[v] (-1 for the root). */
+int32_t far_num_nodes(const far_ctx *ctx);   /* all trees of the context */
+int32_t far_num_slices(const far_ctx *ctx);  /* all trees of the context */
+/* Tree node table (host): lo[v], hi[v] slice interval [lo,hi), parent[v] (-1 for a root);
+ * far_num_nodes(ctx) entries. */
 far_status far_node_table(const far_ctx *ctx, int32_t *lo, int32_t *hi, int32_t *parent);
 const char *far_last_error(const far_ctx *ctx);
 /* Wait for all work queued by this ctx; returns FAR_E_BAD_TIME if any instance failed

@@ -50,7 +50,7 @@ SLOT_DT = np.dtype([("node", "<i4"), ("size_used", "<i4"), ("start", "<i8")])
 RESULT_DT = np.dtype([("makespan", "<i8"), ("makespan_phase2", "<i8"), ("evals", "<i8"), ("events", "<i8"),
                       ("alloc_index", "<i4"), ("family_size", "<i4"), ("moves", "<i4"), ("swaps", "<i4"),
                       ("reverted", "<i4"), ("iterations", "<i4")])
-MAX_EVENTS = 64
+MAX_EVENTS = 256  # >= 2 events per node of the largest forest (8 x 13 nodes)
 
 
 class OracleError(RuntimeError):

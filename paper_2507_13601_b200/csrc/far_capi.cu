@@ -14,6 +14,7 @@
 #include "far_pipeline.cuh"
 #include "far_finish_lane.cuh"
 #include "far_check.cuh"
+#include "far_forest.cuh"
 
 using namespace farb;
 
@@ -22,7 +23,10 @@ constexpr int RING = 256;
 }  // namespace
 
 struct far_ctx {
-  int profile = 0, nc = 0, ns = 0, nn = 0;
+  int profile = 0, nc = 0, ns = 0, nn = 0;  // ns, nn: one tree
+  int gpus = 1;                             // multi-target FAR: g trees
+  uint2 fnodes[FMAXNN];                     // forest node table (far_forest.cuh encoding)
+  uint2* d_fnodes = nullptr;
   int32_t sizes[8] = {0};
   int cr[8] = {0}, de[8] = {0};
   std::string err;
@@ -109,6 +113,12 @@ static far_status ensure_device(far_ctx* ctx) {
     for (const void* f : cf) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   }
   for (const void* f : fns) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
+  CK(cudaFuncSetAttribute((const void*)far_forest_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
+  CK(cudaFuncSetAttribute((const void*)far_forest_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
+  if (ctx->gpus > 1) {
+    CK(cudaMalloc(&ctx->d_fnodes, sizeof(uint2) * FMAXNN));
+    CK(cudaMemcpy(ctx->d_fnodes, ctx->fnodes, sizeof(uint2) * ctx->nn * ctx->gpus, cudaMemcpyHostToDevice));
+  }
   ctx->inited = true;
   return FAR_OK;
 }
@@ -225,8 +235,32 @@ static far_status launch_warp_kernel(far_ctx* ctx, KParams& P, cudaStream_t stre
 //   then the fused kernel with the full layout over the instances K1 deferred (overflow mask).
 //   FAR_FUSED_PHASE2 (debug env) forces the fused warp-per-instance kernel for everything.
 //   MODE_LOCAL: the fused kernel (phase 3 only).
+static far_status launch_forest(far_ctx* ctx, KParams& P, cudaStream_t stream) {
+  if (P.flags & FAR_BEST_IMPROVEMENT)
+    return fail(ctx, FAR_E_INVALID_ARG, "FAR_BEST_IMPROVEMENT: single-GPU trees only");
+  P.errflag = ctx->d_errflag;
+  FParams F;
+  F.P = P;
+  F.nodes = ctx->d_fnodes;
+  F.NNF = ctx->nn * ctx->gpus;
+  F.SF = ctx->ns * ctx->gpus;
+  const FLay L = make_flay(P.n, ctx->nc, F.NNF, F.SF);
+  const int warps = (int)std::max<int64_t>(1, std::min<int64_t>(4, ctx->smem_max / L.bytes));
+  const void* fn = ctx->nc == 3 ? (const void*)far_forest_kernel<3> : (const void*)far_forest_kernel<5>;
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, warps * 32, (size_t)warps * L.bytes));
+  if (per_sm < 1) return fail(ctx, FAR_E_TOO_LARGE, "forest layout does not fit in shared memory");
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((P.I + warps - 1) / warps, (int64_t)ctx->sms * per_sm));
+  if (ctx->nc == 3) far_forest_kernel<3><<<grid, warps * 32, (size_t)warps * L.bytes, stream>>>(F);
+  else far_forest_kernel<5><<<grid, warps * 32, (size_t)warps * L.bytes, stream>>>(F);
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  return FAR_OK;
+}
+
 static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
   if (P.I <= 0) return FAR_OK;
+  if (ctx->gpus > 1) return launch_forest(ctx, P, stream);
   const bool a30 = ctx->nc == 3;
   const int NC = ctx->nc, NN = ctx->nn;
   const int kmax = 1 + P.n * (NC - 1);
@@ -404,21 +438,40 @@ static void fill_params(far_ctx* ctx, const far_opts* o, KParams& P) {
     const int szi = nd_szi(ctx->nc == 3 ? Tree<3>::node[v] : Tree<5>::node[v]);
     P.rsum += P.cr[szi] + P.de[szi];
   }
+  P.rsum *= ctx->gpus;  // every tree of a multi-target forest
 }
 
 extern "C" {
 
 far_status far_create(far_profile profile, const int32_t* reconfig_cost, far_ctx** out) {
+  return far_create_multi(profile, 1, reconfig_cost, out);
+}
+
+far_status far_create_multi(far_profile profile, int32_t num_gpus, const int32_t* reconfig_cost, far_ctx** out) {
   if (!out) return FAR_E_INVALID_ARG;
   *out = nullptr;
   if (profile != FAR_A30 && profile != FAR_A100 && profile != FAR_H100) return FAR_E_UNSUPPORTED_PROFILE;
+  if (num_gpus < 1 || num_gpus > FMAXG) return FAR_E_INVALID_ARG;
   far_ctx* c = new far_ctx();
   c->profile = profile;
+  c->gpus = num_gpus;
   if (profile == FAR_A30) {
     c->nc = 3; c->ns = Tree<3>::S; c->nn = Tree<3>::NN;
   } else {
     c->nc = 5; c->ns = Tree<5>::S; c->nn = Tree<5>::NN;
   }
+  // forest node table: tree t's node v -> id t*NN + v, slices t*S + [lo, hi)
+  for (int t = 0; t < num_gpus; ++t)
+    for (int v = 0; v < c->nn; ++v) {
+      const uint32_t w = c->nc == 3 ? Tree<3>::node[v] : Tree<5>::node[v];
+      auto id = [&](int u) { return u == LEAF ? FNONE : t * c->nn + u; };
+      const int par = nd_par(w) == ROOTP ? FNONE : t * c->nn + nd_par(w);
+      uint2 f;
+      f.x = (uint32_t)(nd_lo(w) + t * c->ns) | ((uint32_t)nd_sz(w) << 8) | ((uint32_t)nd_szi(w) << 12) |
+            ((uint32_t)nd_c0(w) << 16) | ((uint32_t)nd_c1(w) << 20);
+      f.y = (uint32_t)id(nd_ch1(w)) | ((uint32_t)id(nd_ch2(w)) << 8) | ((uint32_t)par << 16);
+      c->fnodes[t * c->nn + v] = f;
+    }
   for (int i = 0; i < c->nc; ++i) c->sizes[i] = c->nc == 3 ? size_of<3>(i) : size_of<5>(i);
   // Table 2 in 1 ms ticks
   static const int a30c[3] = {110, 120, 130}, a30d[3] = {100, 100, 100};
@@ -450,6 +503,7 @@ void far_destroy(far_ctx* ctx) {
     cudaDeviceSynchronize();
     cudaFree(ctx->d_counter);
     cudaFree(ctx->d_errflag);
+    if (ctx->d_fnodes) cudaFree(ctx->d_fnodes);
     for (int r = 0; r < 4; ++r)
       if (ctx->d_ovf[r]) cudaFree(ctx->d_ovf[r]);
     if (ctx->d_buf) cudaFree(ctx->d_buf);
@@ -467,8 +521,9 @@ void far_destroy(far_ctx* ctx) {
 
 int32_t far_num_sizes(const far_ctx* ctx) { return ctx ? ctx->nc : -1; }
 const int32_t* far_sizes(const far_ctx* ctx) { return ctx ? ctx->sizes : nullptr; }
-int32_t far_num_nodes(const far_ctx* ctx) { return ctx ? ctx->nn : -1; }
-int32_t far_num_slices(const far_ctx* ctx) { return ctx ? ctx->ns : -1; }
+int32_t far_num_nodes(const far_ctx* ctx) { return ctx ? ctx->nn * ctx->gpus : -1; }
+int32_t far_num_slices(const far_ctx* ctx) { return ctx ? ctx->ns * ctx->gpus : -1; }
+int32_t far_num_gpus(const far_ctx* ctx) { return ctx ? ctx->gpus : -1; }
 const char* far_last_error(const far_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 far_status far_stage_timing(far_ctx* ctx, int32_t enable) {
@@ -493,11 +548,12 @@ int64_t far_launch_count(const far_ctx* ctx) { return ctx ? ctx->launches : -1; 
 
 far_status far_node_table(const far_ctx* ctx, int32_t* lo, int32_t* hi, int32_t* parent) {
   if (!ctx || !lo || !hi || !parent) return FAR_E_INVALID_ARG;
-  for (int v = 0; v < ctx->nn; ++v) {
-    const uint32_t w = ctx->nc == 3 ? Tree<3>::node[v] : Tree<5>::node[v];
-    lo[v] = nd_lo(w);
-    hi[v] = nd_lo(w) + nd_sz(w);
-    parent[v] = nd_par(w) == ROOTP ? -1 : nd_par(w);
+  for (int v = 0; v < ctx->nn * ctx->gpus; ++v) {
+    const uint2 f = ctx->fnodes[v];
+    lo[v] = (int)(f.x & 255u);
+    hi[v] = lo[v] + (int)((f.x >> 8) & 15u);
+    const int par = (int)((f.y >> 16) & 255u);
+    parent[v] = par == FNONE ? -1 : par;
   }
   return FAR_OK;
 }
@@ -524,6 +580,7 @@ far_status far_solve_many(far_ctx* ctx, const int32_t* d_times, int64_t I, int32
   if (!ctx) return FAR_E_INVALID_ARG;
   if (I < 0 || n < 0) return fail(ctx, FAR_E_INVALID_ARG, "negative I or n");
   if (n > MAXN) return fail(ctx, FAR_E_TOO_LARGE, "n > 1024");
+  if (ctx->gpus > 1 && n > FMAXN) return fail(ctx, FAR_E_TOO_LARGE, "multi-GPU forest: n > 256");
   if (I > 0 && (!d_makespan || (n > 0 && !d_times))) return fail(ctx, FAR_E_INVALID_ARG, "null device pointer");
   far_status st = check_opts(ctx, opts);
   if (st) return st;
@@ -546,6 +603,7 @@ static far_status one_instance(far_ctx* ctx, const int32_t* times, int32_t n, co
   if (!ctx) return FAR_E_INVALID_ARG;
   if (n < 0) return fail(ctx, FAR_E_INVALID_ARG, "negative n");
   if (n > MAXN) return fail(ctx, FAR_E_TOO_LARGE, "n > 1024");
+  if (ctx->gpus > 1 && n > FMAXN) return fail(ctx, FAR_E_TOO_LARGE, "multi-GPU forest: n > 256");
   if ((n > 0 && (!times || !sched)) || !res) return fail(ctx, FAR_E_INVALID_ARG, "null host pointer");
   far_status st = check_opts(ctx, opts);
   if (st) return st;
@@ -603,6 +661,7 @@ far_status far_solve_many_host(far_ctx* ctx, const int32_t* h_times, int64_t I, 
   if (!ctx) return FAR_E_INVALID_ARG;
   if (I < 0 || n < 0) return fail(ctx, FAR_E_INVALID_ARG, "negative I or n");
   if (n > MAXN) return fail(ctx, FAR_E_TOO_LARGE, "n > 1024");
+  if (ctx->gpus > 1 && n > FMAXN) return fail(ctx, FAR_E_TOO_LARGE, "multi-GPU forest: n > 256");
   if (I > 0 && (!h_makespan || (n > 0 && !h_times))) return fail(ctx, FAR_E_INVALID_ARG, "null host pointer");
   far_status st = check_opts(ctx, opts);
   if (st) return st;
@@ -659,6 +718,7 @@ extern "C" far_status far_concat_streams(far_ctx* ctx, const int32_t* d_times, i
                                          far_task_slot* d_sched, far_result* d_batch_res, int32_t* d_seam,
                                          void* cuda_stream) {
   if (!ctx) return FAR_E_INVALID_ARG;
+  if (ctx->gpus > 1) return fail(ctx, FAR_E_UNSUPPORTED_PROFILE, "streams: single-GPU trees only");
   if (S < 0 || B < 0 || n < 0) return fail(ctx, FAR_E_INVALID_ARG, "negative S, B or n");
   if (n > MAXN) return fail(ctx, FAR_E_TOO_LARGE, "n > 1024");
   if (S > 0 && B > 0 && (!d_stream_makespan || !d_offsets || (n > 0 && !d_times)))
@@ -755,6 +815,7 @@ static far_status launch_check(far_ctx* ctx, CParams& Q, int64_t I, int n, bool 
 
 static far_status check_args(far_ctx* ctx, const int32_t* d_times, int64_t I, int32_t n, const far_task_slot* d_sched,
                              const far_opts* opts, CParams& Q) {
+  if (ctx->gpus > 1) return fail(ctx, FAR_E_UNSUPPORTED_PROFILE, "events / validator: single-GPU trees only");
   if (I < 0 || n < 0) return fail(ctx, FAR_E_INVALID_ARG, "negative I or n");
   if (n > MAXN) return fail(ctx, FAR_E_TOO_LARGE, "n > 1024");
   if (I > 0 && n > 0 && (!d_times || !d_sched)) return fail(ctx, FAR_E_INVALID_ARG, "null device pointer");

@@ -64,6 +64,8 @@ def lib():
         p, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
         sig = {
             "far_create": ([C.c_int, p, C.POINTER(p)], C.c_int),
+            "far_create_multi": ([C.c_int, i32, p, C.POINTER(p)], C.c_int),
+            "far_num_gpus": ([p], i32),
             "far_destroy": ([p], None),
             "far_num_sizes": ([p], i32),
             "far_sizes": ([p], C.POINTER(i32)),
@@ -106,15 +108,21 @@ def _opts(max_iterations=100, min_improvement_ppm=0, flags=0):
 class Far:
     """One far_ctx (a MIG profile + reconfiguration costs)."""
 
-    def __init__(self, profile="A100", reconfig_cost=None):
+    def __init__(self, profile="A100", reconfig_cost=None, gpus=1):
+        """profile 'A30' / 'A100' / 'H100'; gpus > 1 (or a profile 'A100x4') = multi-target FAR over
+        that many MIG GPUs (far_create_multi)."""
+        if isinstance(profile, str) and "x" in profile:
+            profile, g = profile.split("x")
+            gpus = int(g)
         self.profile = profile
+        self.gpus = gpus
         self._h = C.c_void_p()
         cost = None if reconfig_cost is None else np.ascontiguousarray(reconfig_cost, dtype=np.int32)
         self._cost = cost
-        rc = lib().far_create(PROFILES.get(profile, -1) if isinstance(profile, str) else int(profile),
-                              _np_ptr(cost), C.byref(self._h))
+        rc = lib().far_create_multi(PROFILES.get(profile, -1) if isinstance(profile, str) else int(profile), gpus,
+                                    _np_ptr(cost), C.byref(self._h))
         if rc:
-            raise FarError(rc, "far_create")
+            raise FarError(rc, "far_create_multi")
         self.nsizes = lib().far_num_sizes(self._h)
         self.sizes = [lib().far_sizes(self._h)[i] for i in range(self.nsizes)]
         self.nnodes = lib().far_num_nodes(self._h)

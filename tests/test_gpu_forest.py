@@ -1,0 +1,101 @@
+"""GPU parity of multi-target FAR (one tree per MIG GPU, all roots at
+time 0) -- far_create_multi + the forest kernel against the oracle's forest, bit-exact on every
+field and every task slot."""
+import numpy as np
+import pytest
+
+from paper_2507_13601_b200 import far, inputs
+from test_gpu_parity import check_against_oracle, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_dev():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch, torch.device("cuda:0")
+
+
+@pytest.mark.parametrize("prof,n", [("A30x2", 8), ("A30x2", 33), ("A30x3", 20), ("A100x2", 16), ("A100x2", 64),
+                                    ("H100x4", 40), ("A100x8", 128), ("A30x8", 256), ("A100x2", 0),
+                                    ("A100x3", 1), ("A30x2", 7)])
+def test_forest_bitexact(O, torch_dev, prof, n):
+    base = prof.split("x")[0]
+    costs = inputs.reconfig_costs(base)
+    count = 60 if n >= 128 else 200
+    tab = inputs.synthetic(base, n, count, 500 + n)
+    for flags in (0, far.EXHAUSTIVE, far.NO_GUARD, far.ZERO_RECONFIG, far.NO_REFINE):
+        ms, slots, res = run_gpu(torch_dev, prof, costs, tab, flags=flags)
+        check_against_oracle(O, prof, costs, tab, ms, slots, res, flags=flags, full=n <= 64)
+
+
+@pytest.mark.parametrize("prof,gen", [("A30x2", "ties"), ("A100x2", "ties"), ("A100x2", "uniform"),
+                                      ("A100x4", "monoties")])
+def test_forest_ties_and_variants(O, torch_dev, prof, gen):
+    base = prof.split("x")[0]
+    costs = inputs.reconfig_costs(base)
+    n = 24
+    tab = {"ties": inputs.small_ties, "uniform": inputs.uniform_random,
+           "monoties": inputs.monotone_ties}[gen](base, n, 200, 41)
+    for flags in (0, far.NONEMPTY_ALT, far.GROW_TIES, far.GROW_TIES | far.EXHAUSTIVE):
+        ms, slots, res = run_gpu(torch_dev, prof, costs, tab, flags=flags)
+        check_against_oracle(O, prof, costs, tab, ms, slots, res, flags=flags)
+    for kw in ({"max_iterations": 1}, {"min_improvement_ppm": 30000}):
+        ms, slots, res = run_gpu(torch_dev, prof, costs, tab, **kw)
+        check_against_oracle(O, prof, costs, tab, ms, slots, res, max_iterations=kw.get("max_iterations", 100),
+                             ppm=kw.get("min_improvement_ppm", 0), full=False)
+
+
+def test_forest_more_gpus_help(O, torch_dev):
+    """Non-vacuous: on the same batches, more MIG GPUs give shorter FAR schedules on average, and
+    the g-GPU schedules differ from the single-GPU ones."""
+    tab = inputs.synthetic("A100", 32, 300, 77)
+    costs = inputs.reconfig_costs("A100")
+    m1 = run_gpu(torch_dev, "A100", costs, tab)[0]
+    m2 = run_gpu(torch_dev, "A100x2", costs, tab)[0]
+    m4 = run_gpu(torch_dev, "A100x4", costs, tab)[0]
+    assert m4.mean() < m2.mean() < m1.mean()
+
+
+def test_forest_host_paths(O, torch_dev):
+    for prof in ("A30x2", "A100x3"):
+        base = prof.split("x")[0]
+        costs = inputs.reconfig_costs(base)
+        F = far.Far(prof, costs)
+        assert F.gpus == int(prof.split("x")[1]) and F.nnodes == len(O.nodes(prof)[0])
+        lo, hi, par = F.node_table()
+        olo, ohi, opar = O.nodes(prof)
+        assert (lo == olo).all() and (hi == ohi).all() and (par == opar).all()
+        for t in inputs.synthetic(base, 19, 30, 58):
+            s, r = F.schedule_batch(t)
+            o = O.far(prof, costs, t, flags=O.NO_REFINE)
+            assert (s["node"] == o["slots"]["node"]).all() and (s["start"] == o["slots"]["start"]).all()
+            assert r["makespan"] == o["result"]["makespan"] and r["alloc_index"] == o["result"]["alloc_index"]
+            s2, r2 = F.local_search(t, s, makespan_phase2=int(r["makespan"]))
+            oslots = np.zeros(len(s), O.SLOT_DT)
+            oslots["node"], oslots["size_used"], oslots["start"] = s["node"], s["size_used"], s["start"]
+            q = O.refine(prof, costs, t, oslots, int(r["makespan"]))
+            for k in ("makespan", "moves", "swaps", "evals", "iterations", "reverted"):
+                assert r2[k] == q["result"][k], k
+            assert (s2["node"] == q["slots"]["node"]).all() and (s2["start"] == q["slots"]["start"]).all()
+        tab = np.ascontiguousarray(inputs.synthetic(base, 21, 500, 59))
+        ms_h, sd_h, rs_h = F.solve_many_host(tab)
+        oms, _ = O.far_many(prof, costs, tab)
+        assert (ms_h == oms).all()
+
+
+def test_forest_errors(torch_dev):
+    torch, dev = torch_dev
+    F = far.Far("A100x2")
+    d = torch.ones((2, 257, 5), dtype=torch.int32, device=dev)
+    with pytest.raises(far.FarError):
+        F.solve_many(d)
+    d = torch.ones((2, 8, 5), dtype=torch.int32, device=dev)
+    with pytest.raises(far.FarError):
+        F.solve_many(d, flags=far.BEST_IMPROVEMENT)
+    with pytest.raises(far.FarError):
+        F.concat_streams(d.reshape(1, 2, 8, 5))
+    with pytest.raises(far.FarError):
+        far.Far("A100x9")
