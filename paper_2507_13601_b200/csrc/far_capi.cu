@@ -671,8 +671,10 @@ far_status far_solve_many_host(far_ctx* ctx, const int32_t* h_times, int64_t I, 
   const size_t per_t = (size_t)n * ctx->nc * 4, per_s = want_sched ? (size_t)n * sizeof(far_task_slot) : 0;
   const size_t per_r = h_res ? sizeof(far_result) : 0, per_m = 4;
   const size_t per = per_t + per_s + per_r + per_m;
-  // chunk: ~48 MB of staging per stream
-  int64_t chunk = std::max<int64_t>(1, ((size_t)48 << 20) / std::max<size_t>(per, 1));
+  // chunk: ~192 MB of staging per stream (PCIe copies of large chunks run near the link rate)
+  size_t chunk_mb = 192;  // measured: 48 MB 61 ms, 96 MB 52 ms, 192 MB 50 ms, 384 MB 52 ms per 1M M5 instances
+  if (const char* e = getenv("FAR_HOST_CHUNK_MB")) chunk_mb = (size_t)std::max(1, std::min(4096, atoi(e)));  // experiments
+  int64_t chunk = std::max<int64_t>(1, (chunk_mb << 20) / std::max<size_t>(per, 1));
   chunk = std::min<int64_t>(chunk, I);
   auto a256 = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t bt = a256(chunk * per_t), bs = a256(chunk * per_s), br = a256(chunk * per_r), bm = a256(chunk * per_m);
