@@ -93,7 +93,7 @@ static far_status ensure_device(far_ctx* ctx) {
   // allow every kernel the full opt-in shared memory; each launch passes its own size
   int optin = 0;
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-  ctx->smem_max = optin - 1024;
+  ctx->smem_max = optin - 3072;  // minus the largest static shared memory of a kernel (2.4 KB)
   const void* fns[6] = {(const void*)far_solve_kernel<3, PIPE_NONE>, (const void*)far_solve_kernel<5, PIPE_NONE>,
                         (const void*)far_solve_kernel<3, PIPE_PREP>, (const void*)far_solve_kernel<5, PIPE_PREP>,
                         (const void*)far_stream_kernel<3>, (const void*)far_stream_kernel<5>};

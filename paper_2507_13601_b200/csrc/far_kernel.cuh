@@ -527,8 +527,15 @@ __device__ void refine_warp(int n, const int* D, uint16_t* nlist, int* ncnt, int
 template <int NC>
 __device__ __noinline__ void refine_best_warp(int n, const int* D, uint16_t* nlist, int* ncnt, int* send,
                                               const uint32_t* ninfo, int max_it, int ppm, int lane, int& moves,
-                                              int& swaps, int& iters, long long& evals) {
+                                              int& swaps, int& iters, long long& evals, uint16_t* flat) {
   constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
+  // per-warp tables of one class, rebuilt every iteration: (max, count) of the slice ends of each
+  // node and of the slices outside each node pair (the score of a transfer between two disjoint
+  // nodes a -> b of d ticks is max(out(a,b), M_a - d, M_b + d) with the counts of those reaching it)
+  __shared__ int2 s_pair[4][64];
+  __shared__ int2 s_node[4][8];
+  int2* pairt = s_pair[(threadIdx.x >> 5) & 3];
+  int2* nodet = s_node[(threadIdx.x >> 5) & 3];
   // classes of >= 2 same-size nodes: contiguous id runs [cf, cl)
   int cf[2] = {0, 0}, cl[2] = {0, 0}, ncls = 0;
   for (int v = 1; v <= NN; ++v) {
@@ -543,6 +550,13 @@ __device__ __noinline__ void refine_best_warp(int n, const int* D, uint16_t* nli
     const uint32_t w = ninfo[v];
     return ((1u << nd_sz(w)) - 1u) << nd_lo(w);
   };
+  auto score = [&](int ia, int ib, int d) {  // class-local node indices a (loses d), b (gains d)
+    const int2 o = pairt[ia * 8 + ib], na = nodet[ia], nb = nodet[ib];
+    const int x = na.x - d, y = nb.x + d;
+    const int w = max(o.x, max(x, y));
+    const int c = (o.x == w ? o.y : 0) + (x == w ? na.y : 0) + (y == w ? nb.y : 0);
+    return ((unsigned long long)(unsigned)w << 24) | ((unsigned long long)c << 21);
+  };
   moves = swaps = iters = 0;
   evals = 0;
   while (iters < max_it) {
@@ -550,56 +564,85 @@ __device__ __noinline__ void refine_best_warp(int n, const int* D, uint16_t* nli
     int e[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) e[s] = send[s];
-    // score of moving d ticks of work from the slices of mask mf to those of mask mt
-    auto score = [&](unsigned mf, unsigned mt, int d) {
+    unsigned long long cur;
+    {
       int w = -1, c = 0;
 #pragma unroll
       for (int s = 0; s < S; ++s) {
-        const int x = e[s] + (((mt >> s) & 1u) ? d : 0) - (((mf >> s) & 1u) ? d : 0);
-        if (x > w) { w = x; c = 1; } else if (x == w) { ++c; }
+        if (e[s] > w) { w = e[s]; c = 1; } else if (e[s] == w) { ++c; }
       }
-      return ((unsigned long long)(unsigned)w << 24) | ((unsigned long long)c << 21);
-    };
-    const unsigned long long cur = score(0u, 0u, 0);
+      cur = ((unsigned long long)(unsigned)w << 24) | ((unsigned long long)c << 21);
+    }
     const int omega_prev = (int)(cur >> 24);
     unsigned long long best = ~0ull;
     for (int g = 0; g < ncls; ++g) {
       const int f = cf[g], V = cl[g] - f, A = V - 1;
+      // tables of this class
+      __syncwarp();
+      for (int p = lane; p < V * 8; p += 32) {
+        const int ia = p >> 3, ib = p & 7;
+        if (ib < V) {
+          const unsigned mx = mask_of(f + ia) | (ia != ib ? mask_of(f + ib) : 0u);
+          int w = -1, c = 0;
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            if ((mx >> s) & 1u) continue;
+            if (e[s] > w) { w = e[s]; c = 1; } else if (e[s] == w) { ++c; }
+          }
+          pairt[p] = make_int2(w, c);
+        }
+      }
+      if (lane < V) {
+        const unsigned mv = mask_of(f + lane);
+        int w = -1, c = 0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          if (!((mv >> s) & 1u)) continue;
+          if (e[s] > w) { w = e[s]; c = 1; } else if (e[s] == w) { ++c; }
+        }
+        nodet[lane] = make_int2(w, c);
+      }
+      // flat entries of the class: task | local node index << 10, in node order
       int m = 0, sq = 0;
-      for (int v = f; v < f + V; ++v) { m += ncnt[v]; sq += ncnt[v] * ncnt[v]; }
+      for (int v = f; v < f + V; ++v) {
+        const int cv = ncnt[v];
+        for (int q = lane; q < cv; q += 32) flat[m + q] = (uint16_t)(nlist[v * n + q] | ((v - f) << 10));
+        m += cv;
+        sq += cv * cv;
+      }
+      __syncwarp();
       evals += (long long)m * A + (long long)(m * m - sq) / 2;
-      // entry index -> (node, position): scan of the class's node counts
-      auto locate = [&](int idx, int& v, int& pos) {
-        v = f;
-        pos = idx;
-        while (pos >= ncnt[v]) { pos -= ncnt[v]; ++v; }
-      };
-      // moves: flat p = idx * A + r, r-th alternative of the entry's node
-      for (int p = lane; p < m * A; p += 32) {
-        const int idx = p / A, r = p - idx * A;
-        int v, pos;
-        locate(idx, v, pos);
-        const int u = f + r + (f + r >= v ? 1 : 0);
-        const int T = nlist[v * n + pos];
-        const unsigned long long k = score(mask_of(v), mask_of(u), D[T]) | ((unsigned long long)T << 10) | (unsigned)u;
-        best = k < best ? k : best;
+      // moves: flat p = idx * A + r, r-th other node of the class
+      {
+        int idx = lane / A, r = lane - (lane / A) * A;
+        const int di = 32 / A, dr = 32 - di * A;
+        for (int p = lane; p < m * A; p += 32) {
+          const int x = flat[idx], T = x & 1023, ia = x >> 10;
+          const int ib = r + (r >= ia ? 1 : 0);
+          const unsigned long long k = score(ia, ib, D[T]) | ((unsigned long long)T << 10) | (unsigned)(f + ib);
+          best = k < best ? k : best;
+          idx += di;
+          r += dr;
+          if (r >= A) { r -= A; ++idx; }
+        }
       }
       // swaps: entry x (uniform) with every entry y of a later node of the class
-      int vx = f, px = 0;
+      int bend = 0, bnode = -1;
       for (int x = 0; x < m; ++x) {
-        while (px >= ncnt[vx]) { px -= ncnt[vx]; ++vx; }
-        const int tx = nlist[vx * n + px];
-        ++px;
-        int before = 0;
-        for (int v = f; v <= vx; ++v) before += ncnt[v];
-        for (int y = before + lane; y < m; y += 32) {
-          int vy, py;
-          locate(y, vy, py);
-          const int ty = nlist[vy * n + py];
-          const int k = min(tx, ty), j = max(tx, ty);
-          const int a = tx < ty ? vx : vy, b = tx < ty ? vy : vx;
-          const unsigned long long key =
-              score(mask_of(a), mask_of(b), D[k] - D[j]) | (1ull << 20) | ((unsigned long long)k << 10) | (unsigned)j;
+        const int fx = flat[x], tx = fx & 1023, ia = fx >> 10;
+        if (ia != bnode) {  // end of x's node block
+          bnode = ia;
+          bend = 0;
+          for (int v = f; v <= f + ia; ++v) bend += ncnt[v];
+        }
+        const int dx = D[tx];
+        for (int y = bend + lane; y < m; y += 32) {
+          const int fy = flat[y], ty = fy & 1023, ib = fy >> 10;
+          const bool lo = tx < ty;
+          const int k = lo ? tx : ty, j = lo ? ty : tx;
+          const int dd = lo ? dx - D[ty] : D[ty] - dx;
+          const unsigned long long key = score(lo ? ia : ib, lo ? ib : ia, dd) | (1ull << 20) |
+                                         ((unsigned long long)k << 10) | (unsigned)j;
           best = key < best ? key : best;
         }
       }
@@ -774,7 +817,8 @@ __device__ __noinline__ void solve_local(const KParams& P, int64_t inst, unsigne
       for (int j = lane; j < n; j += 32) D[j] = T[j * NC + su[j]];
       __syncwarp();
       if (P.flags & FAR_BEST_IMPROVEMENT)
-        refine_best_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
+        refine_best_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev,
+                             (uint16_t*)start);
       else
         refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, (P.flags & FAR_NONEMPTY_ALT) != 0, lane, mv,
                         sw, it, ev);
@@ -864,7 +908,8 @@ __device__ void finish_core(const KParams& P, int64_t inst, uint16_t* nlist, int
       int mv, sw, it;
       long long ev;
       if (P.flags & FAR_BEST_IMPROVEMENT)
-        refine_best_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev);
+        refine_best_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, lane, mv, sw, it, ev,
+                             (uint16_t*)start);
       else
         refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, (P.flags & FAR_NONEMPTY_ALT) != 0, lane, mv,
                         sw, it, ev);
@@ -1615,11 +1660,14 @@ __global__ void __launch_bounds__(128, PIPE == PIPE_PREP ? 5 : 1) far_solve_kern
   const int* wcr = (const int*)(wsm + L.misc) + M_CR;
   const int* wde = (const int*)(wsm + L.misc) + M_DE;
   if (!P.ovf_pass) {
+    // dynamic instance scheduler; the next index is claimed one instance ahead so the atomic's
+    // latency overlaps the current instance's work
+    unsigned long long nxt = 0;
+    if (lane == 0) nxt = atomicAdd(P.counter, 1ull);
     for (;;) {
-      unsigned long long inst = 0;
-      if (lane == 0) inst = atomicAdd(P.counter, 1ull);
-      inst = __shfl_sync(FULL, inst, 0);
+      const unsigned long long inst = __shfl_sync(FULL, nxt, 0);
       if ((int64_t)inst >= P.I) break;
+      if (lane == 0) nxt = atomicAdd(P.counter, 1ull);
       solve_instance<NC, PIPE>(P, (int64_t)inst, wsm, L, wninfo, wcr, wde, lane);
       __syncwarp();
     }

@@ -381,12 +381,12 @@ __global__ void __launch_bounds__(128, 8) far_finish_kernel(KParams P) {
   const int* de = misc + M_DE;
   const bool want_sched = P.sched != nullptr && !(P.flags & FAR_NO_SCHEDULE);
   const bool refine = !(P.flags & FAR_NO_REFINE);
+  unsigned long long nxt = 0;  // next instance claimed one ahead (atomic latency hidden)
+  if (lane == 0) nxt = atomicAdd(P.counter, 1ull);
   for (;;) {
-    unsigned long long u = 0;
-    if (lane == 0) u = atomicAdd(P.counter, 1ull);
-    u = __shfl_sync(FULL, u, 0);
-    const int64_t inst = (int64_t)u;
+    const int64_t inst = (int64_t)__shfl_sync(FULL, nxt, 0);
     if (inst >= P.I) break;
+    if (lane == 0) nxt = atomicAdd(P.counter, 1ull);
     const int* meta = P.ws_meta + inst * 16;
     if (meta[WS_FLAG]) continue;  // error / empty (K1 wrote the outputs) / deferred to the overflow pass
     const unsigned long long best = P.ws_best[inst];
