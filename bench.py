@@ -166,6 +166,20 @@ def secondary(far, torch, dev, reps=5):
     out["M3_events_instances_per_s"] = d.shape[0] / (msv / 1000.0)
     out["M3_validate_instances_per_s"] = d.shape[0] / (ms_chk / 1000.0)
     out["M3_infeasible_outputs"] = int((viol != 0).sum().item())
+    # single-batch latency through the host API (configs[0] / configs[1]: one A30 n=8 batch, one
+    # A100 n=16 Rodinia-like batch): host buffers in, schedule out, median of 200 synchronous calls
+    import time as _time
+    for wn in ("M1", "M2"):
+        w = inputs.WORKLOADS[wn]
+        F = far.Far(w.profile, w.costs())
+        one = np.ascontiguousarray(w.table(count=1))
+        lat = []
+        for r in range(220):
+            t0 = _time.perf_counter()
+            F.solve_many_host(one)
+            if r >= 20:
+                lat.append(_time.perf_counter() - t0)
+        out[f"{wn}_single_batch_latency_us"] = float(np.median(lat) * 1e6)
     # phase-3 variant FAR_BEST_IMPROVEMENT (R30: the north star's literal neighbourhood,
     # every same-size move and every swap pair scored) on the first 100k M5 instances
     w = inputs.WORKLOADS["M5"]

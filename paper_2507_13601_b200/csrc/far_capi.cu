@@ -349,7 +349,7 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     const int g_inst = (int)std::min<int64_t>((P.I + tb - 1) / tb, (int64_t)ctx->sms * 16);
     const int g_items = ctx->sms * 16;
     {  // K2: per-thread shared-memory copy of member 0's lists -> block size by footprint
-      const size_t per_thread = (size_t)4 * NC + 2 * NN + 4 * (size_t)(n4 + 4);
+      const size_t per_thread = (size_t)4 * NC + 2 * NN + 4 * (size_t)(n4 + 1);
       const int tb0 = (int)std::min<size_t>(128, (size_t)ctx->smem_max / per_thread / 32 * 32);
       if (tb0 < 32) return fail(ctx, FAR_E_TOO_LARGE, "member-0 lists do not fit in shared memory");
       const size_t sm0 = per_thread * tb0;

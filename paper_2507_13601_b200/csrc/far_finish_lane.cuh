@@ -31,7 +31,7 @@ __host__ __device__ inline LRow make_lrow(int n, int NN) {
   r.alt = o; o += 4 * ((n + 31) / 32);
   r.off = o; o += 2 * (NN + 1);
   o = (o + 15) & ~15;
-  r.bytes = o + 16;  // +16 B: consecutive rows start in different banks
+  r.bytes = o + 4;  // odd word stride: the 32 rows of a warp start in 32 different banks
   return r;
 }
 

@@ -231,8 +231,9 @@ __global__ void __launch_bounds__(128) far_member0_kernel(PParams P) {
   const int bdim = blockDim.x, tid = threadIdx.x;
   uint32_t* st = (uint32_t*)dsm + tid;
   uint16_t* npos = (uint16_t*)(dsm + 4 * NC * bdim) + tid;
-  // this thread's copy of member 0's lists (row stride n4 + 4 words: 16 B aligned, banks shifted)
-  uint32_t* row = (uint32_t*)(dsm + (4 * NC + 2 * NN) * bdim) + (size_t)tid * (P.ws_n4 + 4);
+  // this thread's copy of member 0's lists (odd row stride n4 + 1 words: the rows of a warp start
+  // in 32 different banks)
+  uint32_t* row = (uint32_t*)(dsm + (4 * NC + 2 * NN) * bdim) + (size_t)tid * (P.ws_n4 + 1);
   const bool exhaustive = (P.flags & FAR_EXHAUSTIVE) != 0;
   for (int64_t i = (int64_t)blockIdx.x * bdim + tid; i < P.I; i += (int64_t)gridDim.x * bdim) {
     const int* meta = P.ws_meta + i * 16;
@@ -241,8 +242,13 @@ __global__ void __launch_bounds__(128) far_member0_kernel(PParams P) {
     const int* lb = P.ws_lb + i * (int64_t)P.ws_kcap;
     {  // independent 16 B loads (many in flight), then every placement reads shared memory
       const int4* src = (const int4*)(P.ws_m0 + i * (int64_t)P.ws_n4);
-      int4* dst = (int4*)row;
-      for (int q = 0; q < (P.ws_n4 >> 2); ++q) dst[q] = __ldcs(src + q);
+      for (int q = 0; q < (P.ws_n4 >> 2); ++q) {
+        const int4 x = __ldcs(src + q);
+        row[4 * q] = (uint32_t)x.x;
+        row[4 * q + 1] = (uint32_t)x.y;
+        row[4 * q + 2] = (uint32_t)x.z;
+        row[4 * q + 3] = (uint32_t)x.w;
+      }
     }
     int pops = 0;
     const int ms0 = sim_member0<NC>(row, P.ws_cnt[i * (int64_t)P.ws_kcap], sm.ninfo, sm.cr, sm.de, st, npos, bdim,
