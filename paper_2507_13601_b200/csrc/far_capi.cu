@@ -268,7 +268,9 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
   if (const char* e = getenv("FAR_DEBUG_KFAST")) kcap_fast = std::max(2, std::min(254, atoi(e)));  // experiments (8-bit intervals)
   int kfast = std::min(kmax, kcap_fast);
   if (P.mode != MODE_SOLVE) kfast = 1;
-  const bool pipe = P.mode == MODE_SOLVE && P.n > 0 && P.n <= 1023 && !getenv("FAR_FUSED_PHASE2");
+  // small batches (latency): the fused warp-per-instance kernel is one launch instead of five
+  const bool pipe = P.mode == MODE_SOLVE && P.n > 0 && P.n <= 1023 && !getenv("FAR_FUSED_PHASE2") &&
+                    (P.I >= 256 || getenv("FAR_PIPELINE_ALWAYS"));
   const bool need_ovf = P.mode == MODE_SOLVE && (kfast < kmax || pipe);
   const int slot = (ctx->launch_id++ % (RING / 8)) * 8;
   CK(cudaMemsetAsync(ctx->d_counter + slot, 0, 8 * sizeof(unsigned long long), stream));
