@@ -251,6 +251,44 @@ __device__ void lane_lists(int n, const uint32_t* __restrict__ rec, const uint16
   }
 }
 
+// Warp-cooperative form of lane_lists for the active lanes' instances (mask am): the record of
+// instance i is read by the whole warp with coalesced 16-B loads (instead of one thread walking
+// 512 B with dependent loads) and its entries are written into lane i's row.  The rows' off[]
+// must already hold the node offsets and alt[] be zero.
+template <int NC>
+__device__ void lane_lists_coop(int n, int64_t base, unsigned am, const KParams& P, unsigned char* wrows, int rbytes,
+                                const LRow& L, int lane) {
+  for (; am; am &= am - 1) {
+    const int i = __ffs(am) - 1;
+    const int64_t inst = base + i;
+    unsigned char* row = wrows + (size_t)i * rbytes;
+    uint32_t* ent = (uint32_t*)(row + L.ent);
+    const uint16_t* off = (const uint16_t*)(row + L.off);
+    uint32_t* alt = (uint32_t*)(row + L.alt);
+    const uint32_t* rec = P.ws_rec + inst * (int64_t)n;
+    const int32_t* t = P.times + inst * (int64_t)n * NC;
+    auto put = [&](int j, uint32_t r) {
+      const int v = (int)(r & 15u), c = (int)((r >> 4) & 7u), pos = (int)(r >> 7);
+      const int d = __ldg(t + j * NC + c);
+      ent[off[v] + pos] = ((uint32_t)d << 10) | (uint32_t)(1023 - j);
+      if (c != nd_c0(cnode<NC>(v))) atomicOr(&alt[j >> 5], 1u << (j & 31));
+    };
+    if ((n & 3) == 0) {
+      const uint4* r4 = (const uint4*)rec;
+      for (int q = lane; q < (n >> 2); q += 32) {
+        const uint4 x = __ldcs(r4 + q);
+        put(4 * q, x.x);
+        put(4 * q + 1, x.y);
+        put(4 * q + 2, x.z);
+        put(4 * q + 3, x.w);
+      }
+    } else {
+      for (int j = lane; j < n; j += 32) put(j, __ldcs(rec + j));
+    }
+  }
+  __syncwarp();
+}
+
 // Node-level replay (the frontier in registers of this thread); writes the schedule when
 // `out` is not null; returns the makespan.
 template <int NC>
@@ -311,10 +349,29 @@ __global__ void __launch_bounds__(128, 3) far_finish_lane_kernel(KParams P) {
   const bool want_sched = P.sched != nullptr && !(P.flags & FAR_NO_SCHEDULE);
   const bool refine = !(P.flags & FAR_NO_REFINE);
   const bool need_replay = refine || want_sched;
-  for (int64_t inst = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; inst < P.I;
+  const int lane = threadIdx.x & 31;
+  unsigned char* wrows = dsm + (size_t)(threadIdx.x & ~31) * L.bytes;
+  // the lanes of a warp hold consecutive instances and step together (the list staging is
+  // warp-cooperative); every lane runs the loop until the warp's first instance passes I
+  for (int64_t inst = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; inst - lane < P.I;
        inst += (int64_t)gridDim.x * blockDim.x) {
+    // error / empty (K1 wrote the outputs) / deferred to the overflow pass: nothing to finish
+    const bool active = inst < P.I && !P.ws_meta[inst * 16 + WS_FLAG];
+    if (active) {
+      for (int w = 0; w < (n + 31) / 32; ++w) alt[w] = 0;
+      int acc = 0;
+      const uint16_t* nc = P.ws_ncnt + inst * 16;
+#pragma unroll
+      for (int v = 0; v < NN; ++v) {
+        off[v] = (uint16_t)acc;
+        acc += __ldg(nc + v);
+      }
+      off[NN] = (uint16_t)acc;
+    }
+    __syncwarp();
+    lane_lists_coop<NC>(n, inst - lane, __ballot_sync(FULL, active), P, wrows, L.bytes, L, lane);
+    if (!active) continue;
     const int* meta = P.ws_meta + inst * 16;
-    if (meta[WS_FLAG]) continue;  // error / empty (K1 wrote the outputs) / deferred to the overflow pass
     const unsigned long long best = P.ws_best[inst];
     const int ms2 = (int)(best >> 16), bestk = (int)(best & 0xFFFFu);
     far_result R;
@@ -326,7 +383,7 @@ __global__ void __launch_bounds__(128, 3) far_finish_lane_kernel(KParams P) {
     far_task_slot* out = want_sched ? P.sched + inst * (int64_t)n : nullptr;
     int msF = ms2;
     for (int pass = 0; pass < 2; ++pass) {
-      lane_lists<NC>(n, rec, P.ws_ncnt + inst * 16, t, ent, off, alt);
+      if (pass) lane_lists<NC>(n, rec, P.ws_ncnt + inst * 16, t, ent, off, alt);
       const bool ref = refine && pass == 0;
       if (ref) {
         int send[S];
