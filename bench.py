@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--baseline-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gather-schedules", action="store_true",
+                    help="N>1: also all-gather the per-task schedules (8 B/task) every step")
     ap.add_argument("--no-baseline", action="store_true")
     ap.add_argument("--profile-run", action="store_true", help="short run for ncu (no clocks/e2e/baseline)")
     ap.add_argument("--no-secondary", action="store_true", help="skip the M3 / M4-stream secondary measurements")
@@ -299,6 +301,8 @@ def main():
     sd = torch.empty((I, WORKLOAD.n, 8), dtype=torch.uint8, device=dev)
     rs = torch.empty((I, 56), dtype=torch.uint8, device=dev)
     gathered = torch.empty(I * world, dtype=torch.int32, device=dev) if world > 1 else None
+    gsched = (torch.empty((I * world, WORKLOAD.n, 8), dtype=torch.uint8, device=dev)
+              if world > 1 and args.gather_schedules and backend == "nccl" else None)
 
     def step(ev=None):
         if ev is not None:
@@ -309,6 +313,8 @@ def main():
         if world > 1:
             if backend == "nccl":
                 dist.all_gather_into_tensor(gathered, ms)
+                if gsched is not None:
+                    dist.all_gather_into_tensor(gsched.view(-1), sd.view(-1))
             else:
                 g = torch.empty(I * world, dtype=torch.int32)
                 dist.all_gather_into_tensor(g, ms.cpu())
@@ -449,7 +455,8 @@ def main():
                        "n_tasks": WORKLOAD.n, "instances_per_rank": I, "global_instances": inst_all,
                        "generator": "PAPER.md §6.3 MixedScaling/WideTimes, seed 5",
                        "l2": f"inputs ({host.nbytes / 1e9:.2f} GB/rank) larger than the 126 MB L2; no flush",
-                       "parallelism": f"dp{world} (instances sharded, NCCL allgather of makespans)"},
+                       "parallelism": f"dp{world} (instances sharded, NCCL allgather of makespans"
+                                  + (" and schedules)" if gsched is not None else ")")},
             "evals_per_s": evals_all / (ms_per_step / 1000.0),
             "alg1_events_simulated_per_s": events_all / (ms_per_step / 1000.0),
             "alg1_events_algorithmic_per_step": alg_events,

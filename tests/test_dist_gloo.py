@@ -32,8 +32,16 @@ def _worker(rank, world, port, total, q):
     tab = w.table(count=hi - lo, start=lo)
     ms, _ = O.far_many(w.profile, w.costs(), tab)
     g = fdist.gather_makespans(torch.from_numpy(ms.astype(np.int32)), total)
+    # packed schedules (8 B per task, the far_task_slot layout): node, size, pad, start
+    sl = np.zeros((hi - lo, w.n, 8), np.uint8)
+    for i in range(hi - lo):
+        o = O.far(w.profile, w.costs(), tab[i])["slots"]
+        sl[i, :, 0] = o["node"]
+        sl[i, :, 1] = o["size_used"]
+        sl[i, :, 4:] = o["start"].astype("<i4").view(np.uint8).reshape(-1, 4)
+    gs = fdist.gather_schedules(torch.from_numpy(sl), total)
     if rank == 0:
-        q.put(g.numpy().tolist())
+        q.put((g.numpy().tolist(), gs.numpy()))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -60,5 +68,12 @@ def test_gloo_allgather_world2(O, total):
         p.join(timeout=120)
         assert p.exitcode == 0
     w = inputs.WORKLOADS["M3"]
-    ref, _ = O.far_many(w.profile, w.costs(), w.table(count=total))
-    assert got == ref.tolist()
+    tab = w.table(count=total)
+    ref, _ = O.far_many(w.profile, w.costs(), tab)
+    got_ms, got_sl = got
+    assert got_ms == ref.tolist()
+    assert got_sl.shape == (total, w.n, 8)
+    for i in (0, total // 2, total - 1):  # the gathered schedules are the whole job's, in order
+        o = O.far(w.profile, w.costs(), tab[i])["slots"]
+        assert (got_sl[i, :, 0] == o["node"]).all() and (got_sl[i, :, 1] == o["size_used"]).all()
+        assert (got_sl[i, :, 4:].copy().view("<i4")[:, 0] == o["start"]).all()
