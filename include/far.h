@@ -128,8 +128,8 @@ far_status far_create(far_profile profile, const int32_t *reconfig_cost, far_ctx
  * is t*NN + v (NN = 7 A30, 13 A100/H100), its slices t*S + [lo, hi).  num_gpus in [1, 8]
  * (else FAR_E_INVALID_ARG); far_create(p, c, out) == far_create_multi(p, 1, c, out).  With
  * num_gpus > 1: far_solve_many / far_solve_many_host / far_schedule_batch / far_local_search /
- * far_lower_bounds take n <= 256 (else FAR_E_TOO_LARGE) and every flag except
- * FAR_BEST_IMPROVEMENT (FAR_E_INVALID_ARG); far_concat_streams, far_schedule_events and
+ * far_lower_bounds take n <= 256 (else FAR_E_TOO_LARGE) and every flag (with
+ * FAR_BEST_IMPROVEMENT the classes are the same-size nodes of all trees); far_concat_streams, far_schedule_events and
  * far_validate_schedules return FAR_E_UNSUPPORTED_PROFILE. */
 far_status far_create_multi(far_profile profile, int32_t num_gpus, const int32_t *reconfig_cost, far_ctx **out);
 int32_t far_num_gpus(const far_ctx *ctx);

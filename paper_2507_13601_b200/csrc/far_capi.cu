@@ -236,8 +236,6 @@ static far_status launch_warp_kernel(far_ctx* ctx, KParams& P, cudaStream_t stre
 //   FAR_FUSED_PHASE2 (debug env) forces the fused warp-per-instance kernel for everything.
 //   MODE_LOCAL: the fused kernel (phase 3 only).
 static far_status launch_forest(far_ctx* ctx, KParams& P, cudaStream_t stream) {
-  if (P.flags & FAR_BEST_IMPROVEMENT)
-    return fail(ctx, FAR_E_INVALID_ARG, "FAR_BEST_IMPROVEMENT: single-GPU trees only");
   P.errflag = ctx->d_errflag;
   FParams F;
   F.P = P;

@@ -48,7 +48,8 @@ __device__ __forceinline__ int fn_par(uint2 w) { return (int)((w.y >> 16) & 255u
 
 // per-warp shared-memory layout (bytes)
 struct FLay {
-  int T, glist, cur, rs[2], rn[2], rp[2], ru[2], ncnt, L, off, cursor, send, D, Q, opened, leaf, misc, bytes;
+  int T, glist, cur, rs[2], rn[2], rp[2], ru[2], ncnt, L, off, cursor, send, D, Q, opened, leaf, misc, tnode, srt,
+      nstat, bytes;
 };
 __host__ __device__ inline FLay make_flay(int n, int NC, int NNF, int SF) {
   FLay L;
@@ -73,6 +74,9 @@ __host__ __device__ inline FLay make_flay(int n, int NC, int NNF, int SF) {
   L.opened = take(NNF + 1);
   L.leaf = take(SF);
   L.misc = take(4 * 32);
+  L.tnode = take(n);        // best-improvement: node of each task
+  L.srt = take(8 * SF);     // best-improvement: slice ends sorted descending (value, slice)
+  L.nstat = take(8 * NNF);  // best-improvement: (max, count) of each node's slice ends
   L.bytes = o;
   return L;
 }
@@ -360,6 +364,121 @@ __device__ void forest_refine(const FParams& F, int n, const int* D, uint16_t* L
   }
 }
 
+// Phase-3 variant FAR_BEST_IMPROVEMENT (R30) over the forest: every move of a task to
+// another node of the same size (any tree) and every swap of two tasks on different same-size
+// nodes is scored by (w', c') = (max slice end after it, #slices at w'); the argmin of (w', c',
+// move before swap, first id, second id) is applied while it lowers (w, c).  Same-size nodes are
+// disjoint, so a transfer of d ticks a -> b scores max(out(a, b), M_a - d, M_b + d), out(a, b)
+// read off the slice ends sorted in descending order (first entries outside a and b).
+template <int NC>
+__device__ void forest_refine_best(const FParams& F, int n, const int* D, uint16_t* L, int* off, int* send,
+                                   uint8_t* tnode, int2* srt, int2* nstat, int lane, int& moves, int& swaps,
+                                   int& iters, long long& evals) {
+  const KParams& P = F.P;
+  const int NNF = F.NNF, SF = F.SF;
+  for (int v = 0; v < NNF; ++v)
+    for (int q = off[v] + lane; q < off[v + 1]; q += 32) tnode[L[q]] = (uint8_t)v;
+  __syncwarp();
+  auto lo_of = [&](int v) { return fn_lo(__ldg(F.nodes + v)); };
+  auto sz_of = [&](int v) { return fn_sz(__ldg(F.nodes + v)); };
+  // (w', c') of moving d ticks from node a to node b (disjoint, same size)
+  auto score = [&](int a, int b, int d) {
+    const int la = lo_of(a), lb = lo_of(b), z = sz_of(a);
+    const int2 na = nstat[a], nb = nstat[b];
+    int ow = -1, oc = 0;
+    for (int r = 0; r < SF; ++r) {
+      const int2 e = srt[r];
+      const bool in = (e.y >= la && e.y < la + z) || (e.y >= lb && e.y < lb + z);
+      if (in) continue;
+      if (ow < 0) ow = e.x;
+      if (e.x != ow) break;
+      ++oc;
+    }
+    const int x = na.x - d, y = nb.x + d;
+    const int w = max(ow, max(x, y));
+    const int c = (ow == w ? oc : 0) + (x == w ? na.y : 0) + (y == w ? nb.y : 0);
+    return ((unsigned long long)(unsigned)w << 27) | ((unsigned long long)c << 21);
+  };
+  moves = swaps = iters = 0;
+  evals = 0;
+  while (iters < P.max_it) {
+    ++iters;
+    // slice ends sorted descending (rank by (value desc, slice asc)), node stats, current (w, c)
+    for (int s = lane; s < SF; s += 32) {
+      const int x = send[s];
+      int r = 0;
+      for (int u = 0; u < SF; ++u) r += send[u] > x || (send[u] == x && u < s);
+      srt[r] = make_int2(x, s);
+    }
+    for (int v = lane; v < NNF; v += 32) {
+      const int l0 = lo_of(v), z = sz_of(v);
+      int w = -1, c = 0;
+      for (int s = l0; s < l0 + z; ++s) {
+        if (send[s] > w) { w = send[s]; c = 1; } else if (send[s] == w) { ++c; }
+      }
+      nstat[v] = make_int2(w, c);
+    }
+    __syncwarp();
+    int cw = srt[0].x, cc = 0;
+    for (int r = 0; r < SF && srt[r].x == cw; ++r) ++cc;
+    const unsigned long long cur = ((unsigned long long)(unsigned)cw << 27) | ((unsigned long long)cc << 21);
+    unsigned long long best = ~0ull;
+    long long ev = 0;
+    for (int x = lane; x < n; x += 32) {  // moves
+      const int a = tnode[x], z = sz_of(a);
+      for (int u = 0; u < NNF; ++u) {
+        if (u == a || sz_of(u) != z) continue;
+        ++ev;
+        const unsigned long long k = score(a, u, D[x]) | ((unsigned long long)x << 10) | (unsigned)u;
+        best = k < best ? k : best;
+      }
+    }
+    for (int k = 0; k < n; ++k) {  // swaps k < j
+      const int a = tnode[k], z = sz_of(a), dk = D[k];
+      for (int j = k + 1 + lane; j < n; j += 32) {
+        const int b = tnode[j];
+        if (b == a || sz_of(b) != z) continue;
+        ++ev;
+        const unsigned long long key = score(a, b, dk - D[j]) | (1ull << 20) | ((unsigned long long)k << 10) |
+                                       (unsigned)j;
+        best = key < best ? key : best;
+      }
+    }
+    evals += warp_sum_ll(ev);
+    const unsigned hi = __reduce_min_sync(FULL, (unsigned)(best >> 32));
+    const unsigned lo = __reduce_min_sync(FULL, (unsigned)(best >> 32) == hi ? (unsigned)best : ~0u);
+    best = ((unsigned long long)hi << 32) | lo;
+    if ((best >> 21) >= (cur >> 21)) break;
+    const int x = (int)((best >> 10) & 1023), y = (int)(best & 1023);
+    int from, to, d, tk1 = -1;
+    if (!((best >> 20) & 1)) {
+      from = tnode[x]; to = y; d = D[x];
+      ++moves;
+    } else {
+      from = tnode[x]; to = tnode[y]; d = D[x] - D[y]; tk1 = y;
+      ++swaps;
+    }
+    fl_remove(L, off, NNF, n, x, from, lane);
+    if (tk1 >= 0) fl_remove(L, off, NNF, n, tk1, to, lane);
+    fl_insert(L, off, NNF, x, to, D, lane);
+    if (tk1 >= 0) fl_insert(L, off, NNF, tk1, from, D, lane);
+    if (lane == 0) {
+      tnode[x] = (uint8_t)to;
+      if (tk1 >= 0) tnode[tk1] = (uint8_t)from;
+    }
+    const int lf = lo_of(from), lt = lo_of(to), z = sz_of(from);
+    for (int s = lane; s < SF; s += 32) {
+      if (s >= lf && s < lf + z) send[s] -= d;
+      if (s >= lt && s < lt + z) send[s] += d;
+    }
+    __syncwarp();
+    int om = 0;
+    for (int s = lane; s < SF; s += 32) om = max(om, send[s]);
+    om = (int)__reduce_max_sync(FULL, (unsigned)om);
+    if (P.ppm > 0 && (long long)(cw - om) * 1000000LL < (long long)P.ppm * cw) break;
+  }
+}
+
 template <int NC>
 __global__ void __launch_bounds__(128) far_forest_kernel(FParams F) {
   extern __shared__ __align__(16) unsigned char fsm[];
@@ -626,7 +745,11 @@ __global__ void __launch_bounds__(128) far_forest_kernel(FParams F) {
       __syncwarp();
       int mv, sw, it;
       long long ev;
-      forest_refine<NC>(F, n, D, L, off, send, Q, opened, leaf, lane, mv, sw, it, ev);
+      if (P.flags & FAR_BEST_IMPROVEMENT)
+        forest_refine_best<NC>(F, n, D, L, off, send, wsm + Ly.tnode, (int2*)(wsm + Ly.srt), (int2*)(wsm + Ly.nstat),
+                               lane, mv, sw, it, ev);
+      else
+        forest_refine<NC>(F, n, D, L, off, send, Q, opened, leaf, lane, mv, sw, it, ev);
       R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
       // ---- H7: line-26 replay + keep-best guard
       const int ob = b2 ^ 1;

@@ -26,7 +26,7 @@ def test_forest_bitexact(O, torch_dev, prof, n):
     costs = inputs.reconfig_costs(base)
     count = 60 if n >= 128 else 200
     tab = inputs.synthetic(base, n, count, 500 + n)
-    for flags in (0, far.EXHAUSTIVE, far.NO_GUARD, far.ZERO_RECONFIG, far.NO_REFINE):
+    for flags in (0, far.EXHAUSTIVE, far.NO_GUARD, far.ZERO_RECONFIG, far.NO_REFINE, far.BEST_IMPROVEMENT):
         ms, slots, res = run_gpu(torch_dev, prof, costs, tab, flags=flags)
         check_against_oracle(O, prof, costs, tab, ms, slots, res, flags=flags, full=n <= 64)
 
@@ -39,13 +39,16 @@ def test_forest_ties_and_variants(O, torch_dev, prof, gen):
     n = 24
     tab = {"ties": inputs.small_ties, "uniform": inputs.uniform_random,
            "monoties": inputs.monotone_ties}[gen](base, n, 200, 41)
-    for flags in (0, far.NONEMPTY_ALT, far.GROW_TIES, far.GROW_TIES | far.EXHAUSTIVE):
+    for flags in (0, far.NONEMPTY_ALT, far.GROW_TIES, far.GROW_TIES | far.EXHAUSTIVE, far.BEST_IMPROVEMENT,
+                  far.BEST_IMPROVEMENT | far.ZERO_RECONFIG):
         ms, slots, res = run_gpu(torch_dev, prof, costs, tab, flags=flags)
         check_against_oracle(O, prof, costs, tab, ms, slots, res, flags=flags)
-    for kw in ({"max_iterations": 1}, {"min_improvement_ppm": 30000}):
-        ms, slots, res = run_gpu(torch_dev, prof, costs, tab, **kw)
-        check_against_oracle(O, prof, costs, tab, ms, slots, res, max_iterations=kw.get("max_iterations", 100),
-                             ppm=kw.get("min_improvement_ppm", 0), full=False)
+    for flags in (0, far.BEST_IMPROVEMENT):
+        for kw in ({"max_iterations": 1}, {"min_improvement_ppm": 30000}):
+            ms, slots, res = run_gpu(torch_dev, prof, costs, tab, flags=flags, **kw)
+            check_against_oracle(O, prof, costs, tab, ms, slots, res, flags=flags,
+                                 max_iterations=kw.get("max_iterations", 100),
+                                 ppm=kw.get("min_improvement_ppm", 0), full=False)
 
 
 def test_forest_more_gpus_help(O, torch_dev):
@@ -80,6 +83,11 @@ def test_forest_host_paths(O, torch_dev):
             for k in ("makespan", "moves", "swaps", "evals", "iterations", "reverted"):
                 assert r2[k] == q["result"][k], k
             assert (s2["node"] == q["slots"]["node"]).all() and (s2["start"] == q["slots"]["start"]).all()
+            s3, r3 = F.local_search(t, s, makespan_phase2=int(r["makespan"]), flags=far.BEST_IMPROVEMENT)
+            q3 = O.refine(prof, costs, t, oslots, int(r["makespan"]), flags=O.BEST_IMPROVEMENT)
+            for k in ("makespan", "moves", "swaps", "evals", "iterations", "reverted"):
+                assert r3[k] == q3["result"][k], k
+            assert (s3["node"] == q3["slots"]["node"]).all() and (s3["start"] == q3["slots"]["start"]).all()
         tab = np.ascontiguousarray(inputs.synthetic(base, 21, 500, 59))
         ms_h, sd_h, rs_h = F.solve_many_host(tab)
         oms, _ = O.far_many(prof, costs, tab)
@@ -93,8 +101,6 @@ def test_forest_errors(torch_dev):
     with pytest.raises(far.FarError):
         F.solve_many(d)
     d = torch.ones((2, 8, 5), dtype=torch.int32, device=dev)
-    with pytest.raises(far.FarError):
-        F.solve_many(d, flags=far.BEST_IMPROVEMENT)
     with pytest.raises(far.FarError):
         F.concat_streams(d.reshape(1, 2, 8, 5))
     with pytest.raises(far.FarError):
