@@ -438,7 +438,19 @@ def main():
         traffic = (tj["dram_read_bytes_per_instance"] + tj["dram_write_bytes_per_instance"]) * I
     except Exception:
         pass
+    # the same denominators measured on this GPU (far_measure_peak microbenchmark, after the timed
+    # region): the integer issue limit (alu + fma pipes), the alu pipe alone, shared-memory loads
+    meas = None
+    if not args.profile_run:
+        try:
+            mix, alu, lds = (F.measure_peak(m) for m in (1, 0, 2))
+            meas = {"int_issue_alu_fma_tops": mix / 1e12, "int_alu_pipe_tops": alu / 1e12,
+                    "smem_load_tbs": lds / 1e12, "frac_vs_measured_issue": achieved / mix,
+                    "source": "far_measure_peak: 8 independent 32-bit chains/thread, 2 CTAs x 1024 threads per SM"}
+        except Exception as e:  # diagnostics only
+            meas = {"error": str(e)}
     roof = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
+            "peak_measured": meas,
             "frac": achieved / peak_ops, "traffic": traffic, "traffic_unit": "bytes per step, all kernels (ncu)",
             "kernel": "far_solve_many kernel chain (prep, member0, members, winner, finish, overflow)",
             "stages_ms_per_step": stages, "dominant_stage": dom,

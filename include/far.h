@@ -264,6 +264,12 @@ far_status far_stage_timing(far_ctx *ctx, int32_t enable);
 int32_t far_stage_times(far_ctx *ctx, float *ms);
 /* Number of kernels the context has launched since far_create (host-side count). */
 int64_t far_launch_count(const far_ctx *ctx);
+/* Roofline denominators measured on this GPU: a microbenchmark kernel of
+ * independent 32-bit chains, timed with CUDA events on the default stream (synchronous).
+ * mode 0: alu-pipe integer ops (IADD3/LOP3) -> *per_s = lane-ops/s; mode 1: alu + fma-pipe
+ * integer ops (IADD3 + IMAD, the issue limit) -> lane-ops/s; mode 2: shared-memory loads ->
+ * bytes/s.  Errors: FAR_E_INVALID_ARG, FAR_E_CUDA. */
+far_status far_measure_peak(far_ctx *ctx, int32_t mode, double *per_s);
 
 #ifdef __cplusplus
 }

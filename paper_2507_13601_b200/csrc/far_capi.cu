@@ -15,6 +15,7 @@
 #include "far_finish_lane.cuh"
 #include "far_check.cuh"
 #include "far_forest.cuh"
+#include "far_peak.cuh"
 
 using namespace farb;
 
@@ -545,6 +546,36 @@ int32_t far_stage_times(far_ctx* ctx, float* ms) {
 }
 
 int64_t far_launch_count(const far_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+far_status far_measure_peak(far_ctx* ctx, int32_t mode, double* per_s) {
+  if (!ctx || !per_s || mode < 0 || mode > 2) return FAR_E_INVALID_ARG;
+  far_status st = ensure_device(ctx);
+  if (st) return st;
+  unsigned* d_out = nullptr;
+  CK(cudaMalloc(&d_out, 4));
+  const int blocks = ctx->sms * 2, threads = 1024, iters = mode == 2 ? 2048 : 4096;
+  auto launch = [&](int it) {
+    if (mode == 0) far_peak_kernel<0><<<blocks, threads>>>(d_out, it);
+    else if (mode == 1) far_peak_kernel<1><<<blocks, threads>>>(d_out, it);
+    else far_peak_kernel<2><<<blocks, threads>>>(d_out, it);
+  };
+  launch(64);  // warm-up (clocks, module load)
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  CK(cudaEventRecord(a));
+  launch(iters);
+  CK(cudaEventRecord(b));
+  CK(cudaEventSynchronize(b));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(d_out);
+  const double ops = (double)blocks * threads * iters * 16.0 * 8.0;
+  *per_s = (mode == 2 ? 4.0 : 1.0) * ops / (ms * 1e-3);
+  return FAR_OK;
+}
 
 far_status far_node_table(const far_ctx* ctx, int32_t* lo, int32_t* hi, int32_t* parent) {
   if (!ctx || !lo || !hi || !parent) return FAR_E_INVALID_ARG;

@@ -65,6 +65,7 @@ def lib():
         sig = {
             "far_create": ([C.c_int, p, C.POINTER(p)], C.c_int),
             "far_create_multi": ([C.c_int, i32, p, C.POINTER(p)], C.c_int),
+            "far_measure_peak": ([p, i32, C.POINTER(C.c_double)], C.c_int),
             "far_num_gpus": ([p], i32),
             "far_destroy": ([p], None),
             "far_num_sizes": ([p], i32),
@@ -147,6 +148,13 @@ class Far:
         lo, hi, par = (np.zeros(self.nnodes, np.int32) for _ in range(3))
         self._check(lib().far_node_table(self._h, _np_ptr(lo), _np_ptr(hi), _np_ptr(par)))
         return lo, hi, par
+
+    def measure_peak(self, mode):
+        """Microbenchmark (far_measure_peak): 0 alu-pipe int lane-ops/s, 1 alu+fma int lane-ops/s,
+        2 shared-memory load bytes/s."""
+        v = C.c_double()
+        self._check(lib().far_measure_peak(self._h, mode, C.byref(v)))
+        return v.value
 
     def sync(self):
         self._check(lib().far_sync(self._h))
