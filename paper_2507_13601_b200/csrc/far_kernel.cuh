@@ -1282,7 +1282,14 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         bool stuck = false;
         for (int j = lane; j < n; j += 32) stuck |= cur[j] == NC - 1 && T[j * NC + cur[j]] == hmax;
         if (__any_sync(FULL, stuck)) break;
-        if (K >= P.kcap) {
+        // one step adds an entry per grown task: the per-size lists must still fit the layout
+        int ngrow = 0;
+        for (int j = lane; j < n; j += 32) ngrow += T[j * NC + cur[j]] == hmax;
+        ngrow = __reduce_add_sync(FULL, ngrow);
+        int etot = 0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) etot += (int)((entp >> (11 * c)) & 2047u);
+        if (K >= P.kcap || etot + ngrow > L.ecap) {
           if (lane == 0) {
             atomicOr(P.ovf + (inst >> 5), 1u << (inst & 31));
             atomicAdd(P.ovf_count, 1ull);

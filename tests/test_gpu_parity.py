@@ -374,3 +374,15 @@ def test_best_improvement_fused_path(O, torch_dev, monkeypatch, profile):
     tab = inputs.synthetic(profile, 40, 100, 64)
     ms, slots, res = run_gpu(torch_dev, profile, costs, tab, flags=far.BEST_IMPROVEMENT)
     check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=far.BEST_IMPROVEMENT)
+
+
+@pytest.mark.parametrize("n", [128, 511])
+def test_grow_ties_many_entries(O, torch_dev, n):
+    """Regression (found by tests/test_gpu_fuzz.py seed 151): with FAR_GROW_TIES and dense ties a
+    growth step adds one list entry per tied task, so the per-size lists can outgrow the fast
+    layout before the family does; such instances must go to the full-layout overflow pass."""
+    costs = inputs.reconfig_costs("H100")
+    tab = inputs.monotone_ties("H100", n, 6 if n > 256 else 40, 7)
+    for flags in (far.GROW_TIES | far.NO_REFINE, far.GROW_TIES):
+        ms, slots, res = run_gpu(torch_dev, "H100", costs, tab, flags=flags)
+        check_against_oracle(O, "H100", costs, tab, ms, slots, res, flags=flags, full=n <= 128)
