@@ -339,19 +339,22 @@ __device__ void list_remove(uint16_t* lst, int* cnt, int j, int lane) {
 }
 
 // "Insert T in I^a.tasks ordered by T.time": decreasing time, ties -> lower index.
-// Warp: the insertion point is the number of entries ordered before j; chunked shift right.
+// Warp: the insertion point is the first entry not ordered before j (the oracle's linear scan;
+// on a sorted list it is the number of entries before j, and input schedules of
+// far_local_search need not be sorted); chunked shift right.
 template <int NC>
 __device__ void list_insert(uint16_t* lst, int* cnt, int j, const int* D, int lane) {
   const int c = *cnt;
   const int dj = D[j];
   if (c < 32) {  // one chunk: position by ballot, shift right by a shuffle
     const int x = lane < c ? lst[lane] : 0;
-    bool before = false;
+    bool nb = false;
     if (lane < c) {
       const int dx = D[x];
-      before = dx > dj || (dx == dj && x < j);
+      nb = !(dx > dj || (dx == dj && x < j));
     }
-    const int pos = __popc(__ballot_sync(FULL, before));
+    const unsigned m = __ballot_sync(FULL, nb);
+    const int pos = m ? __ffs(m) - 1 : c;
     const int y = __shfl_up_sync(FULL, x, 1);
     __syncwarp();
     if (lane <= c) lst[lane] = (uint16_t)(lane < pos ? x : (lane == pos ? j : y));
@@ -359,16 +362,17 @@ __device__ void list_insert(uint16_t* lst, int* cnt, int j, const int* D, int la
     __syncwarp();
     return;
   }
-  int pos = 0;
+  int pos = c;
   for (int b = 0; b < c; b += 32) {
     const int i = b + lane;
-    bool before = false;
+    bool nb = false;
     if (i < c) {
       const int x = lst[i];
       const int dx = D[x];
-      before = dx > dj || (dx == dj && x < j);
+      nb = !(dx > dj || (dx == dj && x < j));
     }
-    pos += __popc(__ballot_sync(FULL, before));
+    const unsigned m = __ballot_sync(FULL, nb);
+    if (m) { pos = b + __ffs(m) - 1; break; }
   }
   for (int top = c - 1; top >= pos; top -= 32) {
     const int i = top - lane;
@@ -488,11 +492,12 @@ __device__ void refine_warp(int n, const int* D, uint16_t* nlist, int* ncnt, int
             ++swaps;
           }
         }
-        for (int x = 0; x < nt; ++x) {  // move: I->A; swap: K I->A then J A->I (same final lists)
-          const int from = x == 0 ? I : A, to = x == 0 ? A : I, task = x == 0 ? tk0 : tk1;
-          list_remove<NC>(nlist + from * n, &ncnt[from], task, lane);
-          list_insert<NC>(nlist + to * n, &ncnt[to], task, D, lane);
-        }
+        // move: K from I to A; swap: remove K from I and J from A, then insert K into A and J
+        // into I (the oracle's order: insertion points do not see the other swapped task)
+        for (int x = 0; x < nt; ++x)
+          list_remove<NC>(nlist + (x == 0 ? I : A) * n, &ncnt[x == 0 ? I : A], x == 0 ? tk0 : tk1, lane);
+        for (int x = 0; x < nt; ++x)
+          list_insert<NC>(nlist + (x == 0 ? A : I) * n, &ncnt[x == 0 ? A : I], x == 0 ? tk0 : tk1, D, lane);
         if (nt) {
           add_on(wI, -delta);
           add_on(ninfo[A], delta);
