@@ -1287,14 +1287,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         bool stuck = false;
         for (int j = lane; j < n; j += 32) stuck |= cur[j] == NC - 1 && T[j * NC + cur[j]] == hmax;
         if (__any_sync(FULL, stuck)) break;
-        // one step adds an entry per grown task: the per-size lists must still fit the layout
-        int ngrow = 0;
-        for (int j = lane; j < n; j += 32) ngrow += T[j * NC + cur[j]] == hmax;
-        ngrow = __reduce_add_sync(FULL, ngrow);
-        int etot = 0;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) etot += (int)((entp >> (11 * c)) & 2047u);
-        if (K >= P.kcap || etot + ngrow > L.ecap) {
+        if (K >= P.kcap) {
           if (lane == 0) {
             atomicOr(P.ovf + (inst >> 5), 1u << (inst & 31));
             atomicAdd(P.ovf_count, 1ull);
@@ -1373,6 +1366,16 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
     for (int c = 0; c < NC; ++c) {
       if (lane == 0) loff[c] = acc;
       acc += (int)((entp >> (11 * c)) & 2047u);
+    }
+    // FAR_GROW_TIES adds an entry per tied task per step, so its lists can outgrow the layout
+    // (n + kcap - 1 entries) before the family does: defer to the full-layout overflow pass
+    if (acc > L.ecap) {
+      if (lane == 0) {
+        atomicOr(P.ovf + (inst >> 5), 1u << (inst & 31));
+        atomicAdd(P.ovf_count, 1ull);
+        if (PIPE == PIPE_PREP) P.ws_meta[inst * 16 + WS_FLAG] = 1;
+      }
+      return;
     }
     if (lane == 0) loff[NC] = acc;
     __syncwarp();

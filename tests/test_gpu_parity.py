@@ -227,13 +227,20 @@ def test_schedule_batch_and_local_search(O, torch_dev):
             assert r2["makespan"] == full["result"]["makespan"]
 
 
-def test_host_pipeline_matches_device(torch_dev):
+@pytest.mark.parametrize("chunk_mb", [None, "1"])
+def test_host_pipeline_matches_device(torch_dev, monkeypatch, chunk_mb):
+    """far_solve_many_host (H2D / chain / D2H over two streams) == far_solve_many; with 1-MB chunks
+    the 5000 instances cross ~17 chunks alternating between the streams and the workspaces."""
+    if chunk_mb:
+        monkeypatch.setenv("FAR_HOST_CHUNK_MB", chunk_mb)
     w = inputs.WORKLOADS["M3"]
     tab = w.table(count=5000)
     ms, slots, res = run_gpu(torch_dev, w.profile, w.costs(), tab)
     F = far.Far(w.profile, w.costs())
     hms, hsl, hres = F.solve_many_host(tab)
-    assert (hms == ms).all() and (hsl["start"] == slots["start"]).all() and (hres["evals"] == res["evals"]).all()
+    assert (hms == ms).all() and (hsl["start"] == slots["start"]).all() and (hsl["node"] == slots["node"]).all()
+    for k in FIELDS:
+        assert (hres[k] == res[k]).all(), k
 
 
 def test_full_size_m3_parity(O, torch_dev):
