@@ -393,3 +393,22 @@ def test_grow_ties_many_entries(O, torch_dev, n):
     for flags in (far.GROW_TIES | far.NO_REFINE, far.GROW_TIES):
         ms, slots, res = run_gpu(torch_dev, "H100", costs, tab, flags=flags)
         check_against_oracle(O, "H100", costs, tab, ms, slots, res, flags=flags, full=n <= 128)
+
+
+@pytest.mark.skipif(bool(__import__("os").environ.get("FAR_SKIP_FULL_M5")), reason="opt-out")
+def test_full_size_m5_parity(O, torch_dev):
+    """BASELINE configs[4] at full size: all 1M A100 x n=128 instances of the bench workload, the
+    makespan and every report field bit-exact (oracle fanned out over the host cores; ~30 s on the
+    16-core B200 host)."""
+    torch, dev = torch_dev
+    w = inputs.WORKLOADS["M5"]
+    tab = w.table(parallel=True)
+    F = far.Far(w.profile, w.costs())
+    ms, _, rs = F.solve_many(torch.from_numpy(tab).to(dev), sched=False)
+    torch.cuda.synchronize()
+    F.sync()
+    ms, res = ms.cpu().numpy(), far.results_np(rs)
+    oms, ores = O.far_many_parallel(w.profile, w.costs(), tab)
+    assert (ms == oms).all(), f"makespan mismatch at {np.nonzero(ms != oms)[0][:10]}"
+    for k in FIELDS:
+        assert (res[k] == ores[k]).all(), k
