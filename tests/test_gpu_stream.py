@@ -110,3 +110,34 @@ def test_best_improvement_streams(O, torch_dev):
     costs = inputs.reconfig_costs("A30")
     out = run_streams(torch_dev, "A30", costs, tab, flags=far.BEST_IMPROVEMENT)
     check(O, "A30", costs, tab, out, flags=O.BEST_IMPROVEMENT)
+
+
+def _oracle_stream(args):
+    from oracle import oracle as O
+    profile, costs, t = args
+    o = O.stream(profile, costs, t)
+    return (o["makespan"], o["trivial"], o["offsets"], o["seam"], o["violations"],
+            o["results"]["makespan"], o["results"]["moves"], o["results"]["swaps"], o["results"]["evals"],
+            o["slots"]["node"], o["slots"]["start"])
+
+
+@pytest.mark.parametrize("wname", ["M4_A30", "M4_A100"])
+def test_m4_full_size_bitexact(O, torch_dev, wname):
+    """BASELINE configs[3] at the bench's size: all 1024 streams x 64 batches x 64 tasks, every
+    stream makespan, offset, seam record, per-batch report and task slot bit-exact (oracle over the
+    host cores)."""
+    import concurrent.futures as cf
+    import os
+    w = inputs.WORKLOADS[wname]
+    S = 1024
+    tab = inputs.synthetic_parallel(w.profile, w.n, S * 64, w.seed).reshape(S, 64, w.n, -1)
+    sm, off, slots, res, seam = run_streams(torch_dev, w.profile, w.costs(), tab)
+    with cf.ProcessPoolExecutor(os.cpu_count() or 1) as ex:
+        outs = list(ex.map(_oracle_stream, [(w.profile, w.costs(), tab[s]) for s in range(S)], chunksize=16))
+    for s, o in enumerate(outs):
+        assert o[4] == 0
+        assert sm[s, 0] == o[0] and sm[s, 1] == o[1], f"stream {s} makespans"
+        assert (off[s] == o[2]).all() and (seam[s] == o[3]).all(), f"stream {s} offsets / seams"
+        assert (res[s]["makespan"] == o[5]).all() and (res[s]["moves"] == o[6]).all(), f"stream {s} reports"
+        assert (res[s]["swaps"] == o[7]).all() and (res[s]["evals"] == o[8]).all(), f"stream {s} reports"
+        assert (slots[s]["node"] == o[9]).all() and (slots[s]["start"] == o[10]).all(), f"stream {s} slots"
