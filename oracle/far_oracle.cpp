@@ -1195,9 +1195,35 @@ int orc_far_many(int profile, const int32_t* costs, const int32_t* times, int64_
 
 }  // extern "C"
 
+// The fold of orc_stream; with probe_k >= 0 it stops after batch probe_k, which is placed
+// delta ticks before its seam offset (test entry orc_stream_probe: minimality of R23's offset).
+static int stream_fold(int profile, const int32_t* costs, const int32_t* times, int B, int n,
+                       int32_t max_iterations, int32_t ppm, uint32_t flags, int64_t* out2, int64_t* offsets,
+                       int32_t* seam, orc_slot* slots, orc_result* batch_res, int32_t* violations, int probe_k,
+                       int64_t delta);
+
 extern "C" int orc_stream(int profile, const int32_t* costs, const int32_t* times, int B, int n,
                           int32_t max_iterations, int32_t ppm, uint32_t flags, int64_t* out2, int64_t* offsets,
                           int32_t* seam, orc_slot* slots, orc_result* batch_res, int32_t* violations) {
+  return stream_fold(profile, costs, times, B, n, max_iterations, ppm, flags, out2, offsets, seam, slots, batch_res,
+                     violations, -1, 0);
+}
+
+// Test entry: violations of the concatenation of batches 0..k when batch k starts delta ticks
+// before its seam offset (everything else as orc_stream).  *offset_k = the unshifted offset.
+extern "C" int orc_stream_probe(int profile, const int32_t* costs, const int32_t* times, int B, int n, int k,
+                                int64_t delta, int64_t* offset_k, int32_t* violations) {
+  std::vector<int64_t> offs(B > 0 ? B : 1, 0);
+  int rc = stream_fold(profile, costs, times, B, n, 100, 0, 0, nullptr, offs.data(), nullptr, nullptr, nullptr,
+                       violations, k, delta);
+  if (offset_k && k >= 0 && k < B) *offset_k = offs[k];
+  return rc;
+}
+
+static int stream_fold(int profile, const int32_t* costs, const int32_t* times, int B, int n,
+                       int32_t max_iterations, int32_t ppm, uint32_t flags, int64_t* out2, int64_t* offsets,
+                       int32_t* seam, orc_slot* slots, orc_result* batch_res, int32_t* violations, int probe_k,
+                       int64_t delta) {
   const int nc = orc_num_sizes(profile);
   if (nc < 0) return nc;
   if (B < 0 || n < 0) return -1;
@@ -1251,9 +1277,15 @@ extern "C" int orc_stream(int profile, const int32_t* costs, const int32_t* time
     SeamEval ev = seam_offset(mm, st, T);
     int reused = 0;
     for (bool b : ev.reuse) reused += b;
+    if (offsets) offsets[k] = ev.O;
+    if (k == probe_k) {  // probe: place this batch delta ticks early, validate, stop
+      ev.O -= delta;
+      place_batch(Pb[k], S, st, T, ev);
+      if (violations) *violations = validate_stream(mm, st);
+      return 0;
+    }
     place_batch(Pb[k], S, st, T, ev);
     ms = std::max(ms, ev.O + T.task_end);
-    if (offsets) offsets[k] = ev.O;
     if (seam) {
       seam[4 * k + 0] = rev;
       seam[4 * k + 1] = ss.moves;

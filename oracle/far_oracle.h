@@ -75,6 +75,10 @@ int orc_validate(int profile, const int32_t *costs, const int32_t *times, int n,
 /* Lower bound pieces: sum_i min_s s*t_i(s) and max_i min_s t_i(s). */
 int orc_lower_bound(int profile, const int32_t *times, int n, int64_t *sum_min_work, int64_t *max_min_time);
 /* Solve many instances [I][n][|C|] sequentially (for timing the baseline). */
+/* Test entry (oracle pins of the seam offset): violations of the concatenation of batches 0..k
+ * of orc_stream's fold when batch k starts delta ticks before its seam offset. */
+int orc_stream_probe(int profile, const int32_t *costs, const int32_t *times, int B, int n, int k,
+                     int64_t delta, int64_t *offset_k, int32_t *violations);
 int orc_far_many(int profile, const int32_t *costs, const int32_t *times, int64_t I, int n,
                  int32_t max_iterations, int32_t min_improvement_ppm, uint32_t flags,
                  int64_t *makespans, orc_result *res);

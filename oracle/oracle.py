@@ -87,6 +87,8 @@ def lib():
             _lib.orc_stream.argtypes = [C.c_int, p, p, C.c_int, C.c_int, C.c_int32, C.c_int32, C.c_uint32,
                                         p, p, p, p, p, p]
             _lib.orc_stream.restype = C.c_int
+            _lib.orc_stream_probe.argtypes = [C.c_int, p, p, C.c_int, C.c_int, C.c_int, C.c_int64, p, p]
+            _lib.orc_stream_probe.restype = C.c_int
     return _lib
 
 
@@ -257,6 +259,16 @@ def stream(profile, costs, times, max_iterations=100, min_improvement_ppm=0, fla
                             flags, _ptr(out2), _ptr(offs), _ptr(seam), _ptr(slots), _ptr(res), _ptr(viol)))
     return {"makespan": int(out2[0]), "trivial": int(out2[1]), "offsets": offs, "seam": seam, "slots": slots,
             "results": res, "violations": int(viol[0])}
+
+
+def stream_probe(profile, costs, times, k, delta):
+    """(seam offset of batch k, violations of batches 0..k with batch k placed delta ticks early)."""
+    t = _times(times)
+    B, n = t.shape[0], t.shape[1]
+    off = np.zeros(1, np.int64)
+    viol = np.zeros(1, np.int32)
+    _check(lib().orc_stream_probe(pid(profile), _ptr(_costs(costs)), _ptr(t), B, n, k, delta, _ptr(off), _ptr(viol)))
+    return int(off[0]), int(viol[0])
 
 
 def table_stats(profile, costs, tables, max_iterations=100, min_improvement_ppm=0, flags=0):

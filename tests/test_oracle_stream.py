@@ -75,3 +75,25 @@ def test_offset_never_later_than_trivial_start(O):
                 ends.append(starts[q] + (r["slots"][q]["start"] + d).max())
             # all previous tasks end before the trivial start; the smart offset may start earlier
             assert starts[k] <= max(ends) + 2 * 26 * 240
+
+
+@pytest.mark.parametrize("profile", ["A30", "A100"])
+def test_seam_offset_is_least_feasible(O, profile):
+    """R23 defines O_k as the LEAST offset >= max(O_{k-1}, 0) for which B_k's timeline is feasible
+    after the placed batches.  Pinned independently through the stream validator (constraints 1-3
+    across batches, lifecycles): placing B_k one tick earlier must violate something, and placing
+    it at O_k must not (checked wherever O_k is above its lower clamp)."""
+    checked = 0
+    for seed, costs in ((5, inputs.reconfig_costs(profile)), (6, inputs.reconfig_costs(profile, zero=True)),
+                        (7, inputs.reconfig_costs(profile))):
+        tab = inputs.synthetic(profile, 8, 10, seed)
+        r = O.stream(profile, costs, tab)
+        offs = r["offsets"]
+        for k in range(1, len(tab)):
+            o_k, v0 = O.stream_probe(profile, costs, tab, k, 0)
+            assert o_k == offs[k] and v0 == 0
+            if offs[k] > max(offs[k - 1], 0):
+                _, v1 = O.stream_probe(profile, costs, tab, k, 1)
+                assert v1 > 0, f"seed {seed} batch {k}: O_k - 1 = {offs[k] - 1} is feasible"
+                checked += 1
+    assert checked >= 5
