@@ -312,13 +312,15 @@ def main():
     gsched = (torch.empty((I * world, WORKLOAD.n, 8), dtype=torch.uint8, device=dev)
               if world > 1 and args.gather_schedules and backend == "nccl" else None)
 
-    def step(ev=None):
+    def step(ev=None, gev=None):
         if ev is not None:
             ev[0].record(stream)
         F.solve_many(d_times, out=(ms, sd, rs), stream=stream)
         if ev is not None:
             ev[1].record(stream)
         if world > 1:
+            if gev is not None:
+                gev[0].record(stream)
             if backend == "nccl":
                 dist.all_gather_into_tensor(gathered, ms)
                 if gsched is not None:
@@ -326,6 +328,8 @@ def main():
             else:
                 g = torch.empty(I * world, dtype=torch.int32)
                 dist.all_gather_into_tensor(g, ms.cpu())
+            if gev is not None:
+                gev[1].record(stream)
 
     for _ in range(args.warmup):
         step()
@@ -345,8 +349,9 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     t_start.record(stream)
+    gevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for s in range(args.steps):
-        step(kev[s])
+        step(kev[s], gevs[s])
     t_end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -365,15 +370,16 @@ def main():
     moves_swaps = int(res["moves"].sum() + res["swaps"].sum())
 
     # max over ranks
-    t = torch.tensor([total_ms, sum(kern_ms), float(evals_step), float(events_step)], dtype=torch.float64,
+    gather_ms = sum(a.elapsed_time(b) for a, b in gevs) if world > 1 else 0.0
+    t = torch.tensor([total_ms, sum(kern_ms), gather_ms, float(evals_step), float(events_step)], dtype=torch.float64,
                      device=dev if backend == "nccl" else "cpu")
     if world > 1:
-        mx = t.clone()
-        dist.all_reduce(mx[:2], op=dist.ReduceOp.MAX)
-        sm_ = t.clone()
-        dist.all_reduce(sm_[2:], op=dist.ReduceOp.SUM)
-        total_ms, kern_total = float(mx[0]), float(mx[1])
-        evals_all, events_all = float(sm_[2]), float(sm_[3])
+        mx = t[:3].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm_ = t[3:].clone()
+        dist.all_reduce(sm_, op=dist.ReduceOp.SUM)
+        total_ms, kern_total, gather_ms = float(mx[0]), float(mx[1]), float(mx[2])
+        evals_all, events_all = float(sm_[0]), float(sm_[1])
     else:
         kern_total = sum(kern_ms)
         evals_all, events_all = float(evals_step), float(events_step)
@@ -478,6 +484,9 @@ def main():
                        "parallelism": f"dp{world} (instances sharded, NCCL allgather of makespans"
                                   + (" and schedules)" if gsched is not None else ")")},
             "evals_per_s": evals_all / (ms_per_step / 1000.0),
+            "multi_gpu": ({"kernel_ms_per_step_max_rank": kern_total / args.steps,
+                           "allgather_ms_per_step_max_rank": gather_ms / args.steps,
+                           "collective": f"all_gather_into_tensor over {backend}"} if world > 1 else None),
             "alg1_events_simulated_per_s": events_all / (ms_per_step / 1000.0),
             "alg1_events_algorithmic_per_step": alg_events,
             "moves_swaps_per_step": moves_swaps,
