@@ -118,6 +118,12 @@ struct Problem {
   Model m;
   Costs c;
   int n = 0;
+  // Variant ORC_SWITCH_COST (R7 variant): a node hosting two sizes (the A100/H100
+  // {S0..S3} node) runs an instance of its current task's size: created with t_create of
+  // that size, destroyed with t_destroy of that size, and destroyed + re-created (sequentially on
+  // reconfig_end) whenever consecutive tasks on it differ in size.  Default: the literal Alg. 1
+  // (P:418-424): one instance of the node's size, no reconfiguration between its 4- and 3-tasks.
+  bool switch_cost = false;
   std::vector<std::vector<i64>> t;  // t[i][c] = t_i(sizes[c])
   i64 time(int i, int size) const { return t[i][size_index(m, size)]; }
 };
@@ -265,7 +271,12 @@ Sched run_event_loop(const Problem& P, const std::vector<int>* alloc,
 
   std::vector<i64> end(N, 0);
   std::vector<bool> has_tasks(N, false);
+  std::vector<int> inst_size(N, 0);  // size of the node's current instance (switch_cost variant)
   i64 reconfig_end = 0;  // line 3
+  auto cr_of = [&](int v, int size) {
+    return P.switch_cost ? P.c.create[size_index(m, size)] : P.c.cr(m, v);
+  };
+  auto de_of = [&](int v) { return P.switch_cost ? P.c.destroy[size_index(m, inst_size[v])] : P.c.de(m, v); };
   // Min-heap of instances ordered by end time (line 4); ties -> lower first slice (Q8).
   using Key = std::pair<i64, int>;  // (end, lo) ; node recovered from lo via map below
   auto cmp = [](const std::pair<Key, int>& a, const std::pair<Key, int>& b) { return a.first > b.first; };
@@ -290,12 +301,24 @@ Sched run_event_loop(const Problem& P, const std::vector<int>* alloc,
       take_size = (*size_used_in)[take];
     }
     if (take >= 0) {
+      if (has_tasks[v] && P.switch_cost && inst_size[v] != take_size) {
+        // variant: the instance changes size -- destroy it, then create the new one
+        i64 ds = std::max(reconfig_end, end[v]);
+        reconfig_end = ds + de_of(v);
+        S.events.push_back({1, v, ds, de_of(v)});
+        const i64 cs = reconfig_end;
+        reconfig_end = cs + cr_of(v, take_size);
+        S.events.push_back({0, v, cs, cr_of(v, take_size)});
+        end[v] = reconfig_end;
+        inst_size[v] = take_size;
+      }
       if (!has_tasks[v]) {  // lines 8-11: give time for I's creation
         i64 cs = std::max(reconfig_end, end[v]);
-        reconfig_end = cs + P.c.cr(m, v);
-        S.events.push_back({0, v, cs, P.c.cr(m, v)});
+        reconfig_end = cs + cr_of(v, take_size);
+        S.events.push_back({0, v, cs, cr_of(v, take_size)});
         end[v] = reconfig_end;
         has_tasks[v] = true;
+        inst_size[v] = take_size;
       }
       // lines 12-15: longest unscheduled task T_j, executed right after in I
       S.node[take] = v;
@@ -309,8 +332,8 @@ Sched run_event_loop(const Problem& P, const std::vector<int>* alloc,
     } else if (unscheduled > 0) {             // line 17: repartitioning
       if (has_tasks[v]) {                     // lines 18-20: give time to destroy I
         i64 ds = std::max(reconfig_end, end[v]);
-        reconfig_end = ds + P.c.de(m, v);
-        S.events.push_back({1, v, ds, P.c.de(m, v)});
+        reconfig_end = ds + de_of(v);
+        S.events.push_back({1, v, ds, de_of(v)});
       }
       for (int ch : m.node[v].children) {  // lines 21-24
         end[ch] = end[v];
@@ -320,8 +343,8 @@ Sched run_event_loop(const Problem& P, const std::vector<int>* alloc,
       (void)vs;
     } else if (full_lifecycle && has_tasks[v]) {  // drop: final destroy of the lifecycle timeline
       i64 ds = std::max(reconfig_end, end[v]);
-      reconfig_end = ds + P.c.de(m, v);
-      S.events.push_back({1, v, ds, P.c.de(m, v)});
+      reconfig_end = ds + de_of(v);
+      S.events.push_back({1, v, ds, de_of(v)});
     }
     // else: drop the instance (no tasks remain anywhere)
   }
@@ -963,9 +986,16 @@ int orc_family_flags(int profile, const int32_t* times, int n, uint32_t flags, i
 
 int orc_schedule_allocation(int profile, const int32_t* costs, const int32_t* times, int n, const int32_t* alloc,
                             orc_slot* slots, orc_event* ev, int32_t* nev, int64_t* makespan, int64_t* pops) {
+  return orc_schedule_allocation_flags(profile, costs, times, n, alloc, 0, slots, ev, nev, makespan, pops);
+}
+
+int orc_schedule_allocation_flags(int profile, const int32_t* costs, const int32_t* times, int n,
+                                  const int32_t* alloc, uint32_t flags, orc_slot* slots, orc_event* ev, int32_t* nev,
+                                  int64_t* makespan, int64_t* pops) {
   Problem P;
-  int rc = load_problem(profile, costs, times, n, false, P);
+  int rc = load_problem(profile, costs, times, n, (flags & ORC_ZERO_RECONFIG) != 0, P);
   if (rc) return rc;
+  P.switch_cost = (flags & ORC_SWITCH_COST) != 0;
   std::vector<int> a(alloc, alloc + n);
   for (int s : a)
     if (size_index(P.m, s) < 0) return -1;
@@ -982,6 +1012,7 @@ int orc_far(int profile, const int32_t* costs, const int32_t* times, int n, int3
   Problem P;
   int rc = load_problem(profile, costs, times, n, (flags & ORC_ZERO_RECONFIG) != 0, P);
   if (rc) return rc;
+  P.switch_cost = (flags & ORC_SWITCH_COST) != 0;
   orc_result r{};
   // Phase 1 + phase 2 on every member; k* = argmin (makespan_k, k)  (Q13)
   auto fam = allocation_family(P, (flags & ORC_GROW_TIES) != 0);
@@ -1010,6 +1041,7 @@ int orc_refine(int profile, const int32_t* costs, const int32_t* times, int n, i
   Problem P;
   int rc = load_problem(profile, costs, times, n, (flags & ORC_ZERO_RECONFIG) != 0, P);
   if (rc) return rc;
+  P.switch_cost = (flags & ORC_SWITCH_COST) != 0;
   if (!slots || !res) return -1;
   const int N = (int)P.m.node.size();
   // Rebuild the tree from the slots: node lists ordered by start time (then index).
@@ -1082,6 +1114,94 @@ int64_t orc_bruteforce(int profile, const int32_t* times, int n) {
 
 // Constraints 1-3 of P:214-230 plus lifecycle consistency of the explicit
 // reconfiguration events.  Returns the number of violations.
+// Validator of the ORC_SWITCH_COST variant: constraints 1-2 as orc_validate; constraint 3 with
+// instances that change size -- per node the events must alternate create, destroy, create, ...
+// (a final destroy optional); each create/destroy pair is one instance whose tasks all have one
+// size s and lie inside [create end, destroy start), with durations t_create(s) / t_destroy(s);
+// every task lies in exactly one instance of its node; events pairwise disjoint; instances of
+// overlapping nodes disjoint in time.
+static int validate_switch(const Problem& P, const orc_slot* slots, const orc_event* ev, int32_t nev) {
+  const Model& m = P.m;
+  const int N = (int)m.node.size(), n = P.n;
+  int bad = 0;
+  auto overlap = [&](int u, int v) { return m.node[u].lo < m.node[v].hi && m.node[v].lo < m.node[u].hi; };
+  std::vector<i64> b(n), f(n);
+  for (int j = 0; j < n; ++j) {
+    const int v = slots[j].node;
+    if (v < 0 || v >= N) { bad++; continue; }
+    bool hosted = false;
+    for (int h : m.node[v].hosted) hosted |= (h == slots[j].size_used);
+    if (!hosted) { bad++; continue; }
+    b[j] = slots[j].start;
+    f[j] = b[j] + P.time(j, slots[j].size_used);
+    if (b[j] < 0) bad++;
+  }
+  if (bad) return bad;
+  for (int i = 0; i < n; ++i)  // (1)
+    for (int j = i + 1; j < n; ++j)
+      if (overlap(slots[i].node, slots[j].node) && b[i] < f[j] && b[j] < f[i]) bad++;
+  for (int k = 0; k < n; ++k) {  // (2)
+    std::vector<int> run;
+    for (int j = 0; j < n; ++j)
+      if (b[j] <= b[k] && b[k] < f[j]) run.push_back(slots[j].node);
+    for (size_t x = 0; x < run.size(); ++x)
+      for (size_t y = x + 1; y < run.size(); ++y)
+        if (run[x] != run[y] && overlap(run[x], run[y])) bad++;
+  }
+  for (int e = 0; e < nev; ++e) {  // (3) sequential reconfiguration
+    if (ev[e].node < 0 || ev[e].node >= N || ev[e].start < 0) { bad++; continue; }
+    for (int g = e + 1; g < nev; ++g)
+      if (ev[e].start < ev[g].start + ev[g].dur && ev[g].start < ev[e].start + ev[e].dur) bad++;
+  }
+  struct Inst { int node; i64 cs, de; };
+  std::vector<Inst> inst;
+  std::vector<int> covered(n, 0);
+  for (int v = 0; v < N; ++v) {
+    std::vector<orc_event> E;
+    for (int e = 0; e < nev; ++e)
+      if (ev[e].node == v) E.push_back(ev[e]);
+    std::sort(E.begin(), E.end(), [](const orc_event& x, const orc_event& y) { return x.start < y.start; });
+    for (size_t q = 0; q < E.size(); q += 2) {
+      if (E[q].kind != 0 || (q + 1 < E.size() && E[q + 1].kind != 1)) { bad++; break; }
+      const i64 cs = E[q].start, ce = cs + E[q].dur;
+      const bool closed = q + 1 < E.size();
+      const i64 ds = closed ? E[q + 1].start : std::numeric_limits<i64>::max();
+      const i64 de = closed ? ds + E[q + 1].dur : ds;
+      int size = -1, ntask = 0;
+      for (int j = 0; j < n; ++j) {
+        if (slots[j].node != v || b[j] < ce || f[j] > ds) continue;
+        ntask++;
+        covered[j]++;
+        if (size < 0) size = slots[j].size_used;
+        else if (size != slots[j].size_used) bad++;
+      }
+      if (ntask == 0) { bad++; continue; }
+      if (E[q].dur != P.c.create[size_index(m, size)]) bad++;
+      if (closed && E[q + 1].dur != P.c.destroy[size_index(m, size)]) bad++;
+      inst.push_back({v, cs, de});
+    }
+  }
+  for (int j = 0; j < n; ++j)
+    if (covered[j] != 1) bad++;
+  for (size_t x = 0; x < inst.size(); ++x)
+    for (size_t y = x + 1; y < inst.size(); ++y) {
+      if (inst[x].node == inst[y].node || !overlap(inst[x].node, inst[y].node)) continue;
+      const Inst& a = inst[x].cs < inst[y].cs ? inst[x] : inst[y];
+      const Inst& c = inst[x].cs < inst[y].cs ? inst[y] : inst[x];
+      if (a.de > c.cs) bad++;
+    }
+  return bad;
+}
+
+int orc_validate_flags(int profile, const int32_t* costs, const int32_t* times, int n, const orc_slot* slots,
+                       const orc_event* ev, int32_t nev, uint32_t flags) {
+  if (!(flags & ORC_SWITCH_COST)) return orc_validate(profile, costs, times, n, slots, ev, nev);
+  Problem P;
+  int rc = load_problem(profile, costs, times, n, costs == nullptr, P);
+  if (rc) return 1000000 - rc;
+  return validate_switch(P, slots, ev, nev);
+}
+
 int orc_validate(int profile, const int32_t* costs, const int32_t* times, int n, const orc_slot* slots,
                  const orc_event* ev, int32_t nev) {
   Problem P;
@@ -1233,6 +1353,7 @@ static int stream_fold(int profile, const int32_t* costs, const int32_t* times, 
   for (int k = 0; k < B; ++k) {
     int rc = load_problem(profile, costs, times + (size_t)k * n * nc, n, (flags & ORC_ZERO_RECONFIG) != 0, Pb[k]);
     if (rc) return rc;
+    Pb[k].switch_cost = (flags & ORC_SWITCH_COST) != 0;
     const Problem& P = Pb[k];
     orc_result r{};
     auto fam = allocation_family(P, (flags & ORC_GROW_TIES) != 0);

@@ -40,8 +40,11 @@ typedef struct {
 /* ORC_BEST_IMPROVEMENT: reading variant (SURVEY.md §0 discrepancy 2 / NEXT-3, R30): phase 3
  * scores every same-size move and every swap pair by the resulting (makespan, #critical slices) and
  * applies the argmin while it improves (default: Alg. 2). */
+/* ORC_SWITCH_COST: reading variant (R7): the A100/H100 {S0..S3} node
+ * runs an instance of its current task's size (create/destroy cost of that size) and is destroyed and
+ * re-created when it switches from its size-4 to its size-3 tasks (default: Alg. 1 literally). */
 enum { ORC_NO_REFINE = 1u, ORC_NO_GUARD = 2u, ORC_ZERO_RECONFIG = 4u, ORC_NONEMPTY_ALT = 32u, ORC_NO_SEAM_MOVES = 64u,
-       ORC_GROW_TIES = 128u, ORC_BEST_IMPROVEMENT = 256u };
+       ORC_GROW_TIES = 128u, ORC_BEST_IMPROVEMENT = 256u, ORC_SWITCH_COST = 512u };
 
 int orc_num_sizes(int profile);
 int orc_num_nodes(int profile);
@@ -67,6 +70,12 @@ int orc_far(int profile, const int32_t *costs, const int32_t *times, int n, int3
 int orc_refine(int profile, const int32_t *costs, const int32_t *times, int n, int32_t max_iterations,
                int32_t min_improvement_ppm, uint32_t flags, orc_slot *slots, orc_result *res,
                orc_event *ev, int32_t *nev);
+int orc_schedule_allocation_flags(int profile, const int32_t *costs, const int32_t *times, int n,
+                                  const int32_t *alloc, uint32_t flags, orc_slot *slots, orc_event *ev,
+                                  int32_t *nev, int64_t *makespan, int64_t *pops);
+/* orc_validate, or with ORC_SWITCH_COST the validator of that variant (instances change size). */
+int orc_validate_flags(int profile, const int32_t *costs, const int32_t *times, int n, const orc_slot *slots,
+                       const orc_event *ev, int32_t nev, uint32_t flags);
 /* Zero-reconfiguration optimum by exhaustive branch and bound (tiny n). */
 int64_t orc_bruteforce(int profile, const int32_t *times, int n);
 /* Constraints 1-3 + lifecycle checks; returns #violations (0 = feasible). */

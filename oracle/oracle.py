@@ -17,7 +17,8 @@ LIB = os.path.join(HERE, "liboracle.so")
 SOURCES = ["far_oracle.cpp"]
 
 PROFILES = {"A30": 0, "A100": 1, "H100": 2}
-NO_REFINE, NO_GUARD, ZERO_RECONFIG, NONEMPTY_ALT, NO_SEAM_MOVES, GROW_TIES, BEST_IMPROVEMENT = 1, 2, 4, 32, 64, 128, 256
+NO_REFINE, NO_GUARD, ZERO_RECONFIG, NONEMPTY_ALT, NO_SEAM_MOVES, GROW_TIES, BEST_IMPROVEMENT, SWITCH_COST = \
+    1, 2, 4, 32, 64, 128, 256, 512
 
 
 def build(force: bool = False) -> str:
@@ -77,6 +78,8 @@ def lib():
             ("orc_refine", [C.c_int, p, p, C.c_int, C.c_int32, C.c_int32, C.c_uint32, p, p, p, p], C.c_int),
             ("orc_bruteforce", [C.c_int, p, C.c_int], C.c_int64),
             ("orc_validate", [C.c_int, p, p, C.c_int, p, p, C.c_int32], C.c_int),
+            ("orc_validate_flags", [C.c_int, p, p, C.c_int, p, p, C.c_int32, C.c_uint32], C.c_int),
+            ("orc_schedule_allocation_flags", [C.c_int, p, p, C.c_int, p, C.c_uint32, p, p, p, p, p], C.c_int),
             ("orc_lower_bound", [C.c_int, p, C.c_int, p, p], C.c_int),
             ("orc_far_many", [C.c_int, p, p, C.c_int64, C.c_int, C.c_int32, C.c_int32, C.c_uint32, p, p], C.c_int),
             ("orc_seam_offset_simple", [C.c_int, p, p], C.c_int64),
@@ -144,7 +147,7 @@ def family(profile, times, flags=0):
     return out[:K].copy()
 
 
-def schedule_allocation(profile, costs, times, alloc):
+def schedule_allocation(profile, costs, times, alloc, flags=0):
     t = _times(times)
     n = t.shape[0]
     a = np.ascontiguousarray(alloc, dtype=np.int32)
@@ -153,8 +156,8 @@ def schedule_allocation(profile, costs, times, alloc):
     nev = np.zeros(1, np.int32)
     ms = np.zeros(1, np.int64)
     pops = np.zeros(1, np.int64)
-    _check(lib().orc_schedule_allocation(pid(profile), _ptr(_costs(costs)), _ptr(t), n, _ptr(a), _ptr(slots),
-                                         _ptr(ev), _ptr(nev), _ptr(ms), _ptr(pops)))
+    _check(lib().orc_schedule_allocation_flags(pid(profile), _ptr(_costs(costs)), _ptr(t), n, _ptr(a), flags,
+                                               _ptr(slots), _ptr(ev), _ptr(nev), _ptr(ms), _ptr(pops)))
     return {"slots": slots, "events": ev[:nev[0]].copy(), "makespan": int(ms[0]), "pops": int(pops[0])}
 
 
@@ -191,11 +194,12 @@ def bruteforce(profile, times):
     return int(v)
 
 
-def validate(profile, costs, times, slots, events):
+def validate(profile, costs, times, slots, events, flags=0):
     t = _times(times)
     s = np.ascontiguousarray(slots, dtype=SLOT_DT)
     e = np.ascontiguousarray(events)
-    return lib().orc_validate(pid(profile), _ptr(_costs(costs)), _ptr(t), t.shape[0], _ptr(s), _ptr(e), len(e))
+    return lib().orc_validate_flags(pid(profile), _ptr(_costs(costs)), _ptr(t), t.shape[0], _ptr(s), _ptr(e), len(e),
+                                    flags)
 
 
 def lower_bound(profile, times):

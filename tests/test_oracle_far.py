@@ -383,3 +383,45 @@ def test_multi_gpu_feasible_and_bounded(O, prof):
     # family member), so w_FAR = t(largest size) = the lower bound max_i min_s t_i(s)
     t = np.tile(inputs.synthetic(base, 1, 1, 9)[0], (g, 1))
     assert O.far(prof, None, t)["result"]["makespan"] == int(t[0].min())
+
+
+# ----------------------------------------------------------------- 4->3 switch-cost variant (R7)
+@pytest.mark.parametrize("case", GOLD["switch_cost"], ids=["switch", "create3"])
+def test_switch_cost_traces(O, case):
+    t = _t(case["times"], case["profile"])
+    costs = inputs.reconfig_costs(case["profile"])
+    for key, flags in (("default", 0), ("switch", O.SWITCH_COST)):
+        r = O.schedule_allocation(case["profile"], costs, t, case["alloc"], flags=flags)
+        assert r["makespan"] == case[key]["makespan"], key
+        assert r["slots"]["start"].tolist() == case[key]["starts"], key
+        assert [list(map(int, e)) for e in r["events"]] == case[key]["events"], key
+        assert O.validate(case["profile"], costs, t, r["slots"], r["events"], flags=flags) == 0
+
+
+@pytest.mark.parametrize("profile", ["A30", "A100", "H100"])
+def test_switch_cost_invariants(O, profile):
+    """Zero reconfiguration: the variant equals the literal reading exactly; A30 (no two-size
+    node): equal with costs too; with costs: feasible under the variant's validator, and
+    non-vacuous (some outputs re-create the {S0..S3} instance)."""
+    costs = inputs.reconfig_costs(profile)
+    zero = inputs.reconfig_costs(profile, zero=True)
+    switched = 0
+    for t in list(inputs.synthetic(profile, 16, 30, 61)) + list(inputs.monotone_ties(profile, 12, 20, 62)):
+        a = O.far(profile, zero, t)
+        b = O.far(profile, zero, t, flags=O.SWITCH_COST)
+        assert a["result"] == b["result"] and (a["slots"] == b["slots"]).all()
+        r = O.far(profile, costs, t, flags=O.SWITCH_COST)
+        assert O.validate(profile, costs, t, r["slots"], r["events"], flags=O.SWITCH_COST) == 0
+        if profile == "A30":
+            d = O.far(profile, costs, t)
+            assert d["result"] == r["result"] and (d["slots"] == r["slots"]).all()
+        ncreate1 = sum(1 for e in r["events"] if e["kind"] == 0 and e["node"] == 1)
+        switched += ncreate1 > 1
+        if ncreate1 > 1:  # the literal validator rejects a re-created node; dropping the switch is caught
+            assert O.validate(profile, costs, t, r["slots"], r["events"]) > 0
+            keep = [e for e in r["events"] if not (e["node"] == 1 and e["kind"] == 1 and e["start"] < max(
+                x["start"] for x in r["events"] if x["node"] == 1))]
+            assert O.validate(profile, costs, t, r["slots"], np.array(keep, r["events"].dtype),
+                              flags=O.SWITCH_COST) > 0
+    if profile != "A30":
+        assert switched > 0
