@@ -81,7 +81,14 @@ enum {
                              scores every move to a same-size node and every swap pair on two
                              same-size nodes by (max slice end, #slices at it) and applies the
                              argmin while it improves; evals = candidates scored (default: Alg. 2,
-                             P:495-560, FAR_NONEMPTY_ALT ignored) */
+                             P:495-560, FAR_NONEMPTY_ALT ignored) */,
+  FAR_SWITCH_COST = 512u  /* reading variant (R7): the A100/H100 {S0..S3}
+                             node runs an instance of its current task's size -- created with
+                             t_create and destroyed with t_destroy of that size -- and is destroyed
+                             and re-created (sequentially) when it switches from its size-4 to its
+                             size-3 tasks (default: Alg. 1 literally, one size-4 instance).  Runs the
+                             fused kernel; far_concat_streams, far_schedule_events and
+                             far_validate_schedules reject it (FAR_E_INVALID_ARG) */
 };
 
 typedef struct {

@@ -268,8 +268,9 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
   int kfast = std::min(kmax, kcap_fast);
   if (P.mode != MODE_SOLVE) kfast = 1;
   // small batches (latency): the fused warp-per-instance kernel is one launch instead of five
+  // (the reading variant FAR_SWITCH_COST runs the fused kernel only)
   const bool pipe = P.mode == MODE_SOLVE && P.n > 0 && P.n <= 1023 && !getenv("FAR_FUSED_PHASE2") &&
-                    (P.I >= 256 || getenv("FAR_PIPELINE_ALWAYS"));
+                    !(P.flags & FAR_SWITCH_COST) && (P.I >= 256 || getenv("FAR_PIPELINE_ALWAYS"));
   const bool need_ovf = P.mode == MODE_SOLVE && (kfast < kmax || pipe);
   const int slot = (ctx->launch_id++ % (RING / 8)) * 8;
   CK(cudaMemsetAsync(ctx->d_counter + slot, 0, 8 * sizeof(unsigned long long), stream));
@@ -752,6 +753,7 @@ extern "C" far_status far_concat_streams(far_ctx* ctx, const int32_t* d_times, i
                                          void* cuda_stream) {
   if (!ctx) return FAR_E_INVALID_ARG;
   if (ctx->gpus > 1) return fail(ctx, FAR_E_UNSUPPORTED_PROFILE, "streams: single-GPU trees only");
+  if (opts && (opts->flags & FAR_SWITCH_COST)) return fail(ctx, FAR_E_INVALID_ARG, "streams: no FAR_SWITCH_COST");
   if (S < 0 || B < 0 || n < 0) return fail(ctx, FAR_E_INVALID_ARG, "negative S, B or n");
   if (n > MAXN) return fail(ctx, FAR_E_TOO_LARGE, "n > 1024");
   if (S > 0 && B > 0 && (!d_stream_makespan || !d_offsets || (n > 0 && !d_times)))
@@ -849,6 +851,8 @@ static far_status launch_check(far_ctx* ctx, CParams& Q, int64_t I, int n, bool 
 static far_status check_args(far_ctx* ctx, const int32_t* d_times, int64_t I, int32_t n, const far_task_slot* d_sched,
                              const far_opts* opts, CParams& Q) {
   if (ctx->gpus > 1) return fail(ctx, FAR_E_UNSUPPORTED_PROFILE, "events / validator: single-GPU trees only");
+  if (opts && (opts->flags & FAR_SWITCH_COST))
+    return fail(ctx, FAR_E_INVALID_ARG, "events / validator: no FAR_SWITCH_COST");
   if (I < 0 || n < 0) return fail(ctx, FAR_E_INVALID_ARG, "negative I or n");
   if (n > MAXN) return fail(ctx, FAR_E_TOO_LARGE, "n > 1024");
   if (I > 0 && n > 0 && (!d_times || !d_sched)) return fail(ctx, FAR_E_INVALID_ARG, "null device pointer");

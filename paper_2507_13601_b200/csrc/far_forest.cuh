@@ -49,7 +49,7 @@ __device__ __forceinline__ int fn_par(uint2 w) { return (int)((w.y >> 16) & 255u
 // per-warp shared-memory layout (bytes)
 struct FLay {
   int T, glist, cur, rs[2], rn[2], rp[2], ru[2], ncnt, L, off, cursor, send, D, Q, opened, leaf, misc, tnode, srt,
-      nstat, bytes;
+      nstat, isz, bytes;
 };
 __host__ __device__ inline FLay make_flay(int n, int NC, int NNF, int SF) {
   FLay L;
@@ -77,6 +77,7 @@ __host__ __device__ inline FLay make_flay(int n, int NC, int NNF, int SF) {
   L.tnode = take(n);        // best-improvement: node of each task
   L.srt = take(8 * SF);     // best-improvement: slice ends sorted descending (value, slice)
   L.nstat = take(8 * NNF);  // best-improvement: (max, count) of each node's slice ends
+  L.isz = take(NNF);        // FAR_SWITCH_COST: size index of each node's current instance
   L.bytes = o;
   return L;
 }
@@ -88,9 +89,11 @@ enum { FM_GCNT = 0, FM_GPTR = 8, FM_END = 16 };
 template <int NC, bool LISTS>
 __device__ int forest_sim(const FParams& F, int n, const int32_t* T, const uint16_t* glist, const int* gcnt, int* gptr,
                           const uint16_t* L, const int* off, int* cursor, const uint8_t* su, int* rstart,
-                          uint8_t* rnode, uint8_t* rpos, uint8_t* rsu, int* ncnt, long long& pops, int lane) {
+                          uint8_t* rnode, uint8_t* rpos, uint8_t* rsu, int* ncnt, long long& pops, int lane,
+                          uint8_t* isz) {
   const KParams& P = F.P;
   const int NNF = F.NNF;
+  const bool r7 = (P.flags & FAR_SWITCH_COST) != 0;  // DESIGN.md R7 variant
   for (int v = lane; v < NNF; v += 32) {
     ncnt[v] = 0;
     if (LISTS) cursor[v] = off[v];
@@ -121,6 +124,7 @@ __device__ int forest_sim(const FParams& F, int n, const int32_t* T, const uint1
     int end = (int)emin;
     ++pops;
     const uint2 w = __ldg(F.nodes + v);
+    const int cur_isz = isz[v];
     int take = -1, tc = 0;
     if (LISTS) {
       if (cursor[v] < off[v + 1]) {
@@ -143,9 +147,15 @@ __device__ int forest_sim(const FParams& F, int n, const int32_t* T, const uint1
     if (take >= 0) {
       if (!has) {  // lines 8-11: give time for I's creation
         const int cs = max(rec, end);
-        rec = cs + P.cr[fn_szi(w)];
+        rec = cs + P.cr[r7 ? tc : fn_szi(w)];
         end = rec;
         has = 1;
+        if (lane == 0) isz[v] = (uint8_t)tc;
+      } else if (r7 && fn_c1(w) != NONE && tc != cur_isz) {  // variant: destroy, then re-create
+        rec = max(rec, end) + P.de[cur_isz];
+        rec += P.cr[tc];
+        end = rec;
+        if (lane == 0) isz[v] = (uint8_t)tc;
       }
       const int st = end;
       end += T[take * NC + tc];
@@ -162,7 +172,7 @@ __device__ int forest_sim(const FParams& F, int n, const int32_t* T, const uint1
       nslot_node = v;
       ne = end;
     } else if (unsched > 0) {  // line 17: repartition
-      if (has) rec = max(rec, end) + P.de[fn_szi(w)];  // lines 18-20
+      if (has) rec = max(rec, end) + P.de[(r7 && fn_c1(w) != NONE) ? cur_isz : fn_szi(w)];  // lines 18-20
       if (fn_ch1(w) == FNONE) {
         clear = true;
       } else {  // lines 21-24: children start at I.end
@@ -597,7 +607,7 @@ __global__ void __launch_bounds__(128) far_forest_kernel(FParams F) {
           const int bb = b2 ^ 1;
           const int ms = forest_sim<NC, false>(F, n, T, glist, gcnt, gptr, L, off, cursor, cur,
                                                (int*)(wsm + Ly.rs[bb]), wsm + Ly.rn[bb], wsm + Ly.rp[bb],
-                                               wsm + Ly.ru[bb], ncnt, pops, lane);
+                                               wsm + Ly.ru[bb], ncnt, pops, lane, wsm + Ly.isz);
           if (ms < best) { best = ms; bestk = K; b2 = bb; }
         }
         ++K;
@@ -755,7 +765,8 @@ __global__ void __launch_bounds__(128) far_forest_kernel(FParams F) {
       const int ob = b2 ^ 1;
       long long rp_pops = 0;
       const int msR = forest_sim<NC, true>(F, n, T, glist, gcnt, gptr, L, off, cursor, ru2, (int*)(wsm + Ly.rs[ob]),
-                                           wsm + Ly.rn[ob], wsm + Ly.rp[ob], wsm + Ly.ru[ob], ncnt, rp_pops, lane);
+                                           wsm + Ly.rn[ob], wsm + Ly.rp[ob], wsm + Ly.ru[ob], ncnt, rp_pops, lane,
+                                           wsm + Ly.isz);
       if (!(P.flags & FAR_NO_GUARD) && msR > ms2) {
         R.reverted = 1;
       } else {

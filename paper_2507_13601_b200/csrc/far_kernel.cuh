@@ -304,6 +304,76 @@ __device__ int replay_warp(int n, const int* D, const uint16_t* nlist, const int
   return ms;
 }
 
+// Task-level replay (Alg. 2 line 26) for the reading variant FAR_SWITCH_COST (R7): the
+// Alg. 1 event loop taking each node's tasks from its list, where the two-size {S0..S3} node
+// runs an instance of its task's size (su[j]) -- created with that size's cost, destroyed and
+// re-created when consecutive tasks differ in size -- so a node's tasks no longer run back to
+// back and the node-level replay does not apply.  Frontier spread over the lanes as in
+// node_sim_warp; cursor[NN] is scratch.  Writes start[j], onode[j]; returns the makespan.
+template <int NC>
+__device__ __noinline__ int replay_tasks_warp(int n, const int* D, const uint16_t* nlist, const int* ncnt,
+                                              const uint8_t* su, int* cursor, int* start, uint8_t* onode,
+                                              const uint32_t* ninfo, const int* cr, const int* de, int lane) {
+  constexpr int NN = Tree<NC>::NN;
+  if (lane < NN) cursor[lane] = 0;
+  __syncwarp();
+  unsigned e = lane == 0 ? 0u : 0xFFFFFFFFu;  // root in slot 0 at time 0
+  uint32_t slotnode = 0, live = 1, has = 0;
+  int rec = 0, ms = 0, unsched = n, isz = 0;
+  while (live) {
+    const unsigned m = __reduce_min_sync(FULL, e);
+    const int bs = (int)(m & 7u);
+    int be = (int)(m >> 3);
+    const int v = (int)((slotnode >> (4 * bs)) & 15u);
+    const uint32_t w = ninfo[v];
+    const int q = cursor[v];
+    __syncwarp();
+    if (q < ncnt[v]) {  // lines 7-16: the node's next task
+      const int j = nlist[v * n + q];
+      const int c = su[j];
+      if (!((has >> bs) & 1)) {
+        rec = max(rec, be) + cr[c];
+        be = rec;
+        has |= 1u << bs;
+        if (nd_c1(w) != NONE) isz = c;  // the (one) two-size node's instance
+      } else if (nd_c1(w) != NONE && c != isz) {  // the instance changes size
+        rec = max(rec, be) + de[isz];
+        rec += cr[c];
+        be = rec;
+        isz = c;
+      }
+      if (lane == 0) {
+        start[j] = be;
+        onode[j] = (uint8_t)v;
+        cursor[v] = q + 1;
+      }
+      be += D[j];
+      ms = max(ms, be);
+      --unsched;
+      if (lane == bs) e = ((unsigned)be << 3) | (unsigned)bs;
+    } else if (unsched > 0) {  // lines 17-24
+      if ((has >> bs) & 1) rec = max(rec, be) + de[nd_c1(w) != NONE ? isz : nd_szi(w)];
+      has &= ~(1u << bs);
+      const int ch1 = nd_ch1(w);
+      if (ch1 != LEAF) {
+        const int s2 = nd_ch2lo(w);
+        slotnode = (slotnode & ~(15u << (4 * bs))) | ((uint32_t)ch1 << (4 * bs));
+        slotnode = (slotnode & ~(15u << (4 * s2))) | ((uint32_t)nd_ch2(w) << (4 * s2));
+        live |= 1u << s2;
+        if (lane == s2) e = ((unsigned)be << 3) | (unsigned)s2;
+      } else {
+        live &= ~(1u << bs);
+        if (lane == bs) e = 0xFFFFFFFFu;
+      }
+    } else {  // drop
+      live &= ~(1u << bs);
+      if (lane == bs) e = 0xFFFFFFFFu;
+    }
+    __syncwarp();
+  }
+  return ms;
+}
+
 // ---------------------------------------------------------------------------
 // Phase 3: Alg. 2 on node lists (warp-cooperative).  sliceEnd in smem.
 // ---------------------------------------------------------------------------
@@ -828,7 +898,9 @@ __device__ __noinline__ void solve_local(const KParams& P, int64_t inst, unsigne
         refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, (P.flags & FAR_NONEMPTY_ALT) != 0, lane, mv,
                         sw, it, ev);
       R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
-      const int msR = replay_warp<NC>(n, D, nlist, ncnt, nsum, life, start, bestnode, ninfo, cr, de, lane);
+      const int msR = (P.flags & FAR_SWITCH_COST)
+                          ? replay_tasks_warp<NC>(n, D, nlist, ncnt, su, nsum, start, bestnode, ninfo, cr, de, lane)
+                          : replay_warp<NC>(n, D, nlist, ncnt, nsum, life, start, bestnode, ninfo, cr, de, lane);
       if (!(P.flags & FAR_NO_GUARD) && msR > ms2) {
         R.reverted = 1;
       } else {
@@ -921,7 +993,9 @@ __device__ void finish_core(const KParams& P, int64_t inst, uint16_t* nlist, int
       R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
     }
     if (!need_replay) break;
-    const int msR = replay_warp<NC>(n, D, nlist, ncnt, nsum, life, start, onode, ninfo, cr, de, lane);
+    const int msR = (P.flags & FAR_SWITCH_COST)
+                        ? replay_tasks_warp<NC>(n, D, nlist, ncnt, su, nsum, start, onode, ninfo, cr, de, lane)
+                        : replay_warp<NC>(n, D, nlist, ncnt, nsum, life, start, onode, ninfo, cr, de, lane);
     if (ref && !(P.flags & FAR_NO_GUARD) && msR > ms2) {
       R.reverted = 1;  // keep-best guard: return the phase-2 schedule (replayed in pass 1)
       if (!want_sched) break;
@@ -1518,6 +1592,9 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
   // (H2) is >= the best makespan of the earlier passes cannot become k* = argmin
   // (makespan, k) and is skipped (exact; FAR_EXHAUSTIVE disables it).
   const bool prune = !(P.flags & FAR_EXHAUSTIVE);
+  // reading variant FAR_SWITCH_COST (R7): the two-size {S0..S3} node runs an instance of
+  // its task's size (isz) and is destroyed + re-created when the size changes
+  const bool r7 = (P.flags & FAR_SWITCH_COST) != 0;
   int* memb = misc + M_MEMB;
   int nextk = 0;
   while (nextk < K) {
@@ -1555,7 +1632,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       }
       Frontier<S> F;
       F.init();
-      int rec = 0;
+      int rec = 0, isz = 0;
       ms = 0;
 #pragma unroll
       for (int s = 0; s < S; ++s) sl[s] = 0;
@@ -1575,9 +1652,15 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
         ++pops;
         if (sv >> 16) {
           if (!((F.has >> bs) & 1)) {  // lines 8-11: creation, sequenced on reconfig_end
-            rec = max(rec, be) + cr[nd_szi(w)];
+            rec = max(rec, be) + cr[r7 ? c : nd_szi(w)];
             be = rec;
             F.has |= 1u << bs;
+            if (nd_c1(w) != NONE) isz = c;  // the (one) two-size node's instance
+          } else if (r7 && nd_c1(w) != NONE && c != isz) {  // variant: destroy, then re-create
+            rec = max(rec, be) + de[isz];
+            rec += cr[c];
+            be = rec;
+            isz = c;
           }
           // line 12: longest unscheduled task of size c for member k (skip other members'
           // entries; two entries per step -- the list has one padding entry)
@@ -1596,7 +1679,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
           --total;
           F.set(bs, be);
         } else {  // lines 17-24 (total > 0 here)
-          if ((F.has >> bs) & 1) rec = max(rec, be) + de[nd_szi(w)];
+          if ((F.has >> bs) & 1) rec = max(rec, be) + de[(r7 && nd_c1(w) != NONE) ? isz : nd_szi(w)];
           if (!F.split(bs, be, w)) {  // a removed leaf keeps its slice end
 #pragma unroll
             for (int s = 0; s < S; ++s) sl[s] = (s == bs) ? be : sl[s];

@@ -20,7 +20,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "far.h")
 
 PROFILES = {"A30": 0, "A100": 1, "H100": 2}
 NO_REFINE, NO_GUARD, ZERO_RECONFIG, NO_SCHEDULE, EXHAUSTIVE, NONEMPTY_ALT, NO_SEAM_MOVES, GROW_TIES, \
-    BEST_IMPROVEMENT = 1, 2, 4, 8, 16, 32, 64, 128, 256
+    BEST_IMPROVEMENT, SWITCH_COST = 1, 2, 4, 8, 16, 32, 64, 128, 256, 512
 STATUS = {0: "FAR_OK", 1: "FAR_E_INVALID_ARG", 2: "FAR_E_UNSUPPORTED_PROFILE", 3: "FAR_E_BAD_TIME",
           4: "FAR_E_TOO_LARGE", 5: "FAR_E_CUDA", 6: "FAR_E_OOM"}
 

@@ -13,7 +13,7 @@ from test_gpu_parity import check_against_oracle, run_gpu
 pytestmark = pytest.mark.gpu
 
 FLAG_POOL = ("NO_GUARD", "NONEMPTY_ALT", "GROW_TIES", "EXHAUSTIVE", "BEST_IMPROVEMENT", "ZERO_RECONFIG",
-             "NO_REFINE")
+             "NO_REFINE", "SWITCH_COST")
 
 
 @pytest.fixture(scope="module")
@@ -171,7 +171,7 @@ def test_random_local_search(O, torch_dev, seed):
     F = far.Far(prof, costs)
     oslots = np.zeros(n, O.SLOT_DT)
     oslots["node"], oslots["size_used"], oslots["start"] = s["node"], s["size_used"], s["start"]
-    for fname in ("", "NO_GUARD", "NONEMPTY_ALT", "BEST_IMPROVEMENT"):
+    for fname in ("", "NO_GUARD", "NONEMPTY_ALT", "BEST_IMPROVEMENT", "SWITCH_COST"):
         flags = getattr(far, fname) if fname else 0
         oflags = getattr(O, fname) if fname else 0
         mi = int(rng.choice([0, 1, 100]))

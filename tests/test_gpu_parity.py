@@ -52,7 +52,8 @@ def run_gpu(torch_dev, profile, costs, tab, **kw):
 
 
 def check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=0, max_iterations=100, ppm=0, full=True):
-    oflags = flags & (O.NO_REFINE | O.NO_GUARD | O.ZERO_RECONFIG | O.NONEMPTY_ALT | O.GROW_TIES | O.BEST_IMPROVEMENT)
+    oflags = flags & (O.NO_REFINE | O.NO_GUARD | O.ZERO_RECONFIG | O.NONEMPTY_ALT | O.GROW_TIES | O.BEST_IMPROVEMENT |
+                      O.SWITCH_COST)
     oms, ores = O.far_many(profile, costs, tab, max_iterations=max_iterations, min_improvement_ppm=ppm, flags=oflags)
     bad = np.nonzero(ms != oms)[0]
     assert len(bad) == 0, f"makespan mismatch at {bad[:10]}: gpu {ms[bad[:5]]} oracle {oms[bad[:5]]}"
@@ -412,3 +413,47 @@ def test_full_size_m5_parity(O, torch_dev):
     assert (ms == oms).all(), f"makespan mismatch at {np.nonzero(ms != oms)[0][:10]}"
     for k in FIELDS:
         assert (res[k] == ores[k]).all(), k
+
+
+@pytest.mark.parametrize("profile,gen,n", [("A100", "mixed", 16), ("H100", "mixed", 40), ("A100", "ties", 24),
+                                           ("A100", "monoties", 24), ("A30", "mixed", 12), ("A100", "mixed", 300)])
+def test_switch_cost_variant(O, torch_dev, profile, gen, n):
+    """The NEXT-3 variant FAR_SWITCH_COST (R7: the {S0..S3} node re-created on a 4->3
+    switch, instances created / destroyed at their task size) against the oracle; non-vacuous."""
+    costs = inputs.reconfig_costs(profile)
+    count = 30 if n > 256 else 300
+    tab = {"mixed": inputs.synthetic, "ties": inputs.small_ties, "monoties": inputs.monotone_ties}[gen](
+        profile, n, count, 90 + n)
+    _, _, r0 = run_gpu(torch_dev, profile, costs, tab)
+    for flags in (far.SWITCH_COST, far.SWITCH_COST | far.NO_GUARD, far.SWITCH_COST | far.EXHAUSTIVE | far.GROW_TIES,
+                  far.SWITCH_COST | far.BEST_IMPROVEMENT, far.SWITCH_COST | far.NO_REFINE):
+        ms, slots, res = run_gpu(torch_dev, profile, costs, tab, flags=flags)
+        check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=flags, full=n <= 64)
+        if flags == far.SWITCH_COST and profile != "A30":
+            assert (res["makespan_phase2"] != r0["makespan_phase2"]).any()
+
+
+def test_switch_cost_local_search_and_forest(O, torch_dev):
+    for prof in ("A100", "H100x2"):
+        base = prof.split("x")[0]
+        costs = inputs.reconfig_costs(base)
+        F = far.Far(prof, costs)
+        for t in inputs.synthetic(base, 20, 20, 92):
+            s, r = F.schedule_batch(t, flags=far.SWITCH_COST)
+            o = O.far(prof, costs, t, flags=O.NO_REFINE | O.SWITCH_COST)
+            assert (s["node"] == o["slots"]["node"]).all() and (s["start"] == o["slots"]["start"]).all()
+            s2, r2 = F.local_search(t, s, makespan_phase2=int(r["makespan"]), flags=far.SWITCH_COST)
+            oslots = np.zeros(len(s), O.SLOT_DT)
+            oslots["node"], oslots["size_used"], oslots["start"] = s["node"], s["size_used"], s["start"]
+            q = O.refine(prof, costs, t, oslots, int(r["makespan"]), flags=O.SWITCH_COST)
+            for k in ("makespan", "moves", "swaps", "evals", "iterations", "reverted"):
+                assert r2[k] == q["result"][k], k
+            assert (s2["node"] == q["slots"]["node"]).all() and (s2["start"] == q["slots"]["start"]).all()
+        tab = inputs.synthetic(base, 24, 200, 93)
+        ms, slots, res = run_gpu(torch_dev, prof, costs, tab, flags=far.SWITCH_COST)
+        check_against_oracle(O, prof, costs, tab, ms, slots, res, flags=far.SWITCH_COST)
+    torch, dev = torch_dev
+    F = far.Far("A100")
+    d = torch.ones((2, 2, 8, 5), dtype=torch.int32, device=dev)
+    with pytest.raises(far.FarError):
+        F.concat_streams(d, flags=far.SWITCH_COST)
