@@ -701,25 +701,33 @@ __device__ __noinline__ void refine_best_warp(int n, const int* D, uint16_t* nli
           if (r >= A) { r -= A; ++idx; }
         }
       }
-      // swaps: entry x (uniform) with every entry y of a later node of the class
-      int bend = 0, bnode = -1;
-      for (int x = 0; x < m; ++x) {
-        const int fx = flat[x], tx = fx & 1023, ia = fx >> 10;
-        if (ia != bnode) {  // end of x's node block
-          bnode = ia;
-          bend = 0;
-          for (int v = f; v <= f + ia; ++v) bend += ncnt[v];
+      // swaps: every pair of class nodes (a < b), lanes over the |a| x |b| task pairs (flat index
+      // stepped incrementally: no division in the loop)
+      int abase = 0;
+      for (int ia = 0; ia < V; ++ia) {
+        const int na = ncnt[f + ia];
+        int bbase = abase + na;
+        for (int ib = ia + 1; ib < V; ++ib) {
+          const int nb = ncnt[f + ib], tot = na * nb;
+          if (tot > 0) {
+            const int di = 32 / nb, da = 32 - di * nb;
+            int qi = lane / nb, qa = lane - (lane / nb) * nb;
+            for (int p = lane; p < tot; p += 32) {
+              const int tx = flat[abase + qi] & 1023, ty = flat[bbase + qa] & 1023;
+              const bool lo = tx < ty;
+              const int k = lo ? tx : ty, j = lo ? ty : tx;
+              const int dd = D[k] - D[j];
+              const unsigned long long key = score(lo ? ia : ib, lo ? ib : ia, dd) | (1ull << 20) |
+                                             ((unsigned long long)k << 10) | (unsigned)j;
+              best = key < best ? key : best;
+              qi += di;
+              qa += da;
+              if (qa >= nb) { qa -= nb; ++qi; }
+            }
+          }
+          bbase += nb;
         }
-        const int dx = D[tx];
-        for (int y = bend + lane; y < m; y += 32) {
-          const int fy = flat[y], ty = fy & 1023, ib = fy >> 10;
-          const bool lo = tx < ty;
-          const int k = lo ? tx : ty, j = lo ? ty : tx;
-          const int dd = lo ? dx - D[ty] : D[ty] - dx;
-          const unsigned long long key = score(lo ? ia : ib, lo ? ib : ia, dd) | (1ull << 20) |
-                                         ((unsigned long long)k << 10) | (unsigned)j;
-          best = key < best ? key : best;
-        }
+        abase += na;
       }
     }
     // warp argmin of the packed keys
