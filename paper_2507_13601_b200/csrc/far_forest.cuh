@@ -124,7 +124,7 @@ __device__ int forest_sim(const FParams& F, int n, const int32_t* T, const uint1
     int end = (int)emin;
     ++pops;
     const uint2 w = __ldg(F.nodes + v);
-    const int cur_isz = isz[v];
+    const int cur_isz = r7 ? isz[v] : 0;
     int take = -1, tc = 0;
     if (LISTS) {
       if (cursor[v] < off[v + 1]) {
