@@ -457,3 +457,13 @@ def test_switch_cost_local_search_and_forest(O, torch_dev):
     d = torch.ones((2, 2, 8, 5), dtype=torch.int32, device=dev)
     with pytest.raises(far.FarError):
         F.concat_streams(d, flags=far.SWITCH_COST)
+
+
+@pytest.mark.parametrize("n", [1023, 1024])
+def test_variants_at_maximum_n(O, torch_dev, n):
+    """The reading variants at the largest batch sizes (warp finish / fused kernel layouts)."""
+    tab = np.minimum(inputs.synthetic("A100", n, 2, 5 + n, times="narrow"), 900)  # makespan bound < 2^29
+    costs = inputs.reconfig_costs("A100")
+    for flags in (far.BEST_IMPROVEMENT, far.SWITCH_COST, far.BEST_IMPROVEMENT | far.SWITCH_COST):
+        ms, slots, res = run_gpu(torch_dev, "A100", costs, tab, flags=flags)
+        check_against_oracle(O, "A100", costs, tab, ms, slots, res, flags=flags)
