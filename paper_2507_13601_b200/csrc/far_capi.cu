@@ -306,7 +306,8 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
                  o_m0 = o_items + a256(I * (size_t)(kfast - 1 > 0 ? kfast - 1 : 1) * 8);
     const int n4 = (P.n + 3) & ~3;
     const size_t o_ncnt = o_m0 + a256(I * (size_t)n4 * 4);
-    const size_t o_end = o_ncnt + a256(I * 32);
+    const size_t o_d0 = o_ncnt + a256(I * 32);
+    const size_t o_end = o_d0 + a256(I * (size_t)n4 * 4);
     const int r = ctx->launch_id & 1;
     if ((st = grow(ctx, &ctx->d_pws[r], &ctx->d_pws_bytes[r], o_end))) return st;
     char* w = ctx->d_pws[r];
@@ -323,6 +324,7 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     P.ws_m0 = (uint32_t*)(w + o_m0);
     P.ws_n4 = n4;
     P.ws_ncnt = (uint16_t*)(w + o_ncnt);
+    P.ws_d0 = (uint32_t*)(w + o_d0);
     // ---- K1: H0-H3 per instance (warp)
     P.kcap = kfast;
     P.ovf_pass = 0;

@@ -267,23 +267,29 @@ __device__ void lane_lists_coop(int n, int64_t base, unsigned am, const KParams&
     uint32_t* alt = (uint32_t*)(row + L.alt);
     const uint32_t* rec = P.ws_rec + inst * (int64_t)n;
     const int32_t* t = P.times + inst * (int64_t)n * NC;
-    auto put = [&](int j, uint32_t r) {
+    auto put = [&](int j, uint32_t r, int d) {
       const int v = (int)(r & 15u), c = (int)((r >> 4) & 7u), pos = (int)(r >> 7);
-      const int d = __ldg(t + j * NC + c);
+      if (d < 0) d = __ldg(t + j * NC + c);
       ent[off[v] + pos] = ((uint32_t)d << 10) | (uint32_t)(1023 - j);
       if (c != nd_c0(cnode<NC>(v))) atomicOr(&alt[j >> 5], 1u << (j & 31));
     };
     if ((n & 3) == 0) {
       const uint4* r4 = (const uint4*)rec;
+      // k* = 0 (most instances): the durations were written by prep (member 0's t_j(a1_j)),
+      // read coalesced instead of gathered from the runtime table
+      const bool k0 = (P.ws_best[inst] & 0xFFFFull) == 0;
+      const uint4* d4 = (const uint4*)(P.ws_d0 + inst * (int64_t)P.ws_n4);
       for (int q = lane; q < (n >> 2); q += 32) {
         const uint4 x = __ldcs(r4 + q);
-        put(4 * q, x.x);
-        put(4 * q + 1, x.y);
-        put(4 * q + 2, x.z);
-        put(4 * q + 3, x.w);
+        uint4 dd = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        if (k0) dd = __ldcs(d4 + q);
+        put(4 * q, x.x, (int)dd.x);
+        put(4 * q + 1, x.y, (int)dd.y);
+        put(4 * q + 2, x.z, (int)dd.z);
+        put(4 * q + 3, x.w, (int)dd.w);
       }
     } else {
-      for (int j = lane; j < n; j += 32) put(j, __ldcs(rec + j));
+      for (int j = lane; j < n; j += 32) put(j, __ldcs(rec + j), -1);
     }
   }
   __syncwarp();

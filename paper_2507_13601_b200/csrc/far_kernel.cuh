@@ -64,6 +64,7 @@ struct KParams {
   uint16_t* ws_ncnt;            // [I][16]       k*'s node list lengths (lane-per-instance finish)
   uint32_t* ws_m0;              // [I][ws_n4]    member 0's compact per-size LPT lists (t | task << 22)
   int ws_n4;
+  uint32_t* ws_d0;              // [I][ws_n4]    member 0's duration per task t_j(a1_j) (finish, k* = 0)
 };
 enum { PIPE_NONE = 0, PIPE_PREP = 1 };  // far_solve_kernel template modes: fused / H0-H3 -> ws
 enum { WS_FLAG = 8, WS_K = 9 };  // ws_meta slots: flag 0 = phase 2 pending, 1 = finished or deferred
@@ -1579,7 +1580,10 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
           x = (uint32_t)en.x | ((uint32_t)ltask[i] << 22);
         }
         const unsigned bal = __ballot_sync(FULL, z);
-        if (z) gm[base + __popc(bal & ((1u << lane) - 1))] = x;
+        if (z) {
+          gm[base + __popc(bal & ((1u << lane) - 1))] = x;
+          P.ws_d0[inst * (int64_t)P.ws_n4 + ltask[i]] = (uint32_t)lent[i].x;  // t_j(a1_j)
+        }
         base += __popc(bal);
       }
     }
