@@ -9,7 +9,7 @@
 //
 // Parity pins: see tests/test_oracle_*.py (partition counts, SPEC traces, bounds,
 // brute force, validator, golden phase-3 examples).  The multi-batch stream fold
-// (O8) lives in far_oracle_stream.cpp.
+// (O8) is stream_fold / orc_stream at the end of this file.
 
 #include "far_oracle.h"
 
