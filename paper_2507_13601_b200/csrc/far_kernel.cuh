@@ -943,7 +943,7 @@ __device__ __noinline__ void solve_local(const KParams& P, int64_t inst, unsigne
 // Node lists of k* from the pipelined phase-2 record (node, size index, position per task).
 template <int NC>
 __device__ void lists_from_record(int n, const uint32_t* rec, const int32_t* t, uint16_t* nlist, int* ncnt,
-                                  uint8_t* su, int* D, int lane) {
+                                  uint8_t* su, int* D, int lane, const uint32_t* d0) {
   constexpr int NN = Tree<NC>::NN;
   if (lane < NN) ncnt[lane] = 0;
   __syncwarp();
@@ -952,7 +952,8 @@ __device__ void lists_from_record(int n, const uint32_t* rec, const int32_t* t, 
     const int v = (int)(r & 15u);
     nlist[v * n + (int)(r >> 7)] = (uint16_t)j;
     su[j] = (uint8_t)((r >> 4) & 7u);
-    D[j] = __ldg(t + j * NC + su[j]);
+    // k* = 0: member 0's durations written by prep (coalesced); else gather the runtime table
+    D[j] = d0 ? (int)__ldcs(d0 + j) : __ldg(t + j * NC + su[j]);
     atomicAdd(&ncnt[v], 1);
   }
   __syncwarp();
@@ -981,7 +982,7 @@ __device__ void finish_core(const KParams& P, int64_t inst, uint16_t* nlist, int
   for (int pass = 0; pass < 2; ++pass) {
     if (FROM_REC) {
       lists_from_record<NC>(n, P.ws_rec + inst * (int64_t)n, P.times + inst * (int64_t)n * NC, nlist, ncnt, su, D,
-                            lane);
+                            lane, bestk == 0 ? P.ws_d0 + inst * (int64_t)P.ws_n4 : nullptr);
     } else {
       build_node_lists<NC>(n, bestk, lent, ltask, loff, bestnode, nlist, ncnt, su, lane);
       for (int j = lane; j < n; j += 32) D[j] = T[j * NC + su[j]];
