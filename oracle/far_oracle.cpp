@@ -145,19 +145,16 @@ int load_problem(int profile, const int32_t* costs, const int32_t* times, int n,
       if (costs[c] < 0 || costs[nc + c] < 0) return -3;
     }
   }
+  // The oracle's domain is every int32 time >= 1 and cost >= 0: with n <= 1024 every makespan
+  // is < 2^10 * 2^31 + 2 * 13 * 8 * 2^31 < 2^42, and the largest product it forms (the ppm stop
+  // rule, omega * 10^6) stays below 2^62.  The CUDA path's narrower int32 range (include/far.h
+  // "Integer range") is the kernel's contract, not the oracle's.
   P.t.assign(n, std::vector<i64>(nc, 0));
-  i64 bound = 0;
-  for (int i = 0; i < n; ++i) {
-    i64 mx = 0;
+  for (int i = 0; i < n; ++i)
     for (int c = 0; c < nc; ++c) {
       P.t[i][c] = times[(size_t)i * nc + c];
       if (P.t[i][c] < 1) return -3;
-      mx = std::max(mx, P.t[i][c]);
     }
-    bound += mx;
-  }
-  for (size_t v = 0; v < P.m.node.size(); ++v) bound += P.c.cr(P.m, (int)v) + P.c.de(P.m, (int)v);
-  if (bound >= (i64(1) << 29)) return -3;
   return 0;
 }
 
@@ -1320,13 +1317,23 @@ int orc_far_many(int profile, const int32_t* costs, const int32_t* times, int64_
 static int stream_fold(int profile, const int32_t* costs, const int32_t* times, int B, int n,
                        int32_t max_iterations, int32_t ppm, uint32_t flags, int64_t* out2, int64_t* offsets,
                        int32_t* seam, orc_slot* slots, orc_result* batch_res, int32_t* violations, int probe_k,
-                       int64_t delta);
+                       int64_t delta, int64_t* ends = nullptr);
 
 extern "C" int orc_stream(int profile, const int32_t* costs, const int32_t* times, int B, int n,
                           int32_t max_iterations, int32_t ppm, uint32_t flags, int64_t* out2, int64_t* offsets,
                           int32_t* seam, orc_slot* slots, orc_result* batch_res, int32_t* violations) {
   return stream_fold(profile, costs, times, B, n, max_iterations, ppm, flags, out2, offsets, seam, slots, batch_res,
                      violations, -1, 0);
+}
+
+// Test entry: orc_stream plus ends[k] = O_k + E_k, the end of batch k's placed timeline (the
+// quantity R24's keep-best rule compares).
+extern "C" int orc_stream_ends(int profile, const int32_t* costs, const int32_t* times, int B, int n,
+                               int32_t max_iterations, int32_t ppm, uint32_t flags, int64_t* out2, int64_t* offsets,
+                               int32_t* seam, orc_slot* slots, orc_result* batch_res, int32_t* violations,
+                               int64_t* ends) {
+  return stream_fold(profile, costs, times, B, n, max_iterations, ppm, flags, out2, offsets, seam, slots, batch_res,
+                     violations, -1, 0, ends);
 }
 
 // Test entry: violations of the concatenation of batches 0..k when batch k starts delta ticks
@@ -1343,7 +1350,7 @@ extern "C" int orc_stream_probe(int profile, const int32_t* costs, const int32_t
 static int stream_fold(int profile, const int32_t* costs, const int32_t* times, int B, int n,
                        int32_t max_iterations, int32_t ppm, uint32_t flags, int64_t* out2, int64_t* offsets,
                        int32_t* seam, orc_slot* slots, orc_result* batch_res, int32_t* violations, int probe_k,
-                       int64_t delta) {
+                       int64_t delta, int64_t* ends) {
   const int nc = orc_num_sizes(profile);
   if (nc < 0) return nc;
   if (B < 0 || n < 0) return -1;
@@ -1399,6 +1406,7 @@ static int stream_fold(int profile, const int32_t* costs, const int32_t* times, 
     int reused = 0;
     for (bool b : ev.reuse) reused += b;
     if (offsets) offsets[k] = ev.O;
+    if (ends) ends[k] = ev.end;
     if (k == probe_k) {  // probe: place this batch delta ticks early, validate, stop
       ev.O -= delta;
       place_batch(Pb[k], S, st, T, ev);

@@ -9,11 +9,10 @@
  * [n][|C_G|] in the profile's size order (A30: 1,2,4; A100/H100: 1,2,3,4,7),
  * in caller ticks.  costs are int32[2][|C_G|] = {create[], destroy[]}.
  * All internal arithmetic is int64.  Return value 0 = ok, <0 = error:
- *   -1 invalid argument, -2 unsupported profile, -3 bad time (t < 1,
- *   negative cost, or the makespan bound below exceeded), -4 too large.
- * Makespan bound (same rule as the CUDA path):
- *   sum_i max_c t_i(c) + sum_{tree nodes v} (t_create(|v|) + t_destroy(|v|))
- *   must be < 2^29.
+ *   -1 invalid argument, -2 unsupported profile, -3 bad time (t < 1 or
+ *   negative cost), -4 too large (n > 1024).
+ * Domain: every int32 time >= 1 and cost >= 0 (all arithmetic is int64; the
+ * CUDA path's narrower range, include/far.h "Integer range", is its own).
  */
 #ifndef FAR_ORACLE_H
 #define FAR_ORACLE_H

@@ -90,6 +90,9 @@ def lib():
             _lib.orc_stream.argtypes = [C.c_int, p, p, C.c_int, C.c_int, C.c_int32, C.c_int32, C.c_uint32,
                                         p, p, p, p, p, p]
             _lib.orc_stream.restype = C.c_int
+            _lib.orc_stream_ends.argtypes = [C.c_int, p, p, C.c_int, C.c_int, C.c_int32, C.c_int32, C.c_uint32,
+                                             p, p, p, p, p, p, p]
+            _lib.orc_stream_ends.restype = C.c_int
             _lib.orc_stream_probe.argtypes = [C.c_int, p, p, C.c_int, C.c_int, C.c_int, C.c_int64, p, p]
             _lib.orc_stream_probe.restype = C.c_int
     return _lib
@@ -246,7 +249,7 @@ def far_many_parallel(profile, costs, times, workers=None, **kw):
     return ms, res
 
 
-def stream(profile, costs, times, max_iterations=100, min_improvement_ppm=0, flags=0):
+def stream(profile, costs, times, max_iterations=100, min_improvement_ppm=0, flags=0, ends=False):
     """§4 multi-batch fold over one stream: times [B][n][|C|].  Returns dict with makespan,
     trivial makespan, offsets [B], seam [B][4] {reversed, moves, swaps, reused}, slots [B][n]
     (batch-relative starts of the final timeline), per-batch results and the number of
@@ -259,10 +262,19 @@ def stream(profile, costs, times, max_iterations=100, min_improvement_ppm=0, fla
     slots = np.zeros((B, n), SLOT_DT)
     res = np.zeros(B, RESULT_DT)
     viol = np.zeros(1, np.int32)
-    _check(lib().orc_stream(pid(profile), _ptr(_costs(costs)), _ptr(t), B, n, max_iterations, min_improvement_ppm,
-                            flags, _ptr(out2), _ptr(offs), _ptr(seam), _ptr(slots), _ptr(res), _ptr(viol)))
-    return {"makespan": int(out2[0]), "trivial": int(out2[1]), "offsets": offs, "seam": seam, "slots": slots,
-            "results": res, "violations": int(viol[0])}
+    e = np.zeros(B, np.int64)
+    if ends:  # + per-batch end O_k + E_k of the placed timeline (test entry orc_stream_ends)
+        _check(lib().orc_stream_ends(pid(profile), _ptr(_costs(costs)), _ptr(t), B, n, max_iterations,
+                                     min_improvement_ppm, flags, _ptr(out2), _ptr(offs), _ptr(seam), _ptr(slots),
+                                     _ptr(res), _ptr(viol), _ptr(e)))
+    else:
+        _check(lib().orc_stream(pid(profile), _ptr(_costs(costs)), _ptr(t), B, n, max_iterations, min_improvement_ppm,
+                                flags, _ptr(out2), _ptr(offs), _ptr(seam), _ptr(slots), _ptr(res), _ptr(viol)))
+    out = {"makespan": int(out2[0]), "trivial": int(out2[1]), "offsets": offs, "seam": seam, "slots": slots,
+           "results": res, "violations": int(viol[0])}
+    if ends:
+        out["ends"] = e
+    return out
 
 
 def stream_probe(profile, costs, times, k, delta):

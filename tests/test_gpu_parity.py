@@ -205,6 +205,26 @@ def test_input_errors_flagged(torch_dev):
     F.sync()  # flag cleared
 
 
+def test_kernel_range_is_narrower_than_the_oracle(O, torch_dev):
+    """The kernel's int32 range (include/far.h "Integer range": sum_i max_s t_i(s) + costs < 2^29)
+    is its own contract: inputs beyond it are still solved by the int64 oracle, and the kernel
+    flags them FAR_E_BAD_TIME instead of returning a wrong schedule."""
+    torch, dev = torch_dev
+    for profile in ("A30", "A100"):
+        tab = (inputs.synthetic(profile, 9, 4, 41) % 63 + 1).astype(np.int64) << 25
+        tab = tab.astype(np.int32)
+        for t in tab:
+            assert O.far(profile, None, t)["result"]["makespan"] > 0
+        F = far.Far(profile, inputs.reconfig_costs(profile, zero=True))
+        ms, sd, rs = F.solve_many(torch.from_numpy(tab).to(dev))
+        torch.cuda.synchronize()
+        assert (ms.cpu().numpy() == -1).all()
+        assert (far.results_np(rs)["status"] == 3).all()
+        with pytest.raises(far.FarError) as e:
+            F.sync()
+        assert e.value.status == 3
+
+
 def test_schedule_batch_and_local_search(O, torch_dev):
     for profile in ("A30", "A100", "H100"):
         costs = inputs.reconfig_costs(profile)

@@ -53,6 +53,8 @@ def test_refine_examples(O, case):
     r = O.refine(case["profile"], None, t, p2["slots"], p2["makespan"])
     res = r["result"]
     assert (res["makespan"], res["moves"], res["swaps"]) == (case["makespan"], case["moves"], case["swaps"])
+    # the headline evals/s rests on this counter (R27); hand-traced in the golden file (trace_alg2)
+    assert (res["evals"], res["iterations"]) == (case["evals"], case["iterations"])
     assert r["slots"]["node"].tolist() == case["nodes"]
     # Fig. 6: > 1.5x ; Fig. 7: almost 1.25x
     ratio = Fraction(case["phase2_makespan"], case["makespan"])
@@ -228,7 +230,7 @@ def test_input_errors(O):
     with pytest.raises(O.OracleError):
         O.far("A30", None, np.array([[1, 0, 1]], np.int32))        # t < 1
     with pytest.raises(O.OracleError):
-        O.far("A30", None, np.full((3, 3), 1 << 29, np.int32))     # makespan bound
+        O.far("A30", None, np.full((1025, 3), 1, np.int32))        # n > 1024
     with pytest.raises(O.OracleError):
         O.far(7, None, np.ones((1, 3), np.int32))                  # unknown profile
 
@@ -425,3 +427,25 @@ def test_switch_cost_invariants(O, profile):
                               flags=O.SWITCH_COST) > 0
     if profile != "A30":
         assert switched > 0
+
+
+@pytest.mark.parametrize("profile", ["A30", "A100"])
+def test_int64_domain_scaling(O, profile):
+    """The oracle's domain is all int32 times (int64 arithmetic).  Pinned by scale invariance: with
+    zero reconfiguration every quantity FAR compares (work s*t, makespans, |2t - m|, |2D - m|) is
+    homogeneous of degree 1 in the times, so FAR(c*t) = c*FAR(t) with the same allocation, nodes
+    and moves, and starts scaled by c.  c = 2^25 puts every instance beyond the kernel's range
+    (sum_i max_s t_i(s) >= 2^29, include/far.h "Integer range")."""
+    c = 1 << 25
+    for t in list(inputs.synthetic(profile, 9, 6, 41) % 63 + 1) + list(inputs.small_ties(profile, 9, 6, 42)):
+        t = np.asarray(t, np.int32)
+        assert int(t.max(axis=1).sum()) * c >= 1 << 29
+        a = O.far(profile, None, t)
+        b = O.far(profile, None, (t.astype(np.int64) * c).astype(np.int32))
+        ra, rb = a["result"], b["result"]
+        assert rb["makespan"] == c * ra["makespan"]
+        assert rb["makespan_phase2"] == c * ra["makespan_phase2"]
+        for k in ("alloc_index", "family_size", "moves", "swaps", "evals", "iterations", "reverted", "events"):
+            assert rb[k] == ra[k], k
+        assert (b["slots"]["node"] == a["slots"]["node"]).all()
+        assert (b["slots"]["start"] == c * a["slots"]["start"]).all()

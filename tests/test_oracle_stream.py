@@ -97,3 +97,46 @@ def test_seam_offset_is_least_feasible(O, profile):
                 assert v1 > 0, f"seed {seed} batch {k}: O_k - 1 = {offs[k] - 1} is feasible"
                 checked += 1
     assert checked >= 5
+
+
+GOLD = __import__("json").load(open(__import__("os").path.join(__import__("os").path.dirname(__file__),
+                                                             "golden", "spec_traces.json")))
+
+
+@pytest.mark.parametrize("case", GOLD["stream_seam"], ids=lambda c: c["kind"])
+def test_seam_refine_hand_traces(O, case):
+    """R24 seam move / swap and R25 trivial concatenation pinned by hand traces (golden trace text)."""
+    prof = case["profile"]
+    zero = inputs.reconfig_costs(prof, zero=True)
+    tab = np.asarray(case["times"], np.int32)
+    r = O.stream(prof, zero, tab)
+    assert r["offsets"].tolist() == case["offsets"]
+    assert (r["makespan"], r["trivial"]) == (case["makespan"], case["trivial"])
+    assert r["seam"].tolist() == case["seam"]
+    assert [r["slots"][b]["node"].tolist() for b in range(len(tab))] == case["nodes"]
+    assert [r["slots"][b]["start"].tolist() for b in range(len(tab))] == case["starts"]
+    assert r["violations"] == 0
+    rn = O.stream(prof, zero, tab, flags=O.NO_SEAM_MOVES)
+    assert rn["offsets"].tolist() == case["no_seam_moves"]["offsets"]
+    assert rn["makespan"] == case["no_seam_moves"]["makespan"]
+    assert (rn["seam"][:, 1:3] == 0).all()
+
+
+@pytest.mark.parametrize("profile", ["A30", "A100"])
+def test_seam_ops_never_end_later(O, profile):
+    """Per-seam invariant of R24's keep-best rule: on the same placed state, batch k with seam
+    operations ends (O_k + E_k) no later than without them.  Checked on 2-batch streams, where
+    the placed state (batch 0) is the same with and without FAR_NO_SEAM_MOVES."""
+    fired = 0
+    for seed, costs in ((31, inputs.reconfig_costs(profile)), (32, inputs.reconfig_costs(profile, zero=True))):
+        for n in (3, 6, 11):
+            tab = inputs.synthetic(profile, n, 40, seed + n).reshape(20, 2, n, -1)
+            for pair in tab:
+                a = O.stream(profile, costs, pair, ends=True)
+                b = O.stream(profile, costs, pair, flags=O.NO_SEAM_MOVES, ends=True)
+                assert a["ends"][0] == b["ends"][0]
+                assert a["ends"][1] <= b["ends"][1]
+                if a["seam"][1, 1] + a["seam"][1, 2]:
+                    fired += 1
+                    assert a["ends"][1] < b["ends"][1]  # an accepted seam op strictly shortens B_k
+    assert fired > 0
