@@ -7,10 +7,13 @@ move/swap evals/s.  See DESIGN.md "Measurement".
 
 Workload (BASELINE.json configs[4]): A100/H100 7-slice tree,
 n = 128 tasks per instance, §6.3 MixedScaling / WideTimes generator, Table 2 A100
-reconfiguration costs, seed 5.  1M instances PER RANK (weak scaling: rank r solves the
-instances [r*1M, (r+1)*1M) of the counter-based table).  A step = far_solve_many over
-the rank's resident table (every phase of the hot path, schedules + reports written),
-plus at N>1 the NCCL allgather of the per-instance makespans (H9).
+reconfiguration costs, seed 5.  1M instances in TOTAL, sharded across the N ranks
+(strong scaling): rank r solves the contiguous shard
+dist.shard_range(1M, r, N) of the counter-based table.  A step = far_solve_many over the
+rank's resident shard (every phase of the hot path, schedules + reports written), plus at
+N>1 the NCCL all-gather of the per-instance makespans of the whole job (dist.gather_makespans;
+with --gather-schedules also the 8-B task slots, dist.gather_schedules).  --weak keeps the
+round-1 weak-scaling mode (1M instances per rank).
 """
 import argparse
 import json
@@ -38,7 +41,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--instances", type=int, default=WORKLOAD.count, help="instances per rank")
+    ap.add_argument("--instances", type=int, default=WORKLOAD.count,
+                    help="global instances (strong scaling); per rank with --weak")
+    ap.add_argument("--weak", action="store_true", help="weak scaling: --instances per rank")
+    ap.add_argument("--dump", default=None,
+                    help="rank 0 writes the gathered whole-job makespans / slots to this .npz (tests)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--baseline-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -111,22 +118,70 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def oracle_baseline(seconds, rank_table=None):
-    """The CPU oracle, as it stands, single thread, on the first instances of the workload."""
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or platform.machine()
+
+
+def oracle_baseline(seconds):
+    """The CPU oracle, as it stands, single thread, on the first instances of the workload.
+    The sample is generated BEFORE the clock starts; only orc_far_many is timed."""
     from oracle import oracle as O
     O.build()
     costs = WORKLOAD.costs()
-    done, evals, t0 = 0, 0, time.perf_counter()
-    chunk = 200
-    while time.perf_counter() - t0 < seconds:
-        tab = WORKLOAD.table(count=chunk, start=done)
-        _, res = O.far_many(WORKLOAD.profile, costs, tab)
+    chunk = 250
+    tab = WORKLOAD.table(count=8 * 4096, parallel=True)  # more than `seconds` of oracle work
+    O.far_many(WORKLOAD.profile, costs, tab[:2])  # load the library outside the clock
+    done, evals, events, el = 0, 0, 0, 0.0
+    while el < seconds and done + chunk <= tab.shape[0]:
+        part = tab[done:done + chunk]
+        t0 = time.perf_counter()
+        _, res = O.far_many(WORKLOAD.profile, costs, part)
+        el += time.perf_counter() - t0
         done += chunk
         evals += int(res["evals"].sum())
-    dt = time.perf_counter() - t0
-    return {"value": done / dt, "unit": "instances/s", "cores": 1, "kind": "oracle",
-            "evals_per_s": evals / dt,
-            "sample": f"first {done} instances of {WORKLOAD.name} (A100, n=128, seed 5), single-threaded C++ oracle"}
+        events += int(res["events"].sum())
+    return {"value": done / el, "unit": "instances/s", "cores": 1, "kind": "oracle",
+            "evals_per_s": evals / el, "alg1_events_per_s": events / el, "cpu_model": _cpu_model(),
+            "host_cores": os.cpu_count(),
+            "sample": f"first {done} instances of {WORKLOAD.name} (A100, n=128, seed 5), single-threaded C++ "
+                      f"oracle (orc_far_many) timed alone, inputs generated before the clock",
+            "per_config": oracle_config_table()}
+
+
+def oracle_config_table():
+    """SURVEY.md §8(d) "Oracle timing" (i): the single-threaded oracle on a fixed subset of every
+    BASELINE.json config — all of M1 and M2, the first 10 000 of M3, one M4 stream per tree and
+    the first 1 000 of M5 — as instances (batches) per second, evals/s and Alg. 1 events/s.
+    Inputs are generated before each clock starts."""
+    from oracle import oracle as O
+    out = {}
+    for key, count in (("M1", 10_000), ("M2", 10_000), ("M3", 10_000), ("M5", 1_000)):
+        w = inputs.WORKLOADS[key]
+        tab = w.table(count=count, parallel=True)
+        t0 = time.perf_counter()
+        _, res = O.far_many(w.profile, w.costs(), tab)
+        dt = time.perf_counter() - t0
+        out[w.name] = {"instances": count, "seconds": dt, "instances_per_s": count / dt,
+                       "evals_per_s": float(res["evals"].sum()) / dt,
+                       "alg1_events_per_s": float(res["events"].sum()) / dt}
+    for prof in ("A30", "A100"):
+        w = inputs.WORKLOADS["M4_" + prof]
+        tab = inputs.synthetic(w.profile, w.n, 64, w.seed)  # stream 0: 64 batches x 64 tasks
+        t0 = time.perf_counter()
+        r = O.stream(w.profile, w.costs(), tab)
+        dt = time.perf_counter() - t0
+        out[w.name] = {"streams": 1, "batches": 64, "seconds": dt, "batches_per_s": 64 / dt,
+                       "evals_per_s": float(r["results"]["evals"].sum()) / dt,
+                       "stream_makespan": r["makespan"]}
+    return out
 
 
 def secondary(far, torch, dev, reps=5):
@@ -256,7 +311,7 @@ def run_reference(args, rank, world):
     v = per_step * args.steps / tot
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "instances/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic",
             "config": {"workload": WORKLOAD.name, "profile": "A100", "n_tasks": WORKLOAD.n,
                        "instances_per_step": per_step, "generator": "PAPER.md §6.3 MixedScaling/WideTimes seed 5"},
@@ -295,11 +350,16 @@ def main():
         else:
             dist.init_process_group(backend)
 
-    I = args.instances
-    nc = len(inputs.SIZES[WORKLOAD.profile])
-    # rank's shard of the counter-based table (weak scaling)
+    from paper_2507_13601_b200 import dist as fdist
+
+    # strong scaling (default, BASELINE.json configs[4]): TOTAL instances sharded contiguously over
+    # the ranks; --weak: every rank solves its own TOTAL instances
+    total = args.instances * (world if args.weak else 1)
+    lo, hi = (rank * args.instances, (rank + 1) * args.instances) if args.weak else \
+        fdist.shard_range(total, rank, world)
+    I = hi - lo
     host = inputs.synthetic_parallel(WORKLOAD.profile, WORKLOAD.n, I, WORKLOAD.seed, scaling=WORKLOAD.scaling,
-                                     times=WORKLOAD.times, start=rank * I,
+                                     times=WORKLOAD.times, start=lo,
                                      workers=max(1, min(32, (os.cpu_count() or 1) // world)))
     pinned = torch.from_numpy(host).pin_memory()
     d_times = pinned.to(dev, non_blocking=False)
@@ -308,9 +368,7 @@ def main():
     ms = torch.empty(I, dtype=torch.int32, device=dev)
     sd = torch.empty((I, WORKLOAD.n, 8), dtype=torch.uint8, device=dev)
     rs = torch.empty((I, 56), dtype=torch.uint8, device=dev)
-    gathered = torch.empty(I * world, dtype=torch.int32, device=dev) if world > 1 else None
-    gsched = (torch.empty((I * world, WORKLOAD.n, 8), dtype=torch.uint8, device=dev)
-              if world > 1 and args.gather_schedules and backend == "nccl" else None)
+    gathered = {}
 
     def step(ev=None, gev=None):
         if ev is not None:
@@ -318,16 +376,17 @@ def main():
         F.solve_many(d_times, out=(ms, sd, rs), stream=stream)
         if ev is not None:
             ev[1].record(stream)
-        if world > 1:
+        if world > 1:  # H9: the whole job's makespans (and schedules) on every rank
             if gev is not None:
                 gev[0].record(stream)
             if backend == "nccl":
-                dist.all_gather_into_tensor(gathered, ms)
-                if gsched is not None:
-                    dist.all_gather_into_tensor(gsched.view(-1), sd.view(-1))
-            else:
-                g = torch.empty(I * world, dtype=torch.int32)
-                dist.all_gather_into_tensor(g, ms.cpu())
+                gathered["ms"] = fdist.gather_makespans(ms, total)
+                if args.gather_schedules:
+                    gathered["sd"] = fdist.gather_schedules(sd, total)
+            else:  # gloo (logic test with ranks sharing one GPU): CPU tensors
+                gathered["ms"] = fdist.gather_makespans(ms.cpu(), total)
+                if args.gather_schedules:
+                    gathered["sd"] = fdist.gather_schedules(sd.cpu(), total)
             if gev is not None:
                 gev[1].record(stream)
 
@@ -384,8 +443,16 @@ def main():
         kern_total = sum(kern_ms)
         evals_all, events_all = float(evals_step), float(events_step)
     ms_per_step = total_ms / args.steps
-    inst_all = I * world
+    inst_all = total
     value = inst_all / (ms_per_step / 1000.0)
+
+    if args.dump and rank == 0:  # whole-job outputs as the product gathered them (tests compare with the oracle)
+        if world > 1:
+            g_ms = gathered["ms"].cpu().numpy()
+            g_sd = gathered["sd"].cpu().numpy() if "sd" in gathered else np.zeros((0,), np.uint8)
+        else:
+            g_ms, g_sd = ms.cpu().numpy(), sd.cpu().numpy()
+        np.savez(args.dump, makespan=g_ms, slots=g_sd, total=total)
 
     # secondary configs (rank 0) right after the timed region, before the PCIe-heavy e2e leg
     sec = None
@@ -411,8 +478,9 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt[0])
         ok = bool((hms == ms.cpu().numpy()).all())
-        e2e = {"value": inst_all / dt, "unit": "instances/s", "h2d_bytes_per_step": int(host.nbytes) * world,
-               "d2h_bytes_per_step": int(I * (4 + WORKLOAD.n * 8 + 56)) * world, "matches_device_run": ok,
+        e2e = {"value": inst_all / dt, "unit": "instances/s",
+               "h2d_bytes_per_step": int(total * WORKLOAD.n * nc * 4),
+               "d2h_bytes_per_step": int(total * (4 + WORKLOAD.n * 8 + 56)), "matches_device_run": ok,
                "api": "far_solve_many_host (C-ABI, 2-stream chunk pipeline)"}
 
     if rank != 0:
@@ -434,9 +502,15 @@ def main():
     S, NCs, NN = 7, nc, 13
     OPS_EVENT, OPS_EVAL = 25, 3
     fam = res["family_size"].astype(np.int64)
-    alg_events = int((fam * (WORKLOAD.n + NN)).sum())
-    ops_p1 = int((2 * WORKLOAD.n * NCs + (fam - 1) * (WORKLOAD.n + NCs)).sum())
-    ops = alg_events * OPS_EVENT + evals_step * OPS_EVAL + ops_p1
+    n_ = WORKLOAD.n
+    alg_events = int((fam * (n_ + NN)).sum())
+    ops_p1 = int((2 * n_ * NCs + (fam - 1) * (n_ + NCs)).sum())
+    # phase 2's per-size LPT orders: |C| comparison sorts of n, n log2 n compares each
+    ops_lpt = I * NCs * n_ * int(np.ceil(np.log2(max(n_, 2))))
+    # Alg. 2 line 26: one replay of the refined tree (n placements + one split per node)
+    ops_replay = I * (n_ + NN) * OPS_EVENT
+    ops_members = alg_events * OPS_EVENT
+    ops = ops_members + evals_step * OPS_EVAL + ops_p1 + ops_lpt + ops_replay
     # the hot path is one far_solve_many call = a chain of kernels; the
     # algorithmic op model spans all of H1-H7, so the roofline is taken over the chain, timed
     # by CUDA events on its stream; the per-kernel split comes from far_stage_times
@@ -463,9 +537,38 @@ def main():
                     "source": "far_measure_peak: 8 independent 32-bit chains/thread, 2 CTAs x 1024 threads per SM"}
         except Exception as e:  # diagnostics only
             meas = {"error": str(e)}
+    # the per-event constant is a model ("each ~20-40 integer ops"): the range
+    def _frac(ope):
+        o = (ops_members + ops_replay) / OPS_EVENT * ope + evals_step * OPS_EVAL + ops_p1 + ops_lpt
+        return o / kern_avg_s / peak_ops
+    # per-stage algorithmic fractions: each stage's own share of the work model over its own time
+    st_ops = {"prep": ops_p1 + ops_lpt, "member0+members+winner": ops_members,
+              "finish": evals_step * OPS_EVAL + ops_replay}
+    st_ms = {"prep": stages.get("prep", 0.0),
+             "member0+members+winner": sum(stages.get(k, 0.0) for k in ("member0", "members", "winner")),
+             "finish": stages.get("finish", 0.0)}
+    st_frac = {k: (st_ops[k] / (st_ms[k] / 1e3) / peak_ops if st_ms[k] > 0 else None) for k in st_ops}
+    hw = None
+    try:  # hardware view: ncu issued lane-ops per instance of each kernel (committed capture)
+        with open(os.path.join(ROOT, "profiles", "ncu_issue_M5.json")) as f:
+            hj = json.load(f)
+        mpeak = meas.get("int_issue_alu_fma_tops", 0) * 1e12 if isinstance(meas, dict) else 0
+        mpeak = mpeak or peak_ops
+        hw = {"source": hj.get("source"), "peak": mpeak / 1e12, "stages": {}}
+        for k, v in hj["lane_ops_per_instance"].items():
+            t_ms = stages.get(k)
+            if t_ms:
+                hw["stages"][k] = {"lane_ops_per_instance": v, "frac_of_measured_issue": v * I / (t_ms / 1e3) / mpeak}
+    except Exception:
+        pass
     roof = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
             "peak_measured": meas,
-            "frac": achieved / peak_ops, "traffic": traffic, "traffic_unit": "bytes per step, all kernels (ncu)",
+            "frac": achieved / peak_ops,
+            "frac_range_ops_per_event_20_40": [_frac(20), _frac(40)],
+            "ops_model": {"ops_per_event": OPS_EVENT, "ops_per_eval": OPS_EVAL, "per_step": {
+                "alg1_all_members": ops_members, "phase3_evals": evals_step * OPS_EVAL, "phase1": ops_p1,
+                "lpt_sorts": ops_lpt, "line26_replay": ops_replay}},
+            "stages_alg_frac": st_frac, "stages_hw": hw, "traffic": traffic, "traffic_unit": "bytes per step, all kernels (ncu)",
             "kernel": "far_solve_many kernel chain (prep, member0, members, winner, finish, overflow)",
             "stages_ms_per_step": stages, "dominant_stage": dom,
             "dominant_share": (stages[dom] / chain_ms) if dom else None,
@@ -475,14 +578,16 @@ def main():
             "hbm_gbs_achieved": (host.nbytes + I * (4 + WORKLOAD.n * 8 + 56)) / kern_avg_s / 1e9,
             "hbm_gbs_peak": pk.get("hbm_gbs")}
     line = {"metric": METRIC, "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if args.weak else "strong",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": WORKLOAD.name, "profile": "A100 (7-slice tree, Table 2 A100 costs)",
                        "n_tasks": WORKLOAD.n, "instances_per_rank": I, "global_instances": inst_all,
+                       "shard": [lo, hi],
                        "generator": "PAPER.md §6.3 MixedScaling/WideTimes, seed 5",
                        "l2": f"inputs ({host.nbytes / 1e9:.2f} GB/rank) larger than the 126 MB L2; no flush",
-                       "parallelism": f"dp{world} (instances sharded, NCCL allgather of makespans"
-                                  + (" and schedules)" if gsched is not None else ")")},
+                       "parallelism": f"dp{world} (instances sharded, {backend} allgather of makespans"
+                                  + (" and schedules)" if args.gather_schedules else ")")},
             "evals_per_s": evals_all / (ms_per_step / 1000.0),
             "multi_gpu": ({"kernel_ms_per_step_max_rank": kern_total / args.steps,
                            "allgather_ms_per_step_max_rank": gather_ms / args.steps,

@@ -32,12 +32,19 @@
  * caller memory.  The library owns the far_ctx (constant tables, a lazily grown
  * device workspace and private streams), released by far_destroy.
  * Threading: one far_ctx per host thread; concurrent calls on one ctx are not
- * allowed.
+ * allowed.  Successive asynchronous calls on one ctx may use DIFFERENT streams:
+ * the context orders the reuse of its internal workspaces across streams (an
+ * event per launch), so a later call never overwrites a workspace an earlier
+ * call on another stream is still reading.
  * Errors: every call returns far_status; far_last_error(ctx) gives a message.
  * Argument errors are reported synchronously.  Asynchronous calls
  * (far_solve_many, far_concat_streams) report per-instance input errors in
  * far_result.status (makespan = -1) and raise a sticky device flag that the next
- * far_sync() returns as FAR_E_BAD_TIME; CUDA faults surface as FAR_E_CUDA.
+ * far_sync() returns (bit 1: FAR_E_BAD_TIME, bit 2: FAR_E_INVALID_ARG, bit 4:
+ * stream window overflow, FAR_E_TOO_LARGE); CUDA faults surface as FAR_E_CUDA.
+ * The synchronous host-memory calls (far_schedule_batch, far_local_search,
+ * far_solve_many_host) report only their OWN errors, through a private flag:
+ * they never consume or misreport the asynchronous calls' pending flag.
  */
 #ifndef FAR_H
 #define FAR_H

@@ -33,8 +33,16 @@ struct far_ctx {
   std::string err;
   int device = -1, sms = 0;
   unsigned long long* d_counter = nullptr;  // RING launch counters
-  int launch_id = 0;
+  int64_t launch_id = 0;
+  // d_errflag[0]: sticky flag of the asynchronous calls (reported and cleared by far_sync);
+  // d_errflag[1]: private flag of the synchronous host-memory calls (cleared before and read
+  // after each such call, so they neither consume nor misreport the asynchronous flag)
   int* d_errflag = nullptr;
+  // cross-stream ordering of the context's device workspaces: every launch records an event on
+  // its stream; a launch that reuses a workspace last used on ANOTHER stream waits on that event
+  struct LaunchRec { cudaEvent_t ev; cudaStream_t stream; bool valid; };
+  LaunchRec recs[RING / 8] = {};
+  int64_t pws_last[2] = {-1, -1}, ovf_last[4] = {-1, -1, -1, -1}, cbuf_last = -1;
   // staging for host-memory calls
   char* d_buf = nullptr;   // staging of the synchronous host-memory calls (ctx streams)
   size_t d_buf_bytes = 0;
@@ -87,8 +95,12 @@ static far_status ensure_device(far_ctx* ctx) {
   CK(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, ctx->device));
   CK(cudaMalloc(&ctx->d_counter, RING * sizeof(unsigned long long)));
   CK(cudaMemset(ctx->d_counter, 0, RING * sizeof(unsigned long long)));
-  CK(cudaMalloc(&ctx->d_errflag, sizeof(int)));
-  CK(cudaMemset(ctx->d_errflag, 0, sizeof(int)));
+  CK(cudaMalloc(&ctx->d_errflag, 2 * sizeof(int)));
+  CK(cudaMemset(ctx->d_errflag, 0, 2 * sizeof(int)));
+  for (auto& r : ctx->recs) {
+    CK(cudaEventCreateWithFlags(&r.ev, cudaEventDisableTiming));
+    r.valid = false;
+  }
   CK(cudaStreamCreateWithFlags(&ctx->s[0], cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&ctx->s[1], cudaStreamNonBlocking));
   // allow every kernel the full opt-in shared memory; each launch passes its own size
@@ -139,6 +151,23 @@ static far_status grow(far_ctx* ctx, char** buf, size_t* have, size_t bytes) {
   return FAR_OK;
 }
 static far_status ensure_buf(far_ctx* ctx, size_t bytes) { return grow(ctx, &ctx->d_buf, &ctx->d_buf_bytes, bytes); }
+
+// Make `stream` wait for launch q (a previous user of a workspace) when q ran on another stream.
+// A ring entry overwritten by launch q + 32 is a later launch that itself waited for q (it reused
+// q's counter slot), so waiting on the newer event is still sufficient.
+static far_status order_after(far_ctx* ctx, int64_t q, cudaStream_t stream) {
+  if (q < 0) return FAR_OK;
+  far_ctx::LaunchRec& r = ctx->recs[q % (RING / 8)];
+  if (r.valid && r.stream != stream) CK(cudaStreamWaitEvent(stream, r.ev, 0));
+  return FAR_OK;
+}
+static far_status record_launch(far_ctx* ctx, int64_t id, cudaStream_t stream) {
+  far_ctx::LaunchRec& r = ctx->recs[id % (RING / 8)];
+  CK(cudaEventRecord(r.ev, stream));
+  r.stream = stream;
+  r.valid = true;
+  return FAR_OK;
+}
 
 // ---- per-stage timing (far_stage_timing): one event set per solver launch, stage boundaries
 static far_status t_collect(far_ctx* ctx, far_ctx::EvSet& e) {
@@ -237,7 +266,7 @@ static far_status launch_warp_kernel(far_ctx* ctx, KParams& P, cudaStream_t stre
 //   FAR_FUSED_PHASE2 (debug env) forces the fused warp-per-instance kernel for everything.
 //   MODE_LOCAL: the fused kernel (phase 3 only).
 static far_status launch_forest(far_ctx* ctx, KParams& P, cudaStream_t stream) {
-  P.errflag = ctx->d_errflag;
+  if (!P.errflag) P.errflag = ctx->d_errflag;
   FParams F;
   F.P = P;
   F.nodes = ctx->d_fnodes;
@@ -272,13 +301,18 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
   const bool pipe = P.mode == MODE_SOLVE && P.n > 0 && P.n <= 1023 && !getenv("FAR_FUSED_PHASE2") &&
                     !(P.flags & FAR_SWITCH_COST) && (P.I >= 256 || getenv("FAR_PIPELINE_ALWAYS"));
   const bool need_ovf = P.mode == MODE_SOLVE && (kfast < kmax || pipe);
-  const int slot = (ctx->launch_id++ % (RING / 8)) * 8;
+  const int64_t lid = ctx->launch_id++;
+  const int slot = (int)(lid % (RING / 8)) * 8;
+  far_status st;
+  if ((st = order_after(ctx, lid - RING / 8, stream))) return st;  // previous user of the counter slot
   CK(cudaMemsetAsync(ctx->d_counter + slot, 0, 8 * sizeof(unsigned long long), stream));
-  P.errflag = ctx->d_errflag;
+  if (!P.errflag) P.errflag = ctx->d_errflag;
   P.ovf_count = ctx->d_counter + slot + 2;
   P.ovf = nullptr;
   if (need_ovf) {
     const int r = (slot / 8) & 3;
+    if ((st = order_after(ctx, ctx->ovf_last[r], stream))) return st;
+    ctx->ovf_last[r] = lid;
     const size_t words = (size_t)((P.I + 31) / 32);
     if (ctx->ovf_words[r] < words) {
       if (ctx->d_ovf[r]) {
@@ -291,7 +325,6 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     P.ovf = ctx->d_ovf[r];
     CK(cudaMemsetAsync(P.ovf, 0, words * 4, stream));
   }
-  far_status st;
   far_ctx::EvSet* tset = nullptr;
   if ((st = t_begin(ctx, stream, tset))) return st;
   if (pipe) {
@@ -308,7 +341,9 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     const size_t o_ncnt = o_m0 + a256(I * (size_t)n4 * 4);
     const size_t o_d0 = o_ncnt + a256(I * 32);
     const size_t o_end = o_d0 + a256(I * (size_t)n4 * 4);
-    const int r = ctx->launch_id & 1;
+    const int r = (int)(lid & 1);
+    if ((st = order_after(ctx, ctx->pws_last[r], stream))) return st;
+    ctx->pws_last[r] = lid;
     if ((st = grow(ctx, &ctx->d_pws[r], &ctx->d_pws_bytes[r], o_end))) return st;
     char* w = ctx->d_pws[r];
     P.ws_ent = (int2*)(w + o_ent);
@@ -418,7 +453,7 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     if ((st = launch_warp_kernel(ctx, P, stream, (P.I + 31) / 32, PIPE_NONE))) return st;
     if ((st = t_mark(ctx, tset, stream, FAR_STAGE_OVERFLOW))) return st;
   }
-  return FAR_OK;
+  return record_launch(ctx, lid, stream);
 }
 
 static far_status check_opts(far_ctx* ctx, const far_opts* o) {
@@ -507,6 +542,7 @@ void far_destroy(far_ctx* ctx) {
     cudaDeviceSynchronize();
     cudaFree(ctx->d_counter);
     cudaFree(ctx->d_errflag);
+    for (auto& r : ctx->recs) cudaEventDestroy(r.ev);
     if (ctx->d_fnodes) cudaFree(ctx->d_fnodes);
     for (int r = 0; r < 4; ++r)
       if (ctx->d_ovf[r]) cudaFree(ctx->d_ovf[r]);
@@ -651,6 +687,8 @@ static far_status one_instance(far_ctx* ctx, const int32_t* times, int32_t n, co
   fill_params(ctx, opts, P);
   if (mode == MODE_SOLVE) P.flags |= FAR_NO_REFINE;
   P.flags &= ~(unsigned)FAR_NO_SCHEDULE;
+  P.errflag = ctx->d_errflag + 1;  // private flag of the synchronous calls
+  CK(cudaMemsetAsync(P.errflag, 0, sizeof(int), s));
   P.times = (const int32_t*)(ctx->d_buf + o_t);
   P.I = 1;
   P.n = n;
@@ -670,10 +708,7 @@ static far_status one_instance(far_ctx* ctx, const int32_t* times, int32_t n, co
   CK(cudaMemcpyAsync(&r, P.res, sizeof(far_result), cudaMemcpyDeviceToHost, s));
   if (sb) CK(cudaMemcpyAsync(sched, P.sched, sb, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  int flag = 0;
-  CK(cudaMemcpy(&flag, ctx->d_errflag, sizeof(int), cudaMemcpyDeviceToHost));
-  if (flag) CK(cudaMemset(ctx->d_errflag, 0, sizeof(int)));
-  *res = r;
+  *res = r;  // the call's own error is the status in its record (the private flag is not needed)
   if (r.status != FAR_OK)
     return fail(ctx, (far_status)r.status,
                 r.status == FAR_E_BAD_TIME ? "input check failed (t < 1 or makespan bound)" : "invalid input schedule");
@@ -718,6 +753,9 @@ far_status far_solve_many_host(far_ctx* ctx, const int32_t* h_times, int64_t I, 
   fill_params(ctx, opts, P);
   P.n = n;
   P.mode = MODE_SOLVE;
+  P.errflag = ctx->d_errflag + 1;  // private flag of the synchronous calls
+  CK(cudaMemsetAsync(P.errflag, 0, sizeof(int), ctx->s[0]));
+  CK(cudaStreamSynchronize(ctx->s[0]));
   int64_t nchunks = (I + chunk - 1) / chunk;
   for (int64_t q = 0; q < nchunks; ++q) {
     const int si = (int)(q & 1);
@@ -739,10 +777,12 @@ far_status far_solve_many_host(far_ctx* ctx, const int32_t* h_times, int64_t I, 
   CK(cudaStreamSynchronize(ctx->s[0]));
   CK(cudaStreamSynchronize(ctx->s[1]));
   int flag = 0;
-  CK(cudaMemcpy(&flag, ctx->d_errflag, sizeof(int), cudaMemcpyDeviceToHost));
-  if (flag) {
-    CK(cudaMemset(ctx->d_errflag, 0, sizeof(int)));
-    return fail(ctx, FAR_E_BAD_TIME, "an instance failed the input checks (t < 1 or makespan bound)");
+  CK(cudaMemcpy(&flag, ctx->d_errflag + 1, sizeof(int), cudaMemcpyDeviceToHost));
+  if (flag) {  // this call's own bits, decoded as far_sync does
+    CK(cudaMemset(ctx->d_errflag + 1, 0, sizeof(int)));
+    return fail(ctx, (flag & 1) ? FAR_E_BAD_TIME : FAR_E_INVALID_ARG,
+                (flag & 1) ? "an instance failed the input checks (t < 1 or makespan bound)"
+                           : "an instance had an invalid input schedule");
   }
   return FAR_OK;
 }
@@ -773,6 +813,8 @@ extern "C" far_status far_concat_streams(far_ctx* ctx, const int32_t* d_times, i
   auto a256 = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t bs = a256((size_t)IB * n * sizeof(far_task_slot)), br = a256((size_t)IB * sizeof(far_result)),
                bm = a256((size_t)IB * 4);
+  cudaStream_t stream0 = (cudaStream_t)cuda_stream;
+  if ((st = order_after(ctx, ctx->cbuf_last, stream0))) return st;  // d_cbuf's previous user
   if ((st = grow(ctx, &ctx->d_cbuf, &ctx->d_cbuf_bytes, bs + br + bm))) return st;
   // 1) FAR phases 1-3 on every batch of every stream (data-parallel)
   KParams P;
@@ -819,7 +861,11 @@ extern "C" far_status far_concat_streams(far_ctx* ctx, const int32_t* d_times, i
     far_stream_kernel<5><<<grid, warps * 32, smem, stream>>>(Q);
   CK(cudaGetLastError());
   ++ctx->launches;
-  return t_mark(ctx, tset, stream, FAR_STAGE_STREAM);
+  if ((st = t_mark(ctx, tset, stream, FAR_STAGE_STREAM))) return st;
+  // the fold is the last user of d_cbuf: order the next concat after it (same event ring)
+  ctx->cbuf_last = ctx->launch_id++;
+  if ((st = order_after(ctx, ctx->cbuf_last - RING / 8, stream))) return st;
+  return record_launch(ctx, ctx->cbuf_last, stream);
 }
 
 // ---- schedule events and validation (far_check.cuh), one warp per instance
@@ -831,7 +877,9 @@ static far_status launch_check(far_ctx* ctx, CParams& Q, int64_t I, int n, bool 
   int warps = 0, per_sm = 0;
   far_status st = pick_shape(ctx, fn, bytes, warps, per_sm);
   if (st) return st;
-  const int slot = (ctx->launch_id++ % (RING / 8)) * 8;
+  const int64_t lid = ctx->launch_id++;
+  const int slot = (int)(lid % (RING / 8)) * 8;
+  if ((st = order_after(ctx, lid - RING / 8, stream))) return st;
   CK(cudaMemsetAsync(ctx->d_counter + slot, 0, sizeof(unsigned long long), stream));
   Q.counter = ctx->d_counter + slot;
   far_ctx::EvSet* tset = nullptr;
@@ -847,7 +895,8 @@ static far_status launch_check(far_ctx* ctx, CParams& Q, int64_t I, int n, bool 
   }
   CK(cudaGetLastError());
   ++ctx->launches;
-  return t_mark(ctx, tset, stream, FAR_STAGE_CHECK);
+  if ((st = t_mark(ctx, tset, stream, FAR_STAGE_CHECK))) return st;
+  return record_launch(ctx, lid, stream);
 }
 
 static far_status check_args(far_ctx* ctx, const int32_t* d_times, int64_t I, int32_t n, const far_task_slot* d_sched,

@@ -13,7 +13,7 @@ Generators
   from the clipped normals of PAPER.md:1000-1006, transition memory→compute
   with probability 0.3 per slice step.  Readings (DESIGN.md
   §"Input recipe"): clipping = clamp; count ties → smaller size; a transitioned
-  task continues near-linearly; times are quantised to ticks with
+  task is sub-linear from then on (literally); times are quantised to ticks with
   max(1, floor(1000·t + 0.5)) — monotone, so property 1 survives.
 * :func:`rodinia_like` — config M2: the 16 frozen archetype profiles of
   ``data/rodinia_like.json`` with a per-instance input-size multiplier
@@ -114,10 +114,13 @@ def _synthetic_chunk(rng, B, n, sizes, nslices, p, p_sup, tmin, tmax):
         z = rng.standard_normal((B, n))
         u = rng.random((B, n))
         sub = s >= cls
-        # memory-bound: super-linear on 1->2; later steps stay super w.p. 0.7
+        # memory-bound: super-linear on 1->2; on each later step it stays super-linear w.p. 0.7,
+        # else it "becomes compute-bound" and moves to SUB-linear speedup for good (PAPER.md:991:
+        # "moving to sub-linear speedup with a probability of 1-(1-0.3)^2 (becomes compute-bound)")
         if s > 1:
             transitioned |= mem & ~sub & (u < 0.3)
-        sup = mem & ~sub & ~transitioned
+        sub = sub | transitioned
+        sup = mem & ~sub
         near = ~sub & ~sup
         r = np.where(sup, np.clip(-0.25 + 0.25 * z, -0.5, 0.0),
                      np.where(near, np.clip(0.1 + 0.1 * z, 0.0, 0.2),
@@ -230,7 +233,8 @@ class Workload:
         if self.kind == "rodinia":
             return rodinia_like(c, self.seed, start)
         if parallel:
-            return synthetic_parallel(self.profile, self.n, c, self.seed, scaling=self.scaling, times=self.times)
+            return synthetic_parallel(self.profile, self.n, c, self.seed, scaling=self.scaling, times=self.times,
+                                      start=start)
         return synthetic(self.profile, self.n, c, self.seed, scaling=self.scaling, times=self.times, start=start)
 
     def costs(self) -> np.ndarray:

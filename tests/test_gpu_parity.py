@@ -487,3 +487,53 @@ def test_variants_at_maximum_n(O, torch_dev, n):
     for flags in (far.BEST_IMPROVEMENT, far.SWITCH_COST, far.BEST_IMPROVEMENT | far.SWITCH_COST):
         ms, slots, res = run_gpu(torch_dev, "A100", costs, tab, flags=flags)
         check_against_oracle(O, "A100", costs, tab, ms, slots, res, flags=flags)
+
+
+def test_async_calls_on_different_streams(O, torch_dev):
+    """Successive asynchronous calls on one ctx on DIFFERENT streams (A, A, B, B, A ...) reuse the
+    context's workspaces (two pipeline workspaces, counter slots, overflow masks): the context must
+    order each reuse after the previous user's stream (include/far.h "Threading")."""
+    torch, dev = torch_dev
+    w = inputs.WORKLOADS["M5"]
+    F = far.Far(w.profile, w.costs())
+    tabs = [torch.from_numpy(w.table(count=3000, start=3000 * k)).to(dev) for k in range(5)]
+    ref = []
+    for d in tabs:  # single-stream reference results
+        ms, _, _ = F.solve_many(d)
+        ref.append(ms.clone())
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    outs = []
+    for rep in range(3):
+        order = [0, 0, 1, 1, 0] if rep == 0 else ([1, 0, 1, 0, 1] if rep == 1 else [0, 1, 1, 0, 0])
+        for k, si in enumerate(order):
+            outs.append((k, F.solve_many(tabs[k], stream=streams[si])[0]))
+    torch.cuda.synchronize()
+    F.sync()
+    for k, ms in outs:
+        assert torch.equal(ms, ref[k]), k
+    oms, _ = O.far_many(w.profile, w.costs(), tabs[4].cpu().numpy())
+    assert (ref[4].cpu().numpy() == oms).all()
+
+
+def test_sync_calls_keep_the_async_error_flag(torch_dev):
+    """A pending error of an asynchronous far_solve_many is neither consumed nor misreported by the
+    synchronous host-memory calls; far_sync reports it afterwards (include/far.h "Errors")."""
+    torch, dev = torch_dev
+    tab = inputs.synthetic("A30", 5, 4, 3)
+    bad = tab.copy()
+    bad[1, 2, 1] = 0
+    F = far.Far("A30")
+    F.solve_many(torch.from_numpy(bad).to(dev))          # async: flags instance 1, not synced
+    slots, r = F.schedule_batch(tab[0])                   # sync call on good input: OK
+    assert r["status"] == 0
+    ms, _, _ = F.solve_many_host(np.ascontiguousarray(tab))  # sync call on good input: OK
+    assert (ms > 0).all()
+    with pytest.raises(far.FarError) as e:                # the async error is still pending
+        F.sync()
+    assert e.value.status == 3
+    F.sync()
+    with pytest.raises(far.FarError) as e:                # a sync call reports its own error ...
+        F.solve_many_host(np.ascontiguousarray(bad))
+    assert e.value.status == 3
+    F.sync()                                              # ... and leaves no flag behind
