@@ -358,6 +358,7 @@ def main():
     lo, hi = (rank * args.instances, (rank + 1) * args.instances) if args.weak else \
         fdist.shard_range(total, rank, world)
     I = hi - lo
+    nc = len(inputs.SIZES[WORKLOAD.profile])
     host = inputs.synthetic_parallel(WORKLOAD.profile, WORKLOAD.n, I, WORKLOAD.seed, scaling=WORKLOAD.scaling,
                                      times=WORKLOAD.times, start=lo,
                                      workers=max(1, min(32, (os.cpu_count() or 1) // world)))
