@@ -40,16 +40,6 @@ __device__ __forceinline__ uint32_t cnode(int u) {
   return NC == 3 ? c_nodes3[u] : c_nodes5[u];
 }
 
-// max over the slices of node w of the slice ends
-template <int S>
-__device__ __forceinline__ int lane_end(uint32_t w, const int (&send)[S]) {
-  const int lo = nd_lo(w), hi = lo + nd_sz(w);
-  int e = 0;
-#pragma unroll
-  for (int s = 0; s < S; ++s) e = (s >= lo && s < hi) ? max(e, send[s]) : e;
-  return e;
-}
-
 // Move the entry x from node `from` to node `to` at its ordered position.
 template <int NN>
 __device__ __forceinline__ void lane_transfer(uint32_t* ent, uint16_t* off, int from, int to, uint32_t x) {
@@ -71,6 +61,57 @@ __device__ __forceinline__ void lane_transfer(uint32_t* ent, uint16_t* off, int 
     ent[tgt] = x;
     for (int v = to + 1; v <= from; ++v) off[v] = (uint16_t)(off[v] + 1);
   }
+}
+
+// Replace entry x_old at index g of the ordered segment [b, e) by x_new, keeping the segment in
+// descending entry order.  A swap removes T_k from I and inserts T_j, and removes T_j
+// from I^a and inserts T_k: on ordered lists this is the same as the two transfers of the warp
+// path (K: I -> I^a, then J: I^a -> I), without moving the segments in between.
+__device__ __forceinline__ void lane_replace(uint32_t* ent, int b, int e, int g, uint32_t x_new) {
+  if (x_new < ent[g]) {  // later in the order
+    for (; g + 1 < e && ent[g + 1] > x_new; ++g) ent[g] = ent[g + 1];
+  } else {  // earlier in the order
+    for (; g > b && ent[g - 1] < x_new; --g) ent[g] = ent[g - 1];
+  }
+  ent[g] = x_new;
+}
+
+// Alg. 2 line 11: I^a = the node of I's size, != I, with the minimum end of its last
+// slice (ties -> lower first slice).  Only the leaves and the 2-slice nodes have same-size
+// alternatives in the Fig. 3 trees (every other size has one node: A30 4; A100 7, 4, 3), so the
+// search is over those two compile-time classes; key = end << 3 | first slice.  Returns -1 if
+// there is no alternative (then lines 23-24 open the parent).
+template <int NC>
+__device__ __forceinline__ int lane_alt(int I, const int (&send)[Tree<NC>::S], uint32_t cand, int& eA) {
+  constexpr int S = Tree<NC>::S;
+  const uint32_t wI = cnode<NC>(I);
+  const int szI = nd_sz(wI), loI = nd_lo(wI);
+  unsigned key = 0xFFFFFFFFu;
+  if (szI == 1) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int u = tree_leaf<NC>(s);
+      const unsigned k = ((unsigned)send[s] << 3) | (unsigned)s;
+      if (s != loI && ((cand >> u) & 1)) key = min(key, k);
+    }
+  } else if (szI == 2) {
+#pragma unroll
+    for (int u = 0; u < Tree<NC>::NN; ++u) {
+      const uint32_t wu = tree_node<NC>(u);
+      if (nd_sz(wu) != 2) continue;
+      const int lo = nd_lo(wu);
+      const unsigned k = ((unsigned)max(send[lo], send[lo + 1]) << 3) | (unsigned)lo;
+      if (u != I && ((cand >> u) & 1)) key = min(key, k);
+    }
+  }
+  if (key == 0xFFFFFFFFu) return -1;
+  eA = (int)(key >> 3);
+  const int lo = (int)(key & 7u);
+  if (szI == 1) return tree_leaf<NC>(lo);
+#pragma unroll
+  for (int u = 0; u < Tree<NC>::NN; ++u)
+    if (nd_sz(tree_node<NC>(u)) == 2 && nd_lo(tree_node<NC>(u)) == lo) return u;
+  return -1;
 }
 
 // Alg. 2 on one thread; same readings as refine_warp.
@@ -113,15 +154,8 @@ __device__ void refine_lane(uint32_t* ent, uint16_t* off, int (&send)[Tree<NC>::
       if (I == 0) { stop = true; break; }
       const uint32_t wI = cnode<NC>(I);
       // alternative I^a: same size, != I, minimum (end, first slice)
-      int A = -1, eA = INT_MAX, loA = 15;
-#pragma unroll
-      for (int u = 0; u < NN; ++u) {
-        const uint32_t wu = cnode<NC>(u);
-        if (u != I && nd_sz(wu) == nd_sz(wI) && ((cand >> u) & 1)) {  // argmin (end, first slice)
-          const int eu = lane_end<S>(wu, send);
-          if (eu < eA || (eu == eA && nd_lo(wu) < loA)) { eA = eu; A = u; loA = nd_lo(wu); }
-        }
-      }
+      int eA = INT_MAX;
+      const int A = lane_alt<NC>(I, send, cand, eA);
       bool done = false;
       if (A >= 0) {
         const int m = omega - eA;
@@ -166,9 +200,12 @@ __device__ void refine_lane(uint32_t* ent, uint16_t* off, int (&send)[Tree<NC>::
           // two-pointer sweep instead of the |I| * |A| scan (same argmin, same tie-breaks).
           unsigned bd2 = UINT_MAX, bkey = UINT_MAX;
           uint32_t xk = 0, xj = 0;
+          int gk = 0, gj = 0;  // indices of the chosen T_k (in I) and T_j (in I^a)
           int r = bA, bst = bA;  // r: first entry with 2t <= T; bst: start of the equal-t block before r
           const int eAo = bA + nA;
-          for (int q = bI; q < bI + nI && m > 0; ++q) {
+          // a pair needs t_k > t_j: none if I's longest task is not longer than I^a's shortest
+          const bool any = m > 1 && nI > 0 && nA > 0 && (ent[bI] >> 10) > (ent[eAo - 1] >> 10);
+          for (int q = bI; any && q < bI + nI; ++q) {
             const uint32_t a = ent[q];
             const int tk = (int)(a >> 10), k = 1023 - (int)(a & 1023u);
             const int T = 2 * tk - m;
@@ -183,7 +220,7 @@ __device__ void refine_lane(uint32_t* ent, uint16_t* off, int (&send)[Tree<NC>::
               if (dl < m) {  // dl > 0 since 2 t_j <= 2 t_k - m < 2 t_k
                 const unsigned d = (unsigned)abs(2 * dl - m);
                 const unsigned key = ((unsigned)k << 10) | (unsigned)(1023 - (int)(b & 1023u));
-                if (d < bd2 || (d == bd2 && key < bkey)) { bd2 = d; bkey = key; xk = a; xj = b; }
+                if (d < bd2 || (d == bd2 && key < bkey)) { bd2 = d; bkey = key; xk = a; xj = b; gk = q; gj = r; }
               }
             }
             // above: first entry of the block before r; needs t_j < t_k
@@ -193,13 +230,13 @@ __device__ void refine_lane(uint32_t* ent, uint16_t* off, int (&send)[Tree<NC>::
               if (dl > 0) {  // dl < m since 2 t_j > 2 t_k - m
                 const unsigned d = (unsigned)abs(2 * dl - m);
                 const unsigned key = ((unsigned)k << 10) | (unsigned)(1023 - (int)(b & 1023u));
-                if (d < bd2 || (d == bd2 && key < bkey)) { bd2 = d; bkey = key; xk = a; xj = b; }
+                if (d < bd2 || (d == bd2 && key < bkey)) { bd2 = d; bkey = key; xk = a; xj = b; gk = q; gj = bst; }
               }
             }
           }
-          if (bd2 != UINT_MAX) {  // K: I -> A, then J: A -> I (same final lists as the warp path)
-            lane_transfer<NN>(ent, off, I, A, xk);
-            lane_transfer<NN>(ent, off, A, I, xj);
+          if (bd2 != UINT_MAX) {  // T_k: I -> I^a and T_j: I^a -> I, both lists kept ordered
+            lane_replace(ent, bI, bI + nI, gk, xj);
+            lane_replace(ent, bA, eAo, gj, xk);
             const int delta = (int)(xk >> 10) - (int)(xj >> 10);
             const uint32_t wA = cnode<NC>(A);
 #pragma unroll
@@ -253,43 +290,60 @@ __device__ void lane_lists(int n, const uint32_t* __restrict__ rec, const uint16
 
 // Warp-cooperative form of lane_lists for the active lanes' instances (mask am): the record of
 // instance i is read by the whole warp with coalesced 16-B loads (instead of one thread walking
-// 512 B with dependent loads) and its entries are written into lane i's row.  The rows' off[]
-// must already hold the node offsets and alt[] be zero.
+// 512 B with dependent loads) and its entries are written into lane i's row.  The next
+// instance's first 16-B chunk is loaded before the current one is scattered, so the loads of
+// consecutive instances overlap.  k0: bit i set if instance i's winner is member 0 (then the
+// durations prep wrote are read coalesced instead of gathered from the runtime table).  The rows'
+// off[] must already hold the node offsets and alt[] be zero.
 template <int NC>
-__device__ void lane_lists_coop(int n, int64_t base, unsigned am, const KParams& P, unsigned char* wrows, int rbytes,
-                                const LRow& L, int lane) {
-  for (; am; am &= am - 1) {
-    const int i = __ffs(am) - 1;
-    const int64_t inst = base + i;
-    unsigned char* row = wrows + (size_t)i * rbytes;
-    uint32_t* ent = (uint32_t*)(row + L.ent);
-    const uint16_t* off = (const uint16_t*)(row + L.off);
-    uint32_t* alt = (uint32_t*)(row + L.alt);
-    const uint32_t* rec = P.ws_rec + inst * (int64_t)n;
-    const int32_t* t = P.times + inst * (int64_t)n * NC;
-    auto put = [&](int j, uint32_t r, int d) {
-      const int v = (int)(r & 15u), c = (int)((r >> 4) & 7u), pos = (int)(r >> 7);
-      if (d < 0) d = __ldg(t + j * NC + c);
-      ent[off[v] + pos] = ((uint32_t)d << 10) | (uint32_t)(1023 - j);
-      if (c != nd_c0(cnode<NC>(v))) atomicOr(&alt[j >> 5], 1u << (j & 31));
+__device__ void lane_lists_coop(int n, int64_t base, unsigned am, unsigned k0, const KParams& P, unsigned char* wrows,
+                                int rbytes, const LRow& L, int lane) {
+  auto put = [&](uint32_t* ent, const uint16_t* off, uint32_t* alt, const int32_t* t, int j, uint32_t r, int d) {
+    const int v = (int)(r & 15u), c = (int)((r >> 4) & 7u), pos = (int)(r >> 7);
+    if (d < 0) d = __ldg(t + j * NC + c);
+    ent[off[v] + pos] = ((uint32_t)d << 10) | (uint32_t)(1023 - j);
+    if (c != nd_c0(cnode<NC>(v))) atomicOr(&alt[j >> 5], 1u << (j & 31));
+  };
+  if ((n & 3) == 0) {
+    const int n4 = n >> 2;
+    const uint4 NOD = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    auto load = [&](int i, int q, uint4& x, uint4& dd) {
+      const int64_t inst = base + i;
+      x = __ldcs((const uint4*)(P.ws_rec + inst * (int64_t)n) + q);
+      dd = ((k0 >> i) & 1) ? __ldcs((const uint4*)(P.ws_d0 + inst * (int64_t)P.ws_n4) + q) : NOD;
     };
-    if ((n & 3) == 0) {
-      const uint4* r4 = (const uint4*)rec;
-      // k* = 0 (most instances): the durations were written by prep (member 0's t_j(a1_j)),
-      // read coalesced instead of gathered from the runtime table
-      const bool k0 = (P.ws_best[inst] & 0xFFFFull) == 0;
-      const uint4* d4 = (const uint4*)(P.ws_d0 + inst * (int64_t)P.ws_n4);
-      for (int q = lane; q < (n >> 2); q += 32) {
-        const uint4 x = __ldcs(r4 + q);
-        uint4 dd = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-        if (k0) dd = __ldcs(d4 + q);
-        put(4 * q, x.x, (int)dd.x);
-        put(4 * q + 1, x.y, (int)dd.y);
-        put(4 * q + 2, x.z, (int)dd.z);
-        put(4 * q + 3, x.w, (int)dd.w);
+    uint4 xn = NOD, dn = NOD;
+    if (am && lane < n4) load(__ffs(am) - 1, lane, xn, dn);
+    for (; am; am &= am - 1) {
+      const int i = __ffs(am) - 1;
+      const int64_t inst = base + i;
+      unsigned char* row = wrows + (size_t)i * rbytes;
+      uint32_t* ent = (uint32_t*)(row + L.ent);
+      const uint16_t* off = (const uint16_t*)(row + L.off);
+      uint32_t* alt = (uint32_t*)(row + L.alt);
+      const int32_t* t = P.times + inst * (int64_t)n * NC;
+      const uint4 x0 = xn, d0 = dn;
+      const unsigned rest = am & (am - 1);
+      if (rest && lane < n4) load(__ffs(rest) - 1, lane, xn, dn);
+      for (int q = lane; q < n4; q += 32) {
+        uint4 x = x0, dd = d0;
+        if (q != lane) load(i, q, x, dd);
+        put(ent, off, alt, t, 4 * q, x.x, (int)dd.x);
+        put(ent, off, alt, t, 4 * q + 1, x.y, (int)dd.y);
+        put(ent, off, alt, t, 4 * q + 2, x.z, (int)dd.z);
+        put(ent, off, alt, t, 4 * q + 3, x.w, (int)dd.w);
       }
-    } else {
-      for (int j = lane; j < n; j += 32) put(j, __ldcs(rec + j), -1);
+    }
+  } else {
+    for (; am; am &= am - 1) {
+      const int i = __ffs(am) - 1;
+      const int64_t inst = base + i;
+      unsigned char* row = wrows + (size_t)i * rbytes;
+      const uint32_t* rec = P.ws_rec + inst * (int64_t)n;
+      const int32_t* t = P.times + inst * (int64_t)n * NC;
+      for (int j = lane; j < n; j += 32)
+        put((uint32_t*)(row + L.ent), (const uint16_t*)(row + L.off), (uint32_t*)(row + L.alt), t, j, __ldcs(rec + j),
+            -1);
     }
   }
   __syncwarp();
@@ -374,11 +428,12 @@ __global__ void __launch_bounds__(128, 3) far_finish_lane_kernel(KParams P) {
       }
       off[NN] = (uint16_t)acc;
     }
+    const unsigned long long best = active ? P.ws_best[inst] : 0ull;
     __syncwarp();
-    lane_lists_coop<NC>(n, inst - lane, __ballot_sync(FULL, active), P, wrows, L.bytes, L, lane);
+    lane_lists_coop<NC>(n, inst - lane, __ballot_sync(FULL, active), __ballot_sync(FULL, active && !(best & 0xFFFFull)),
+                        P, wrows, L.bytes, L, lane);
     if (!active) continue;
     const int* meta = P.ws_meta + inst * 16;
-    const unsigned long long best = P.ws_best[inst];
     const int ms2 = (int)(best >> 16), bestk = (int)(best & 0xFFFFu);
     far_result R;
     R.makespan = 0; R.makespan_phase2 = ms2; R.alloc_index = bestk; R.family_size = meta[WS_K];

@@ -78,4 +78,30 @@ template <> struct Tree<5> {
   static constexpr int leaf_of_slice[7] = {7, 8, 9, 10, 11, 12, 6};
 };
 
+// Node word of node u as a constexpr function (folds to a constant when u is a compile-time
+// index, e.g. inside an unrolled loop; the static arrays above are host-side tables).
+template <int NC> __host__ __device__ constexpr uint32_t tree_node(int u) {
+  return NC == 3
+             ? (u == 0 ? pack_node(0, 4, 2, NONE, 2, 1, 2, 2, ROOTP)
+                : u == 1 ? pack_node(0, 2, 1, NONE, 1, 3, 4, 1, 0)
+                : u == 2 ? pack_node(2, 2, 1, NONE, 1, 5, 6, 3, 0)
+                : pack_node(u - 3, 1, 0, NONE, 0, LEAF, LEAF, 0, u <= 4 ? 1 : 2))
+             : (u == 0 ? pack_node(0, 7, 4, NONE, 4, 1, 2, 4, ROOTP)
+                : u == 1 ? pack_node(0, 4, 3, 2, 3, 3, 4, 2, 0)
+                : u == 2 ? pack_node(4, 3, 2, NONE, 2, 5, 6, 6, 0)
+                : u == 3 ? pack_node(0, 2, 1, NONE, 1, 7, 8, 1, 1)
+                : u == 4 ? pack_node(2, 2, 1, NONE, 1, 9, 10, 3, 1)
+                : u == 5 ? pack_node(4, 2, 1, NONE, 1, 11, 12, 5, 2)
+                : u == 6 ? pack_node(6, 1, 0, NONE, 0, LEAF, LEAF, 0, 2)
+                : pack_node(u - 7, 1, 0, NONE, 0, LEAF, LEAF, 0, 3 + (u - 7) / 2));
+}
+// leaf node id of slice s (constexpr form of Tree<NC>::leaf_of_slice)
+template <int NC> __host__ __device__ constexpr int tree_leaf(int s) {
+  return NC == 3 ? 3 + s : (s < 6 ? 7 + s : 6);
+}
+static_assert(tree_node<3>(6) == Tree<3>::node[6] && tree_node<3>(3) == Tree<3>::node[3], "A30 node table");
+static_assert(tree_node<5>(12) == Tree<5>::node[12] && tree_node<5>(9) == Tree<5>::node[9] &&
+                  tree_node<5>(6) == Tree<5>::node[6] && tree_node<5>(2) == Tree<5>::node[2],
+              "A100 node table");
+
 }  // namespace farb
