@@ -12,6 +12,7 @@
 #include "far_kernel.cuh"
 #include "far_stream.cuh"
 #include "far_pipeline.cuh"
+#include "far_prep.cuh"
 #include "far_finish_lane.cuh"
 #include "far_check.cuh"
 #include "far_forest.cuh"
@@ -128,6 +129,8 @@ static far_status ensure_device(far_ctx* ctx) {
   for (const void* f : fns) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   CK(cudaFuncSetAttribute((const void*)far_forest_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   CK(cudaFuncSetAttribute((const void*)far_forest_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
+  CK(cudaFuncSetAttribute((const void*)far_prep_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
+  CK(cudaFuncSetAttribute((const void*)far_prep_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   if (ctx->gpus > 1) {
     CK(cudaMalloc(&ctx->d_fnodes, sizeof(uint2) * FMAXNN));
     CK(cudaMemcpy(ctx->d_fnodes, ctx->fnodes, sizeof(uint2) * ctx->nn * ctx->gpus, cudaMemcpyHostToDevice));
@@ -259,9 +262,24 @@ static far_status launch_warp_kernel(far_ctx* ctx, KParams& P, cudaStream_t stre
   return FAR_OK;
 }
 
+// K1 for n <= 128: far_prep_kernel<NC> (far_prep.cuh).
+static far_status launch_prep(far_ctx* ctx, KParams& P, cudaStream_t stream) {
+  const void* fn = ctx->nc == 3 ? (const void*)far_prep_kernel<3> : (const void*)far_prep_kernel<5>;
+  const PLayout L = make_playout(P.n, ctx->nc, P.kcap);
+  int warps = 0, per_sm = 0;
+  far_status st = pick_shape(ctx, fn, L.bytes, warps, per_sm);
+  if (st) return st;
+  const size_t smem = (size_t)warps * L.bytes;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((P.I + warps - 1) / warps, (int64_t)ctx->sms * per_sm));
+  void* args[] = {&P};
+  CK(cudaLaunchKernel(fn, grid, warps * 32, args, smem, stream));
+  ++ctx->launches;
+  return FAR_OK;
+}
+
 // Launch the solver for I instances on `stream`.
 //   MODE_SOLVE: the pipelined solver (far_pipeline.cuh: K1 prep -> K2 member 0 -> K3 candidate
-//   members -> K4 winner record -> K5 finish) for families of <= 64 members with t < 2^22,
+//   members -> K4 winner record -> K5 finish) for families of <= 96 members with t < 2^22,
 //   then the fused kernel with the full layout over the instances K1 deferred (overflow mask).
 //   FAR_FUSED_PHASE2 (debug env) forces the fused warp-per-instance kernel for everything.
 //   MODE_LOCAL: the fused kernel (phase 3 only).
@@ -360,11 +378,16 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     P.ws_n4 = n4;
     P.ws_ncnt = (uint16_t*)(w + o_ncnt);
     P.ws_d0 = (uint32_t*)(w + o_d0);
-    // ---- K1: H0-H3 per instance (warp)
+    // ---- K1: H0-H3 per instance (warp): the register-resident prep for n <= 128 (far_prep.cuh),
+    //      the general PIPE_PREP instantiation of the fused kernel otherwise (and for FAR_GROW_TIES)
     P.kcap = kfast;
     P.ovf_pass = 0;
     P.counter = ctx->d_counter + slot + 0;
-    if ((st = launch_warp_kernel(ctx, P, stream, P.I, PIPE_PREP))) return st;
+    if (P.n <= 128 && kfast <= 129 && !(P.flags & FAR_GROW_TIES) && !getenv("FAR_OLD_PREP")) {
+      if ((st = launch_prep(ctx, P, stream))) return st;
+    } else if ((st = launch_warp_kernel(ctx, P, stream, P.I, PIPE_PREP))) {
+      return st;
+    }
     if ((st = t_mark(ctx, tset, stream, FAR_STAGE_PREP))) return st;
     // ---- K2-K4: phase 2 at lane granularity
     PParams Q;

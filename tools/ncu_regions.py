@@ -19,7 +19,7 @@ for r in rows:
         t = int(d["Thread Instructions Executed"] or 0)
     except Exception:
         continue
-    k = ph(int(r[0])) if f == "far_kernel.cuh" else "lib:" + f
+    k = ph(int(r[0])) if f == (sys.argv[0] and __import__("os").environ.get("NCU_FILE","far_kernel.cuh")) else "lib:" + f
     if k == "frontier": k = "frontier(p2)" if t / max(i, 1) > 4 else "frontier(lane0)"
     a = agg.setdefault(k, [0, 0, 0]); a[0] += s; a[1] += i; a[2] += t
 ts = sum(v[0] for v in agg.values()); ti = sum(v[1] for v in agg.values())
