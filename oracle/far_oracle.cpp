@@ -1296,13 +1296,19 @@ int orc_lower_bound(int profile, const int32_t* times, int n, int64_t* sum_min_w
 
 int orc_far_many(int profile, const int32_t* costs, const int32_t* times, int64_t I, int n, int32_t max_iterations,
                  int32_t ppm, uint32_t flags, int64_t* makespans, orc_result* res) {
+  return orc_far_many_slots(profile, costs, times, I, n, max_iterations, ppm, flags, makespans, res, nullptr);
+}
+
+int orc_far_many_slots(int profile, const int32_t* costs, const int32_t* times, int64_t I, int n,
+                       int32_t max_iterations, int32_t ppm, uint32_t flags, int64_t* makespans, orc_result* res,
+                       orc_slot* slots) {
   const int nc = orc_num_sizes(profile);
   if (nc < 0) return nc;
   int worst = 0;
   for (int64_t i = 0; i < I; ++i) {
     orc_result r{};
-    int rc = orc_far(profile, costs, times + (size_t)i * n * nc, n, max_iterations, ppm, flags, nullptr, &r, nullptr,
-                     nullptr);
+    int rc = orc_far(profile, costs, times + (size_t)i * n * nc, n, max_iterations, ppm, flags,
+                     slots ? slots + (size_t)i * n : nullptr, &r, nullptr, nullptr);
     if (rc) { worst = rc; r.makespan = -1; }
     if (makespans) makespans[i] = r.makespan;
     if (res) res[i] = r;

@@ -90,6 +90,10 @@ int orc_stream_probe(int profile, const int32_t *costs, const int32_t *times, in
 int orc_far_many(int profile, const int32_t *costs, const int32_t *times, int64_t I, int n,
                  int32_t max_iterations, int32_t min_improvement_ppm, uint32_t flags,
                  int64_t *makespans, orc_result *res);
+/* orc_far_many plus every instance's schedule: slots[I][n] (NULL: none). */
+int orc_far_many_slots(int profile, const int32_t *costs, const int32_t *times, int64_t I, int n,
+                       int32_t max_iterations, int32_t ppm, uint32_t flags, int64_t *makespans, orc_result *res,
+                       orc_slot *slots);
 
 #ifdef __cplusplus
 }

@@ -82,6 +82,8 @@ def lib():
             ("orc_schedule_allocation_flags", [C.c_int, p, p, C.c_int, p, C.c_uint32, p, p, p, p, p], C.c_int),
             ("orc_lower_bound", [C.c_int, p, C.c_int, p, p], C.c_int),
             ("orc_far_many", [C.c_int, p, p, C.c_int64, C.c_int, C.c_int32, C.c_int32, C.c_uint32, p, p], C.c_int),
+            ("orc_far_many_slots", [C.c_int, p, p, C.c_int64, C.c_int, C.c_int32, C.c_int32, C.c_uint32, p, p, p],
+             C.c_int),
             ("orc_seam_offset_simple", [C.c_int, p, p], C.c_int64),
         ]:
             f = getattr(_lib, name)
@@ -229,24 +231,47 @@ def _far_many_worker(args):
     return far_many(profile, costs, times, **kw)
 
 
-def far_many_parallel(profile, costs, times, workers=None, **kw):
-    """Oracle fanned out over host cores (independent processes) — for full parity only."""
+def _far_many_check_worker(args):
+    """Solve a chunk with schedules and compare them with the given device slots (node, size_used,
+    start) -> (makespans, results, number of instances whose schedule differs, first such index)."""
+    profile, costs, times, dev_slots, kw = args
+    t = _times(times)
+    I, n = t.shape[0], t.shape[1]
+    ms = np.zeros(I, np.int64)
+    res = np.zeros(I, RESULT_DT)
+    sl = np.zeros((I, n), SLOT_DT)
+    lib().orc_far_many_slots(pid(profile), _ptr(_costs(costs)), _ptr(t), I, n, kw.get("max_iterations", 100),
+                             kw.get("min_improvement_ppm", 0), kw.get("flags", 0), _ptr(ms), _ptr(res), _ptr(sl))
+    bad = ((sl["node"] != dev_slots["node"]) | (sl["size_used"] != dev_slots["size_used"]) |
+           (sl["start"] != dev_slots["start"])).any(axis=1)
+    nb = int(bad.sum())
+    return ms, res, nb, int(np.argmax(bad)) if nb else -1
+
+
+def far_many_parallel_check(profile, costs, times, dev_slots, workers=None, **kw):
+    """Oracle over host cores with every schedule compared, chunk by chunk inside the workers, with
+    the device slots dev_slots [I][n] (fields node, size_used, start) -> (makespans, results,
+    number of mismatching schedules, first mismatching instance or -1)."""
     import concurrent.futures as cf
     t = _times(times)
     workers = workers or (os.cpu_count() or 1)
-    if workers <= 1 or t.shape[0] < 64:
-        return far_many(profile, costs, t, **kw)
-    parts = np.array_split(np.arange(t.shape[0]), workers * 4)
+    parts = np.array_split(np.arange(t.shape[0]), max(1, workers * 8))
     ms = np.zeros(t.shape[0], np.int64)
     res = np.zeros(t.shape[0], RESULT_DT)
+    nbad, first = 0, -1
     with cf.ProcessPoolExecutor(workers) as ex:
-        futs = {ex.submit(_far_many_worker, (profile, costs, t[p[0]:p[-1] + 1], kw)): p for p in parts if len(p)}
+        futs = {ex.submit(_far_many_check_worker, (profile, costs, t[p[0]:p[-1] + 1],
+                                                   dev_slots[p[0]:p[-1] + 1], kw)): p for p in parts if len(p)}
         for f in cf.as_completed(futs):
             p = futs[f]
-            m, r = f.result()
+            m, r, nb, fb = f.result()
             ms[p[0]:p[-1] + 1] = m
             res[p[0]:p[-1] + 1] = r
-    return ms, res
+            if nb:
+                nbad += nb
+                g = p[0] + fb
+                first = g if first < 0 else min(first, g)
+    return ms, res, nbad, first
 
 
 def stream(profile, costs, times, max_iterations=100, min_improvement_ppm=0, flags=0, ends=False):

@@ -351,8 +351,9 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     const int ecap1 = LF.ecap + 1;
     auto a256 = [](size_t x) { return (x + 255) & ~(size_t)255; };
     const size_t I = (size_t)P.I;
-    const size_t o_ent = 0, o_lb = o_ent + a256(I * ecap1 * 8), o_cnt = o_lb + a256(I * kfast * 4),
-                 o_meta = o_cnt + a256(I * kfast * 8), o_best = o_meta + a256(I * 64), o_evt = o_best + a256(I * 8),
+    const int kstride = (kfast + 3) & ~3;  // per-instance stride of ws_lb / ws_cnt (16-B rows)
+    const size_t o_ent = 0, o_lb = o_ent + a256(I * ecap1 * 8), o_cnt = o_lb + a256(I * kstride * 4),
+                 o_meta = o_cnt + a256(I * kstride * 8), o_best = o_meta + a256(I * 64), o_evt = o_best + a256(I * 8),
                  o_rec = o_evt + a256(I * 8), o_sl = o_rec + a256(I * P.n * 4), o_items = o_sl + a256(I * 32),
                  o_m0 = o_items + a256(I * (size_t)(kfast - 1 > 0 ? kfast - 1 : 1) * 8);
     const int n4 = (P.n + 3) & ~3;
@@ -373,7 +374,7 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     P.ws_rec = (uint32_t*)(w + o_rec);
     P.ws_sl = (int*)(w + o_sl);
     P.ws_ecap1 = ecap1;
-    P.ws_kcap = kfast;
+    P.ws_kcap = kstride;
     P.ws_m0 = (uint32_t*)(w + o_m0);
     P.ws_n4 = n4;
     P.ws_ncnt = (uint16_t*)(w + o_ncnt);
@@ -401,7 +402,7 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     Q.flags = P.flags;
     Q.ws_ent = P.ws_ent; Q.ws_lb = P.ws_lb; Q.ws_cnt = P.ws_cnt; Q.ws_meta = P.ws_meta;
     Q.ws_best = P.ws_best; Q.ws_evt = P.ws_evt; Q.ws_rec = P.ws_rec; Q.ws_sl = P.ws_sl;
-    Q.ws_ecap1 = ecap1; Q.ws_kcap = kfast;
+    Q.ws_ecap1 = ecap1; Q.ws_kcap = kstride;
     Q.ws_m0 = P.ws_m0; Q.ws_n4 = n4; Q.ws_ncnt = P.ws_ncnt;
     Q.items = (int2*)(w + o_items);
     Q.nitems = ctx->d_counter + slot + 3;

@@ -257,13 +257,27 @@ __global__ void __launch_bounds__(128) far_member0_kernel(PParams P) {
     const unsigned long long b0 = best_key(ms0, 0);
     P.ws_best[i] = b0;
     P.ws_evt[i] = (unsigned long long)pops;
-    // members that can still beat (ms_0, 0): (LB_k, k) < (ms_0, 0) lexicographically
-    int cand = 0;
-    for (int k = 1; k < K; ++k) cand += exhaustive || best_key(lb[k], k) < b0;
-    if (cand) {
-      unsigned long long base = atomicAdd(P.nitems, (unsigned long long)cand);
-      for (int k = 1; k < K; ++k)
-        if (exhaustive || best_key(lb[k], k) < b0) P.items[base++] = make_int2((int)i, k);
+    // members that can still beat (ms_0, 0): (LB_k, k) < (ms_0, 0) lexicographically, i.e.
+    // LB_k < ms_0 (k >= 1).  One pass, 32 members per chunk: 16-B loads (ws_kcap is a multiple of
+    // 4), a bit per candidate, one atomic per chunk with candidates.
+    for (int k0 = 0; k0 < K; k0 += 32) {
+      unsigned mask = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (k0 + 4 * u < K) {
+          const int4 x = __ldg((const int4*)(lb + k0) + u);
+          mask |= (unsigned)(exhaustive || x.x < ms0) << (4 * u);
+          mask |= (unsigned)(exhaustive || x.y < ms0) << (4 * u + 1);
+          mask |= (unsigned)(exhaustive || x.z < ms0) << (4 * u + 2);
+          mask |= (unsigned)(exhaustive || x.w < ms0) << (4 * u + 3);
+        }
+      }
+      if (k0 == 0) mask &= ~1u;                                // member 0 itself
+      if (K - k0 < 32) mask &= (1u << (K - k0)) - 1u;         // past the family
+      if (mask) {
+        unsigned long long slot = atomicAdd(P.nitems, (unsigned long long)__popc(mask));
+        for (; mask; mask &= mask - 1) P.items[slot++] = make_int2((int)i, k0 + __ffs(mask) - 1);
+      }
     }
   }
   (void)NN;

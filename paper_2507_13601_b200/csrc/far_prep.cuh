@@ -225,14 +225,18 @@ __device__ __forceinline__ void prep_instance(const KParams& P, int64_t inst, un
     W = __reduce_add_sync(FULL, W);
     c0 = (unsigned long long)warp_sum_ll((long long)c0);
     // ---- H2: growth steps = non-terminal chain elements with key > T*, a prefix of each chain
+    //      (keys strictly decrease along a chain, so the count needs no early exit)
     int gsum = 0;
 #pragma unroll 1
     for (int j = lane; j < n; j += 32) {
       const uint32_t w = info[j];
+      unsigned m = (w >> 3) & ((1u << (NC - 1)) - 1u);
       int g = 0;
-      for (unsigned m = (w >> 3) & ((1u << (NC - 1)) - 1u); m; m &= m - 1) {
-        if (growth_key<NC>(T[j * NC + __ffs(m) - 1], j, g) <= tstar) break;
-        ++g;
+#pragma unroll
+      for (int p = 0; p < NC - 1; ++p) {
+        const int c = m ? __ffs(m) - 1 : 0;
+        g += (m != 0) & (growth_key<NC>(T[j * NC + c], j, p) > tstar);
+        m &= m - 1;
       }
       info[j] = w | ((uint32_t)g << 8);
       gsum += g;
@@ -246,18 +250,35 @@ __device__ __forceinline__ void prep_instance(const KParams& P, int64_t inst, un
     Gn = __shfl_sync(FULL, excl, 31);
     excl -= gsum;
     if (Gn + 1 <= P.kcap) {
-      // steps in task order, each task's in chain order
+      // first step index per task; the growing tasks (g > 0, at most Gn of them) listed in gt
+      uint32_t* gt = (uint32_t*)lbh;  // lbh is written after the steps are ranked
+      int ng = 0;
 #pragma unroll 1
-      for (int j = lane; j < n; j += 32) {
+      for (int j0 = 0; j0 < n; j0 += 32) {
+        const int j = j0 + lane;
+        const uint32_t w = j < n ? info[j] : 0u;
+        const int g = (int)((w >> 8) & 7u);
+        if (j < n) info[j] = w | ((uint32_t)excl << 11);
+        const unsigned b = __ballot_sync(FULL, g > 0);
+        if (g > 0) gt[ng + __popc(b & lt)] = (uint32_t)j | ((uint32_t)excl << 8);
+        ng += __popc(b);
+        excl += g;
+      }
+      __syncwarp();
+      // steps of each growing task in chain order (lane per growing task)
+#pragma unroll 1
+      for (int i = lane; i < ng; i += 32) {
+        const uint32_t x = gt[i];
+        const int j = (int)(x & 255u);
+        int e = (int)(x >> 8);
         const uint32_t w = info[j];
         const int g = (int)((w >> 8) & 7u);
-        info[j] = w | ((uint32_t)excl << 11);
         unsigned m = (w >> 3) & 31u;
-        for (int p = 0; p < g; ++p, ++excl) {
+        for (int p = 0; p < g; ++p, ++e) {
           const int c = __ffs(m) - 1;
           m &= m - 1;
-          gk[excl] = growth_key<NC>(T[j * NC + c], j, p);
-          ginfo[excl] = (uint32_t)j | ((uint32_t)c << 8) | ((uint32_t)(__ffs(m) - 1) << 11) | ((uint32_t)(p == g - 1) << 14);
+          gk[e] = growth_key<NC>(T[j * NC + c], j, p);
+          ginfo[e] = (uint32_t)j | ((uint32_t)c << 8) | ((uint32_t)(__ffs(m) - 1) << 11) | ((uint32_t)(p == g - 1) << 14);
         }
       }
       if (lane < ((Gn + 3) & ~3) - Gn) gk[Gn + lane] = 0u;  // pads: never above a key

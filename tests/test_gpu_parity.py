@@ -419,20 +419,23 @@ def test_grow_ties_many_entries(O, torch_dev, n):
 @pytest.mark.skipif(bool(__import__("os").environ.get("FAR_SKIP_FULL_M5")), reason="opt-out")
 def test_full_size_m5_parity(O, torch_dev):
     """BASELINE configs[4] at full size: all 1M A100 x n=128 instances of the bench workload, the
-    makespan and every report field bit-exact (oracle fanned out over the host cores; ~30 s on the
-    16-core B200 host)."""
+    makespan, every report field AND every task slot (node, size used, start) of all 1M schedules
+    bit-exact (oracle fanned out over the host cores, the schedules compared chunk by chunk inside
+    the workers; ~1 min on the 16-core B200 host)."""
     torch, dev = torch_dev
     w = inputs.WORKLOADS["M5"]
     tab = w.table(parallel=True)
     F = far.Far(w.profile, w.costs())
-    ms, _, rs = F.solve_many(torch.from_numpy(tab).to(dev), sched=False)
+    ms, sd, rs = F.solve_many(torch.from_numpy(tab).to(dev))
     torch.cuda.synchronize()
     F.sync()
-    ms, res = ms.cpu().numpy(), far.results_np(rs)
-    oms, ores = O.far_many_parallel(w.profile, w.costs(), tab)
+    ms, res, slots = ms.cpu().numpy(), far.results_np(rs), far.slots_np(sd)
+    del sd
+    oms, ores, nbad, first = O.far_many_parallel_check(w.profile, w.costs(), tab, slots)
     assert (ms == oms).all(), f"makespan mismatch at {np.nonzero(ms != oms)[0][:10]}"
     for k in FIELDS:
         assert (res[k] == ores[k]).all(), k
+    assert nbad == 0, f"{nbad} schedules differ, first at instance {first}"
 
 
 @pytest.mark.parametrize("profile,gen,n", [("A100", "mixed", 16), ("H100", "mixed", 40), ("A100", "ties", 24),
