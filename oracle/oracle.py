@@ -248,6 +248,26 @@ def _far_many_check_worker(args):
     return ms, res, nb, int(np.argmax(bad)) if nb else -1
 
 
+def far_many_parallel(profile, costs, times, workers=None, **kw):
+    """Oracle fanned out over host cores (independent processes) — for full parity only."""
+    import concurrent.futures as cf
+    t = _times(times)
+    workers = workers or (os.cpu_count() or 1)
+    if workers <= 1 or t.shape[0] < 64:
+        return far_many(profile, costs, t, **kw)
+    parts = np.array_split(np.arange(t.shape[0]), workers * 4)
+    ms = np.zeros(t.shape[0], np.int64)
+    res = np.zeros(t.shape[0], RESULT_DT)
+    with cf.ProcessPoolExecutor(workers) as ex:
+        futs = {ex.submit(_far_many_worker, (profile, costs, t[p[0]:p[-1] + 1], kw)): p for p in parts if len(p)}
+        for f in cf.as_completed(futs):
+            p = futs[f]
+            m, r = f.result()
+            ms[p[0]:p[-1] + 1] = m
+            res[p[0]:p[-1] + 1] = r
+    return ms, res
+
+
 def far_many_parallel_check(profile, costs, times, dev_slots, workers=None, **kw):
     """Oracle over host cores with every schedule compared, chunk by chunk inside the workers, with
     the device slots dev_slots [I][n] (fields node, size_used, start) -> (makespans, results,

@@ -201,37 +201,45 @@ __device__ void refine_lane(uint32_t* ent, uint16_t* off, int (&send)[Tree<NC>::
           unsigned bd2 = UINT_MAX, bkey = UINT_MAX;
           uint32_t xk = 0, xj = 0;
           int gk = 0, gj = 0;  // indices of the chosen T_k (in I) and T_j (in I^a)
-          int r = bA, bst = bA;  // r: first entry with 2t <= T; bst: start of the equal-t block before r
           const int eAo = bA + nA;
           // a pair needs t_k > t_j: none if I's longest task is not longer than I^a's shortest
           const bool any = m > 1 && nI > 0 && nA > 0 && (ent[bI] >> 10) > (ent[eAo - 1] >> 10);
-          for (int q = bI; any && q < bI + nI; ++q) {
-            const uint32_t a = ent[q];
-            const int tk = (int)(a >> 10), k = 1023 - (int)(a & 1023u);
-            const int T = 2 * tk - m;
-            while (r < eAo && 2 * (int)(ent[r] >> 10) > T) {
-              if (r == bA || (ent[r] >> 10) != (ent[r - 1] >> 10)) bst = r;
-              ++r;
-            }
-            // below (or equal): entry r (first of its equal-t block); needs t_j > t_k - m
-            if (r < eAo) {
-              const uint32_t b = ent[r];
-              const int dl = tk - (int)(b >> 10);
-              if (dl < m) {  // dl > 0 since 2 t_j <= 2 t_k - m < 2 t_k
-                const unsigned d = (unsigned)abs(2 * dl - m);
-                const unsigned key = ((unsigned)k << 10) | (unsigned)(1023 - (int)(b & 1023u));
-                if (d < bd2 || (d == bd2 && key < bkey)) { bd2 = d; bkey = key; xk = a; xj = b; gk = q; gj = r; }
+          if (any) {
+            // r: first entry of I^a with 2t <= T (cur = ent[r], 0 past the end); bst: start of the
+            // equal-t block before r (bv = ent[bst]); registers hold the entries so that a
+            // pointer step is one shared-memory load
+            int r = bA, bst = bA;
+            uint32_t cur = ent[bA], bv = cur, prevt = 0xFFFFFFFFu;
+            uint32_t a = ent[bI];
+            for (int q = bI; q < bI + nI; ++q) {
+              const uint32_t an = q + 1 < bI + nI ? ent[q + 1] : 0u;  // next T_k, loaded ahead
+              const int tk = (int)(a >> 10), k = 1023 - (int)(a & 1023u);
+              const int T = 2 * tk - m;
+              while (r < eAo && 2 * (int)(cur >> 10) > T) {
+                if ((cur >> 10) != prevt) { bst = r; bv = cur; }
+                prevt = cur >> 10;
+                ++r;
+                cur = r < eAo ? ent[r] : 0u;
               }
-            }
-            // above: first entry of the block before r; needs t_j < t_k
-            if (r > bA) {
-              const uint32_t b = ent[bst];
-              const int dl = tk - (int)(b >> 10);
-              if (dl > 0) {  // dl < m since 2 t_j > 2 t_k - m
-                const unsigned d = (unsigned)abs(2 * dl - m);
-                const unsigned key = ((unsigned)k << 10) | (unsigned)(1023 - (int)(b & 1023u));
-                if (d < bd2 || (d == bd2 && key < bkey)) { bd2 = d; bkey = key; xk = a; xj = b; gk = q; gj = bst; }
+              // below (or equal): entry r (first of its equal-t block); needs t_j > t_k - m
+              if (r < eAo) {
+                const int dl = tk - (int)(cur >> 10);
+                if (dl < m) {  // dl > 0 since 2 t_j <= 2 t_k - m < 2 t_k
+                  const unsigned d = (unsigned)abs(2 * dl - m);
+                  const unsigned key = ((unsigned)k << 10) | (unsigned)(1023 - (int)(cur & 1023u));
+                  if (d < bd2 || (d == bd2 && key < bkey)) { bd2 = d; bkey = key; xk = a; xj = cur; gk = q; gj = r; }
+                }
               }
+              // above: first entry of the block before r; needs t_j < t_k
+              if (r > bA) {
+                const int dl = tk - (int)(bv >> 10);
+                if (dl > 0) {  // dl < m since 2 t_j > 2 t_k - m
+                  const unsigned d = (unsigned)abs(2 * dl - m);
+                  const unsigned key = ((unsigned)k << 10) | (unsigned)(1023 - (int)(bv & 1023u));
+                  if (d < bd2 || (d == bd2 && key < bkey)) { bd2 = d; bkey = key; xk = a; xj = bv; gk = q; gj = bst; }
+                }
+              }
+              a = an;
             }
           }
           if (bd2 != UINT_MAX) {  // T_k: I -> I^a and T_j: I^a -> I, both lists kept ordered

@@ -907,6 +907,7 @@ __device__ __noinline__ void solve_local(const KParams& P, int64_t inst, unsigne
         refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, (P.flags & FAR_NONEMPTY_ALT) != 0, lane, mv,
                         sw, it, ev);
       R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
+      __syncwarp();  // refine_best_warp's scratch is start[], which the replay writes
       const int msR = (P.flags & FAR_SWITCH_COST)
                           ? replay_tasks_warp<NC>(n, D, nlist, ncnt, su, nsum, start, bestnode, ninfo, cr, de, lane)
                           : replay_warp<NC>(n, D, nlist, ncnt, nsum, life, start, bestnode, ninfo, cr, de, lane);
@@ -1001,6 +1002,7 @@ __device__ void finish_core(const KParams& P, int64_t inst, uint16_t* nlist, int
         refine_warp<NC>(n, D, nlist, ncnt, send, ninfo, P.max_it, P.ppm, (P.flags & FAR_NONEMPTY_ALT) != 0, lane, mv,
                         sw, it, ev);
       R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
+      __syncwarp();  // refine_best_warp's scratch is start[], which the replay writes
     }
     if (!need_replay) break;
     const int msR = (P.flags & FAR_SWITCH_COST)
@@ -1567,6 +1569,7 @@ __device__ void solve_instance(const KParams& P, int64_t inst, unsigned char* ws
       gl[k] = max(lbh[k], lbs[k]);  // max(h_k, ceil(W_k / #slices))
       gc[k] = cnts[k];
     }
+    if (K + lane < ((K + 3) & ~3)) gl[K + lane] = INT_MAX;  // row padding (16-B loads in member0)
     // member 0's entries (interval lo == 0: the a^1 sizes), compacted per size for K2
     {
       uint32_t* gm = P.ws_m0 + inst * (int64_t)P.ws_n4;

@@ -350,6 +350,7 @@ __device__ __forceinline__ void prep_instance(const KParams& P, int64_t inst, un
       cc += __shfl_sync(FULL, dc, 31);
       ww += __shfl_sync(FULL, dw, 31);
     }
+    if (K + lane < ((K + 3) & ~3)) gl[K + lane] = INT_MAX;  // row padding (16-B loads in member0)
   }
 
   // ---- H3: every list entry -- the a^1 entry of each task and one growth entry per step (at the

@@ -449,3 +449,21 @@ def test_int64_domain_scaling(O, profile):
             assert rb[k] == ra[k], k
         assert (b["slots"]["node"] == a["slots"]["node"]).all()
         assert (b["slots"]["start"] == c * a["slots"]["start"]).all()
+
+
+def test_parallel_wrappers_agree_with_sequential(O):
+    """The process-pool fan-outs the full-size GPU parity tests use return exactly the sequential
+    oracle's makespans / reports (and, with the schedule check, flag a single corrupted slot)."""
+    from paper_2507_13601_b200 import inputs
+    w = inputs.WORKLOADS["M3"]
+    tab = w.table(count=130)
+    ms, res = O.far_many(w.profile, w.costs(), tab)
+    pm, pr = O.far_many_parallel(w.profile, w.costs(), tab, workers=2)
+    assert (pm == ms).all() and (pr == res).all()
+    sl = np.zeros((len(tab), tab.shape[1]), O.SLOT_DT)
+    for i in range(len(tab)):
+        sl[i] = O.far(w.profile, w.costs(), tab[i])["slots"]
+    cm, cr, nbad, first = O.far_many_parallel_check(w.profile, w.costs(), tab, sl, workers=2)
+    assert (cm == ms).all() and nbad == 0 and first == -1
+    sl[77, 3]["start"] += 1
+    assert O.far_many_parallel_check(w.profile, w.costs(), tab, sl, workers=2)[2:] == (1, 77)
