@@ -161,11 +161,13 @@ __device__ void refine_lane(uint32_t* ent, uint16_t* off, int (&send)[Tree<NC>::
         const int m = omega - eA;
         const int bI = off[I], nI = off[I + 1] - bI;
         evals += nI;
-        // move: argmin (|2t - m|, index) over t < m
+        // move: argmin (|2t - m|, index) over t < m; I is ordered by t descending, so there is no
+        // candidate unless its last (shortest) task is shorter than m -- the common case
         unsigned bd = UINT_MAX;
         int bj = INT_MAX;
         uint32_t bx = 0;
-        for (int q = bI; q < bI + nI; ++q) {
+        const bool movable = nI > 0 && (int)(ent[bI + nI - 1] >> 10) < m;
+        for (int q = bI; movable && q < bI + nI; ++q) {
           const uint32_t x = ent[q];
           const int t = (int)(x >> 10), j = 1023 - (int)(x & 1023u);
           if (t < m) {
@@ -298,9 +300,8 @@ __device__ void lane_lists(int n, const uint32_t* __restrict__ rec, const uint16
 
 // Warp-cooperative form of lane_lists for the active lanes' instances (mask am): the record of
 // instance i is read by the whole warp with coalesced 16-B loads (instead of one thread walking
-// 512 B with dependent loads) and its entries are written into lane i's row.  The next
-// instance's first 16-B chunk is loaded before the current one is scattered, so the loads of
-// consecutive instances overlap.  k0: bit i set if instance i's winner is member 0 (then the
+// 512 B with dependent loads) and its entries are written into lane i's row; the loads of four
+// instances are in flight together.  k0: bit i set if instance i's winner is member 0 (then the
 // durations prep wrote are read coalesced instead of gathered from the runtime table).  The rows'
 // off[] must already hold the node offsets and alt[] be zero.
 template <int NC>
@@ -320,26 +321,37 @@ __device__ void lane_lists_coop(int n, int64_t base, unsigned am, unsigned k0, c
       x = __ldcs((const uint4*)(P.ws_rec + inst * (int64_t)n) + q);
       dd = ((k0 >> i) & 1) ? __ldcs((const uint4*)(P.ws_d0 + inst * (int64_t)P.ws_n4) + q) : NOD;
     };
-    uint4 xn = NOD, dn = NOD;
-    if (am && lane < n4) load(__ffs(am) - 1, lane, xn, dn);
-    for (; am; am &= am - 1) {
-      const int i = __ffs(am) - 1;
-      const int64_t inst = base + i;
-      unsigned char* row = wrows + (size_t)i * rbytes;
-      uint32_t* ent = (uint32_t*)(row + L.ent);
-      const uint16_t* off = (const uint16_t*)(row + L.off);
-      uint32_t* alt = (uint32_t*)(row + L.alt);
-      const int32_t* t = P.times + inst * (int64_t)n * NC;
-      const uint4 x0 = xn, d0 = dn;
-      const unsigned rest = am & (am - 1);
-      if (rest && lane < n4) load(__ffs(rest) - 1, lane, xn, dn);
+    // groups of 4 instances: their 16-B record / duration loads are issued together, then scattered
+    // (one exposed load latency per group instead of per instance)
+    for (; am;) {
+      int ids[4];
+      uint4 x[4], dd[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ids[u] = am ? __ffs(am) - 1 : -1;
+        am &= am - 1;
+      }
       for (int q = lane; q < n4; q += 32) {
-        uint4 x = x0, dd = d0;
-        if (q != lane) load(i, q, x, dd);
-        put(ent, off, alt, t, 4 * q, x.x, (int)dd.x);
-        put(ent, off, alt, t, 4 * q + 1, x.y, (int)dd.y);
-        put(ent, off, alt, t, 4 * q + 2, x.z, (int)dd.z);
-        put(ent, off, alt, t, 4 * q + 3, x.w, (int)dd.w);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          x[u] = NOD;
+          dd[u] = NOD;
+          if (ids[u] >= 0) load(ids[u], q, x[u], dd[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (ids[u] < 0) continue;
+          const int64_t inst = base + ids[u];
+          unsigned char* row = wrows + (size_t)ids[u] * rbytes;
+          uint32_t* ent = (uint32_t*)(row + L.ent);
+          const uint16_t* off = (const uint16_t*)(row + L.off);
+          uint32_t* alt = (uint32_t*)(row + L.alt);
+          const int32_t* t = P.times + inst * (int64_t)n * NC;
+          put(ent, off, alt, t, 4 * q, x[u].x, (int)dd[u].x);
+          put(ent, off, alt, t, 4 * q + 1, x[u].y, (int)dd[u].y);
+          put(ent, off, alt, t, 4 * q + 2, x[u].z, (int)dd[u].z);
+          put(ent, off, alt, t, 4 * q + 3, x[u].w, (int)dd[u].w);
+        }
       }
     }
   } else {

@@ -223,6 +223,7 @@ __device__ int node_sim_warp(const int* ncnt, const int* nsum, int* life, const 
     life[lane * 6 + 0] = -1;  // not created
     life[lane * 6 + 2] = -1;  // not destroyed
   }
+  __syncwarp();  // lane 0 writes these slots below
   unsigned e = lane == 0 ? 0u : 0xFFFFFFFFu;  // root in slot 0 at time 0
   uint32_t slotnode = 0, live = 1, has = 0;
   int rec = 0, ms = 0, E = 0;

@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
     // ---- load the batch table and its FAR schedule; node lists ordered by (start, task)
     const int32_t* src = P.times + bi * (int64_t)n * NC;
     for (int q = lane; q < n * NC; q += 32) T[q] = __ldg(src + q);
+    __syncwarp();  // T is read below at other lanes' indices
     const far_task_slot* fs = P.sched + bi * (int64_t)n;
     for (int j = lane; j < n; j += 32) {
       const far_task_slot s = fs[j];
