@@ -387,17 +387,20 @@ __device__ int lane_replay(const uint32_t* ent, const uint16_t* off, const uint3
     if (!((F.has >> bs) & 1) && e > b) {  // creation (lines 8-11), then all of v's tasks
       rec = max(rec, be) + cr[nd_szi(w)];
       int acc = rec;
-      for (int q = b; q < e; ++q) {
-        const uint32_t x = ent[q];
-        if (out) {
+      if (out) {
+        // slot word node | size << 8 | start << 32; only the two-size node reads the alt bits
+        const unsigned lo0 = (unsigned)v | ((unsigned)size_of<NC>(nd_c0(w)) << 8);
+        const bool two = nd_c1(w) != NONE;
+        const unsigned lo1 = two ? (unsigned)v | ((unsigned)size_of<NC>(nd_c1(w)) << 8) : lo0;
+        for (int q = b; q < e; ++q) {
+          const uint32_t x = ent[q];
           const int j = 1023 - (int)(x & 1023u);
-          const int c = ((alt[j >> 5] >> (j & 31)) & 1) ? nd_c1(w) : nd_c0(w);
-          const unsigned long long s = (unsigned long long)(unsigned)v |
-                                       ((unsigned long long)(unsigned)size_of<NC>(c) << 8) |
-                                       ((unsigned long long)(unsigned)acc << 32);
-          *(unsigned long long*)(out + j) = s;
+          const unsigned lo = (two && ((alt[j >> 5] >> (j & 31)) & 1)) ? lo1 : lo0;
+          *(unsigned long long*)(out + j) = (unsigned long long)lo | ((unsigned long long)(unsigned)acc << 32);
+          acc += (int)(x >> 10);
         }
-        acc += (int)(x >> 10);
+      } else {
+        for (int q = b; q < e; ++q) acc += (int)(ent[q] >> 10);
       }
       ms = max(ms, acc);
       F.has |= 1u << bs;
