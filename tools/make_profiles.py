@@ -1,4 +1,4 @@
-"""Regenerate the round's profiles/ files from one GPU session's raw outputs:
+"""Regenerate the round's profiles/ files (and profiles/ncu_issue_M5.json) from one GPU session's raw outputs:
   python tools/make_profiles.py ROUND REPORT.ncu-rep LAUNCHES.csv BENCH.json
 writes profiles/ncu_traffic_M5.json, profiles/<ROUND>_ncu_final_raw.txt,
 profiles/<ROUND>_ncu_source_top_lines.txt, profiles/<ROUND>_launches.csv, profiles/<ROUND>_bench_full.json
@@ -22,6 +22,13 @@ tj = json.loads(traffic)
 tj["source"] = (f"ncu --set full capture of one far_solve_many chain, 200k M5 instances "
                 f"(profiles/{rnd}_ncu_summary.md)")
 json.dump(tj, open(os.path.join(P, "ncu_traffic_M5.json"), "w"), indent=1)
+# hardware view for bench.py's roofline.stages_hw: issued lane-ops (warp instructions x active lanes
+# per instruction) per instance of each kernel
+issue = {"workload": tj["workload"], "source": tj["source"],
+         "lane_ops_per_instance": {k["stage"]: k["warp_inst_per_instance"] * k["thread_inst_per_inst"]
+                                   for k in tj["kernels"]},
+         "warp_inst_per_instance": {k["stage"]: k["warp_inst_per_instance"] for k in tj["kernels"]}}
+json.dump(issue, open(os.path.join(P, "ncu_issue_M5.json"), "w"), indent=1)
 
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
@@ -49,7 +56,8 @@ for k in keys:
 open(os.path.join(P, f"{rnd}_ncu_final_raw.txt"), "w").write("\n".join(out) + "\n")
 
 top = []
-for skip, name in ((0, "far_solve_kernel<5, PIPE_PREP> (prep)"), (4, "far_finish_lane_kernel<5> (finish)")):
+for skip, name in ((0, "far_prep_kernel<5> (prep)"), (1, "far_member0_kernel<5> (member0)"),
+                   (2, "far_members_kernel<5> (members)"), (4, "far_finish_lane_kernel<5> (finish)")):
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
                           "--launch-skip", str(skip), "--launch-count", "1"], capture_output=True, text=True).stdout
     tmp = os.path.join("/tmp", f"src_{skip}.csv")

@@ -29,7 +29,8 @@ for k, r in enumerate(rows[2:]):
                            "dram_read_bytes_per_instance": rd / inst, "dram_write_bytes_per_instance": wr / inst,
                            "warps_active_pct": float(r[col["sm__warps_active.avg.pct_of_peak_sustained_active"]]),
                            "issue_active_pct": float(r[col["smsp__issue_active.avg.pct_of_peak_sustained_active"]]),
-                           "thread_inst_per_inst": float(r[col["smsp__thread_inst_executed_per_inst_executed.ratio"]])})
+                           "thread_inst_per_inst": float(r[col["smsp__thread_inst_executed_per_inst_executed.ratio"]]),
+                           "warp_inst_per_instance": val("smsp__inst_executed.sum") / inst})
 out["dram_read_bytes_per_instance"] = tot_r / inst
 out["dram_write_bytes_per_instance"] = tot_w / inst
 out["chain_ms_cold_serialised"] = tot_t * 1e3
