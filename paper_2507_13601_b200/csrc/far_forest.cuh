@@ -668,6 +668,7 @@ __global__ void __launch_bounds__(128) far_forest_kernel(FParams F) {
                 if (i >= q) glist[nc * n + i + 1] = val;
                 __syncwarp();
               }
+              __syncwarp();  // every lane has read gcnt[] (the shift loop may not have run)
               if (lane == 0) {
                 glist[nc * n + q] = (uint16_t)j;
                 gcnt[c] = cnt - 1;

@@ -426,6 +426,7 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
     const SeamRes R = eval_seam<NC>(n, T, su, D, nl, ncnt, nsum, onode, start, life, ninfo, cr, de, rev, st, win, lane);
     const long long O = R.O;
     ms = max(ms, O + R.task_end);
+    __syncwarp();  // every lane's reads of the stream state (eval_seam) precede lane 0's update
     if (lane == 0) {
       // elide the destroys of reused boundary instances
       for (int s = 0; s < S; ++s) {
