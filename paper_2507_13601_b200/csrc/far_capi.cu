@@ -129,8 +129,11 @@ static far_status ensure_device(far_ctx* ctx) {
   for (const void* f : fns) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   CK(cudaFuncSetAttribute((const void*)far_forest_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   CK(cudaFuncSetAttribute((const void*)far_forest_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
-  CK(cudaFuncSetAttribute((const void*)far_prep_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
-  CK(cudaFuncSetAttribute((const void*)far_prep_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
+  {
+    const void* pf[4] = {(const void*)far_prep_kernel<3, true>, (const void*)far_prep_kernel<3, false>,
+                         (const void*)far_prep_kernel<5, true>, (const void*)far_prep_kernel<5, false>};
+    for (const void* f : pf) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
+  }
   if (ctx->gpus > 1) {
     CK(cudaMalloc(&ctx->d_fnodes, sizeof(uint2) * FMAXNN));
     CK(cudaMemcpy(ctx->d_fnodes, ctx->fnodes, sizeof(uint2) * ctx->nn * ctx->gpus, cudaMemcpyHostToDevice));
@@ -262,18 +265,27 @@ static far_status launch_warp_kernel(far_ctx* ctx, KParams& P, cudaStream_t stre
   return FAR_OK;
 }
 
-// K1 for n <= 128: far_prep_kernel<NC> (far_prep.cuh).
-static far_status launch_prep(far_ctx* ctx, KParams& P, cudaStream_t stream) {
-  const void* fn = ctx->nc == 3 ? (const void*)far_prep_kernel<3> : (const void*)far_prep_kernel<5>;
+// K1 for n <= 128 (far_prep.cuh): far_prep_kernel<NC, true> over every instance, then
+// far_prep_kernel<NC, false> over the instances it listed (non-monotone chains; exits at once when
+// the list is empty).  P.counter / P.gen_count: two counter slots of this launch.
+static far_status launch_prep(far_ctx* ctx, KParams& P, cudaStream_t stream, unsigned long long* counter2) {
+  const bool a30 = ctx->nc == 3;
   const PLayout L = make_playout(P.n, ctx->nc, P.kcap);
-  int warps = 0, per_sm = 0;
-  far_status st = pick_shape(ctx, fn, L.bytes, warps, per_sm);
-  if (st) return st;
-  const size_t smem = (size_t)warps * L.bytes;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((P.I + warps - 1) / warps, (int64_t)ctx->sms * per_sm));
-  void* args[] = {&P};
-  CK(cudaLaunchKernel(fn, grid, warps * 32, args, smem, stream));
-  ++ctx->launches;
+  for (int pass = 0; pass < 2; ++pass) {
+    const void* fn = pass == 0 ? (a30 ? (const void*)far_prep_kernel<3, true> : (const void*)far_prep_kernel<5, true>)
+                               : (a30 ? (const void*)far_prep_kernel<3, false> : (const void*)far_prep_kernel<5, false>);
+    int warps = 0, per_sm = 0;
+    far_status st = pick_shape(ctx, fn, L.bytes, warps, per_sm);
+    if (st) return st;
+    const size_t smem = (size_t)warps * L.bytes;
+    int64_t units = pass == 0 ? P.I : std::min<int64_t>(P.I, (int64_t)ctx->sms * per_sm * warps);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((units + warps - 1) / warps, (int64_t)ctx->sms * per_sm));
+    KParams Q = P;
+    if (pass == 1) Q.counter = counter2;
+    void* args[] = {&Q};
+    CK(cudaLaunchKernel(fn, grid, warps * 32, args, smem, stream));
+    ++ctx->launches;
+  }
   return FAR_OK;
 }
 
@@ -359,7 +371,8 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     const int n4 = (P.n + 3) & ~3;
     const size_t o_ncnt = o_m0 + a256(I * (size_t)n4 * 4);
     const size_t o_d0 = o_ncnt + a256(I * 32);
-    const size_t o_end = o_d0 + a256(I * (size_t)n4 * 4);
+    const size_t o_gen = o_d0 + a256(I * (size_t)n4 * 4);
+    const size_t o_end = o_gen + a256(I * 8);
     const int r = (int)(lid & 1);
     if ((st = order_after(ctx, ctx->pws_last[r], stream))) return st;
     ctx->pws_last[r] = lid;
@@ -385,7 +398,9 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     P.ovf_pass = 0;
     P.counter = ctx->d_counter + slot + 0;
     if (P.n <= 128 && kfast <= 129 && !(P.flags & FAR_GROW_TIES) && !getenv("FAR_OLD_PREP")) {
-      if ((st = launch_prep(ctx, P, stream))) return st;
+      P.gen_list = (int64_t*)(w + o_gen);
+      P.gen_count = ctx->d_counter + slot + 6;
+      if ((st = launch_prep(ctx, P, stream, ctx->d_counter + slot + 7))) return st;
     } else if ((st = launch_warp_kernel(ctx, P, stream, P.I, PIPE_PREP))) {
       return st;
     }

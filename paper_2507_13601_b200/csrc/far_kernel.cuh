@@ -65,6 +65,8 @@ struct KParams {
   uint32_t* ws_m0;              // [I][ws_n4]    member 0's compact per-size LPT lists (t | task << 22)
   int ws_n4;
   uint32_t* ws_d0;              // [I][ws_n4]    member 0's duration per task t_j(a1_j) (finish, k* = 0)
+  int64_t* gen_list;            // [I]           instances for the general prep (far_prep.cuh)
+  unsigned long long* gen_count;
 };
 enum { PIPE_NONE = 0, PIPE_PREP = 1 };  // far_solve_kernel template modes: fused / H0-H3 -> ws
 enum { WS_FLAG = 8, WS_K = 9 };  // ws_meta slots: flag 0 = phase 2 pending, 1 = finished or deferred

@@ -114,15 +114,86 @@ __device__ __forceinline__ unsigned growth_key(int t, int j, int p) {
   return ((unsigned)t << 10) | ((unsigned)(127 - j) << 3) | (unsigned)(7 - p);
 }
 
+// H2 when some task's t increases along its growth chain: the growth process step by step
+// (P:343-352): grow the longest current task (ties -> lowest index) to its next chain size; stop
+// when it is already at the largest size.  Writes steps[k] = task | its step number << 8 (into gk),
+// counts each task's steps in info (bits 8-10), returns the number of steps (-1 if the family
+// exceeds kcap) and the longest time of the last member in tlast.
 template <int NC>
-__device__ __forceinline__ void prep_instance(const KParams& P, int64_t inst, unsigned char* wsm, const PLayout& L,
-                                           int lane) {
+__device__ __forceinline__ int seq_growth(const int32_t* T, uint32_t* info, uint32_t* gk, int n, int kcap, int lane,
+                                       unsigned& tlast) {
+  uint32_t* steps = gk;                     // dead until the list keys are built
+  uint8_t* curc = (uint8_t*)(gk + kcap);    // current size index per task
+  for (int j = lane; j < n; j += 32) curc[j] = (uint8_t)(info[j] & 7u);
+  __syncwarp();
+  unsigned lk = 0;
+  for (int j = lane; j < n; j += 32) lk = max(lk, ((unsigned)T[j * NC + curc[j]] << 10) | (unsigned)(1023 - j));
+  int K = 1;
+  for (;;) {
+    const unsigned gkey = __reduce_max_sync(FULL, lk);
+    const int jj = 1023 - (int)(gkey & 1023u);
+    const int c = curc[jj];
+    if (c == NC - 1) {
+      tlast = gkey >> 10;
+      return K - 1;
+    }
+    if (K >= kcap) return -1;
+    const uint32_t w = info[jj];
+    __syncwarp();
+    if (lane == 0) {
+      steps[K - 1] = (uint32_t)jj | (((w >> 8) & 7u) << 8);
+      info[jj] = w + (1u << 8);
+      curc[jj] = (uint8_t)(__ffs(((w >> 3) & 31u) & ~((2u << c) - 1u)) - 1);
+    }
+    __syncwarp();
+    if (lane == (jj & 31)) {
+      lk = 0;
+      for (int j = lane; j < n; j += 32) lk = max(lk, ((unsigned)T[j * NC + curc[j]] << 10) | (unsigned)(1023 - j));
+    }
+    ++K;
+  }
+}
+
+// The sequential steps as elements: step k is task j's p-th, its element index is first_j + p;
+// its rank is k.
+template <int NC>
+__device__ __forceinline__ void seq_elements(const uint32_t* info, const uint32_t* steps, uint32_t* ginfo, int* rnk,
+                                          int Gn, int lane) {
+  for (int k = lane; k < Gn; k += 32) {
+    const uint32_t x = steps[k];
+    const int j = (int)(x & 255u), p = (int)(x >> 8);
+    const uint32_t w = info[j];
+    const int g = (int)((w >> 8) & 7u);
+    unsigned m = (w >> 3) & 31u;
+    for (int q = 0; q < p; ++q) m &= m - 1;
+    const int c = __ffs(m) - 1;
+    m &= m - 1;
+    const int e = (int)(w >> 11) + p;
+    rnk[e] = k;
+    ginfo[e] = (uint32_t)j | ((uint32_t)c << 8) | ((uint32_t)(__ffs(m) - 1) << 11) | ((uint32_t)(p == g - 1) << 14);
+  }
+}
+
+// Defer an instance to the fused overflow pass (outside the prep kernel's domain).
+__device__ __forceinline__ void defer_instance(const KParams& P, int64_t inst, int lane) {
+  if (lane == 0) {
+    atomicOr(P.ovf + (inst >> 5), 1u << (inst & 31));
+    atomicAdd(P.ovf_count, 1ull);
+    P.ws_meta[inst * 16 + WS_FLAG] = 1;
+  }
+}
+
+// H2-H3 and the workspace outputs.  MONO: every task's t is non-increasing along its growth chain
+// (the hot path: the merge form of H2); otherwise the step-by-step growth (out of line).
+template <int NC, bool MONO>
+__device__ __forceinline__ void prep_rest(const KParams& P, int64_t inst, unsigned char* wsm, const PLayout& L,
+                                          int lane, unsigned tstar, unsigned W, unsigned long long c0) {
   constexpr int S = Tree<NC>::S;
   const int n = P.n;
   int32_t* T = (int32_t*)(wsm + L.T);
-  uint32_t* info = (uint32_t*)(wsm + L.info);  // a^1 | chain mask << 3 | #steps << 8 | first step << 11
+  uint32_t* info = (uint32_t*)(wsm + L.info);
   unsigned* gk = (unsigned*)(wsm + L.gk);
-  uint32_t* ginfo = (uint32_t*)(wsm + L.ginfo);  // task | from << 8 | to << 11 | last-of-task << 14
+  uint32_t* ginfo = (uint32_t*)(wsm + L.ginfo);
   int* rnk = (int*)(wsm + L.rnk);
   unsigned long long* cnts = (unsigned long long*)(wsm + L.cnts);
   unsigned* lbs = (unsigned*)(wsm + L.lbs);
@@ -130,103 +201,13 @@ __device__ __forceinline__ void prep_instance(const KParams& P, int64_t inst, un
   unsigned* kk = (unsigned*)(wsm + L.kk);
   int* meta = P.ws_meta + inst * 16;
   const unsigned lt = (1u << lane) - 1u;
-
-  // ---- H0
-  {
-    const int cntT = n * NC;
-    const int32_t* src = P.times + inst * (int64_t)cntT;
-    if ((((uintptr_t)src) & 15) == 0) {
-      const int n4 = cntT >> 2;
-      const int4* s4 = (const int4*)src;
-      int4* d4 = (int4*)T;
-      for (int q = lane; q < n4; q += 32) d4[q] = __ldcs(s4 + q);
-      for (int q = (n4 << 2) + lane; q < cntT; q += 32) T[q] = __ldcs(src + q);
-    } else {
-      for (int q = lane; q < cntT; q += 32) T[q] = __ldcs(src + q);
-    }
-  }
-  __syncwarp();
-
-  // ---- H1: a^1, chains, member-0 counts and area, input checks
-  int bad = 0, mono = 1;
-  long long bsum = 0;
-  int tmax = 0;
-  unsigned W = 0, tstar = 0;
-  unsigned long long c0 = 0;
-  uint32_t* d0 = P.ws_d0 + inst * (int64_t)P.ws_n4;
-#pragma unroll 1
-  for (int j = lane; j < n; j += 32) {
-    int tv[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) tv[c] = T[j * NC + c];
-    int mx = tv[0], mn = tv[0];
-#pragma unroll
-    for (int c = 1; c < NC; ++c) {
-      mx = max(mx, tv[c]);
-      mn = min(mn, tv[c]);
-    }
-    bad |= mn < 1;
-    bsum += mx;
-    tmax = max(tmax, mx);
-    // 32-bit products: meaningful once t < 2^22 is established (checked below)
-    int best = 0;
-    unsigned bw = (unsigned)tv[0];
-#pragma unroll
-    for (int c = 1; c < NC; ++c) {
-      const unsigned w = (unsigned)size_of<NC>(c) * (unsigned)tv[c];
-      if (w < bw) { bw = w; best = c; }
-    }
-    unsigned nxp = 0;  // nx(c), 3 bits per size index
-    {
-      int above = NC - 1;
-      unsigned wa = (unsigned)size_of<NC>(NC - 1) * (unsigned)tv[NC - 1];
-#pragma unroll
-      for (int c = NC - 2; c >= 0; --c) {
-        nxp |= (unsigned)above << (3 * c);
-        const unsigned wc = (unsigned)size_of<NC>(c) * (unsigned)tv[c];
-        if (wc <= wa) { wa = wc; above = c; }
-      }
-    }
-    unsigned cb = 0;
-    int nextc = best, tprev = INT_MAX;
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-      if (c == nextc) {
-        cb |= 1u << c;
-        mono &= tv[c] <= tprev;
-        tprev = tv[c];
-        nextc = c == NC - 1 ? NC : (int)((nxp >> (3 * c)) & 7u);
-      }
-    tstar = max(tstar, growth_key<NC>(tv[NC - 1], j, __popc(cb) - 1));
-    W += bw;
-    c0 += 1ull << (11 * best);
-    d0[j] = (uint32_t)tv[best];  // t_j(a^1_j): member 0's duration (finish, k* = 0)
-    info[j] = (uint32_t)best | (cb << 3);
-  }
-  bad = __any_sync(FULL, bad);
-  bsum = warp_sum_ll(bsum);
-  if (bad || bsum + P.rsum >= BOUND) {
-    if (lane == 0) {
-      far_result R0;
-      R0.makespan = -1; R0.makespan_phase2 = 0; R0.alloc_index = 0; R0.family_size = 0;
-      R0.moves = 0; R0.swaps = 0; R0.iterations = 0; R0.reverted = 0; R0.status = FAR_E_BAD_TIME; R0.reserved = 0;
-      R0.evals = 0; R0.events = 0;
-      P.makespan[inst] = -1;
-      if (P.res) P.res[inst] = R0;
-      atomicOr(P.errflag, 1);
-      meta[WS_FLAG] = 1;
-    }
-    return;
-  }
-  tmax = __reduce_max_sync(FULL, tmax);
+  auto defer = [&]() { defer_instance(P, inst, lane); };
   int Gn = 0;
-  if (__all_sync(FULL, mono) && tmax < (1 << 22)) {
-    tstar = __reduce_max_sync(FULL, tstar);
-    W = __reduce_add_sync(FULL, W);
-    c0 = (unsigned long long)warp_sum_ll((long long)c0);
+  unsigned tlast = tstar >> 10;  // longest task of the last member
+  int gsum = 0;  // this lane's steps
+  if (MONO) {
     // ---- H2: growth steps = non-terminal chain elements with key > T*, a prefix of each chain
     //      (keys strictly decrease along a chain, so the count needs no early exit)
-    int gsum = 0;
 #pragma unroll 1
     for (int j = lane; j < n; j += 32) {
       const uint32_t w = info[j];
@@ -241,31 +222,48 @@ __device__ __forceinline__ void prep_instance(const KParams& P, int64_t inst, un
       info[j] = w | ((uint32_t)g << 8);
       gsum += g;
     }
+    Gn = __reduce_add_sync(FULL, gsum);
+  } else {
+    // ---- H2, general form (a chain along which t increases), out of line: keeps the hot
+    //      monotone path inside the instruction cache
+    Gn = seq_growth<NC>(T, info, gk, n, P.kcap, lane, tlast);
+    if (Gn < 0) {
+      defer();
+      return;
+    }
+    for (int j = lane; j < n; j += 32) gsum += (int)((info[j] >> 8) & 7u);
+  }
+  if (Gn + 1 > P.kcap) {
+    defer();
+    return;
+  }
+  const int K = Gn + 1;
+  // first step index per task (lane-major order of tasks; a task's steps are consecutive and in
+  // chain order); the growing tasks (g > 0, at most Gn of them) listed in gt
+  {
     int excl = gsum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(FULL, excl, o);
       if (lane >= o) excl += y;
     }
-    Gn = __shfl_sync(FULL, excl, 31);
     excl -= gsum;
-    if (Gn + 1 <= P.kcap) {
-      // first step index per task; the growing tasks (g > 0, at most Gn of them) listed in gt
-      uint32_t* gt = (uint32_t*)lbh;  // lbh is written after the steps are ranked
-      int ng = 0;
+    uint32_t* gt = (uint32_t*)lbh;  // lbh is written after the steps are ranked
+    int ng = 0;
 #pragma unroll 1
-      for (int j0 = 0; j0 < n; j0 += 32) {
-        const int j = j0 + lane;
-        const uint32_t w = j < n ? info[j] : 0u;
-        const int g = (int)((w >> 8) & 7u);
-        if (j < n) info[j] = w | ((uint32_t)excl << 11);
-        const unsigned b = __ballot_sync(FULL, g > 0);
-        if (g > 0) gt[ng + __popc(b & lt)] = (uint32_t)j | ((uint32_t)excl << 8);
-        ng += __popc(b);
-        excl += g;
-      }
-      __syncwarp();
-      // steps of each growing task in chain order (lane per growing task)
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      const uint32_t w = j < n ? info[j] : 0u;
+      const int g = (int)((w >> 8) & 7u);
+      if (j < n) info[j] = w | ((uint32_t)excl << 11);
+      const unsigned b = __ballot_sync(FULL, g > 0);
+      if (g > 0) gt[ng + __popc(b & lt)] = (uint32_t)j | ((uint32_t)excl << 8);
+      ng += __popc(b);
+      excl += g;
+    }
+    __syncwarp();
+    if (MONO) {
+      // steps of each growing task in chain order (lane per growing task), keyed for the ranking
 #pragma unroll 1
       for (int i = lane; i < ng; i += 32) {
         const uint32_t x = gt[i];
@@ -282,27 +280,17 @@ __device__ __forceinline__ void prep_instance(const KParams& P, int64_t inst, un
         }
       }
       if (lane < ((Gn + 3) & ~3) - Gn) gk[Gn + lane] = 0u;  // pads: never above a key
-    }
-  }
-  if (!__all_sync(FULL, mono) || tmax >= (1 << 22) || Gn + 1 > P.kcap) {
-    // outside this kernel's domain: the fused kernel solves it (overflow pass)
-    if (lane == 0) {
-      atomicOr(P.ovf + (inst >> 5), 1u << (inst & 31));
-      atomicAdd(P.ovf_count, 1ull);
-      meta[WS_FLAG] = 1;
-    }
-    return;
-  }
-  const int K = Gn + 1;
-  __syncwarp();
-  // rank of each step = #steps with a larger key (step rk turns member rk into member rk + 1)
-  {
-    const int Gp = (Gn + 3) & ~3;
+      __syncwarp();
+      // rank of each step = #steps with a larger key (step rk turns member rk into member rk + 1)
+      const int Gp = (Gn + 3) & ~3;
 #pragma unroll 1
-    for (int e = lane; e - lane < Gn; e += 32) {
-      const unsigned key = e < Gn ? gk[e] : 0xFFFFFFFFu;
-      const int c = count_le(gk, 0, Gp, key);
-      if (e < Gn) rnk[e] = Gp - c;
+      for (int e = lane; e - lane < Gn; e += 32) {
+        const unsigned key = e < Gn ? gk[e] : 0xFFFFFFFFu;
+        const int c = count_le(gk, 0, Gp, key);
+        if (e < Gn) rnk[e] = Gp - c;
+      }
+    } else {
+      seq_elements<NC>(info, gk, ginfo, rnk, Gn, lane);
     }
   }
   __syncwarp();
@@ -320,7 +308,7 @@ __device__ __forceinline__ void prep_instance(const KParams& P, int64_t inst, un
     gent += 1ull << (11 * ct);
   }
   if (lane == 0) {
-    lbh[Gn] = (int)(tstar >> 10);
+    lbh[Gn] = (int)tlast;
     cnts[0] = c0;
     lbs[0] = W;
   }
@@ -430,20 +418,159 @@ __device__ __forceinline__ void prep_instance(const KParams& P, int64_t inst, un
   }
 }
 
-template <int NC>
+template <int NC, bool MONO>
+__device__ __forceinline__ void prep_instance(const KParams& P, int64_t inst, unsigned char* wsm, const PLayout& L,
+                                           int lane) {
+  constexpr int S = Tree<NC>::S;
+  const int n = P.n;
+  int32_t* T = (int32_t*)(wsm + L.T);
+  uint32_t* info = (uint32_t*)(wsm + L.info);  // a^1 | chain mask << 3 | #steps << 8 | first step << 11
+  unsigned* gk = (unsigned*)(wsm + L.gk);
+  uint32_t* ginfo = (uint32_t*)(wsm + L.ginfo);  // task | from << 8 | to << 11 | last-of-task << 14
+  int* rnk = (int*)(wsm + L.rnk);
+  unsigned long long* cnts = (unsigned long long*)(wsm + L.cnts);
+  unsigned* lbs = (unsigned*)(wsm + L.lbs);
+  int* lbh = (int*)(wsm + L.lbh);
+  unsigned* kk = (unsigned*)(wsm + L.kk);
+  int* meta = P.ws_meta + inst * 16;
+  const unsigned lt = (1u << lane) - 1u;
+
+  // ---- H0
+  {
+    const int cntT = n * NC;
+    const int32_t* src = P.times + inst * (int64_t)cntT;
+    if ((((uintptr_t)src) & 15) == 0) {
+      const int n4 = cntT >> 2;
+      const int4* s4 = (const int4*)src;
+      int4* d4 = (int4*)T;
+      for (int q = lane; q < n4; q += 32) d4[q] = __ldcs(s4 + q);
+      for (int q = (n4 << 2) + lane; q < cntT; q += 32) T[q] = __ldcs(src + q);
+    } else {
+      for (int q = lane; q < cntT; q += 32) T[q] = __ldcs(src + q);
+    }
+  }
+  __syncwarp();
+
+  // ---- H1: a^1, chains, member-0 counts and area, input checks
+  int bad = 0, mono = 1;
+  long long bsum = 0;
+  int tmax = 0;
+  unsigned W = 0, tstar = 0;
+  unsigned long long c0 = 0;
+  uint32_t* d0 = P.ws_d0 + inst * (int64_t)P.ws_n4;
+#pragma unroll 1
+  for (int j = lane; j < n; j += 32) {
+    int tv[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) tv[c] = T[j * NC + c];
+    int mx = tv[0], mn = tv[0];
+#pragma unroll
+    for (int c = 1; c < NC; ++c) {
+      mx = max(mx, tv[c]);
+      mn = min(mn, tv[c]);
+    }
+    bad |= mn < 1;
+    bsum += mx;
+    tmax = max(tmax, mx);
+    // 32-bit products: meaningful once t < 2^22 is established (checked below)
+    int best = 0;
+    unsigned bw = (unsigned)tv[0];
+#pragma unroll
+    for (int c = 1; c < NC; ++c) {
+      const unsigned w = (unsigned)size_of<NC>(c) * (unsigned)tv[c];
+      if (w < bw) { bw = w; best = c; }
+    }
+    unsigned nxp = 0;  // nx(c), 3 bits per size index
+    {
+      int above = NC - 1;
+      unsigned wa = (unsigned)size_of<NC>(NC - 1) * (unsigned)tv[NC - 1];
+#pragma unroll
+      for (int c = NC - 2; c >= 0; --c) {
+        nxp |= (unsigned)above << (3 * c);
+        const unsigned wc = (unsigned)size_of<NC>(c) * (unsigned)tv[c];
+        if (wc <= wa) { wa = wc; above = c; }
+      }
+    }
+    unsigned cb = 0;
+    int nextc = best, tprev = INT_MAX;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c == nextc) {
+        cb |= 1u << c;
+        mono &= tv[c] <= tprev;
+        tprev = tv[c];
+        nextc = c == NC - 1 ? NC : (int)((nxp >> (3 * c)) & 7u);
+      }
+    tstar = max(tstar, growth_key<NC>(tv[NC - 1], j, __popc(cb) - 1));
+    W += bw;
+    c0 += 1ull << (11 * best);
+    d0[j] = (uint32_t)tv[best];  // t_j(a^1_j): member 0's duration (finish, k* = 0)
+    info[j] = (uint32_t)best | (cb << 3);
+  }
+  bad = __any_sync(FULL, bad);
+  bsum = warp_sum_ll(bsum);
+  if (bad || bsum + P.rsum >= BOUND) {
+    if (lane == 0) {
+      far_result R0;
+      R0.makespan = -1; R0.makespan_phase2 = 0; R0.alloc_index = 0; R0.family_size = 0;
+      R0.moves = 0; R0.swaps = 0; R0.iterations = 0; R0.reverted = 0; R0.status = FAR_E_BAD_TIME; R0.reserved = 0;
+      R0.evals = 0; R0.events = 0;
+      P.makespan[inst] = -1;
+      if (P.res) P.res[inst] = R0;
+      atomicOr(P.errflag, 1);
+      meta[WS_FLAG] = 1;
+    }
+    return;
+  }
+  tmax = __reduce_max_sync(FULL, tmax);
+  auto defer = [&]() {  // outside this kernel's domain: the fused kernel solves it (overflow pass)
+    if (lane == 0) {
+      atomicOr(P.ovf + (inst >> 5), 1u << (inst & 31));
+      atomicAdd(P.ovf_count, 1ull);
+      meta[WS_FLAG] = 1;
+    }
+  };
+  if (tmax >= (1 << 22)) {
+    defer();
+    return;
+  }
+  const bool allmono = __all_sync(FULL, mono);
+  tstar = __reduce_max_sync(FULL, tstar);
+  W = __reduce_add_sync(FULL, W);
+  c0 = (unsigned long long)warp_sum_ll((long long)c0);
+  if (MONO) {
+    if (!allmono) {  // the general prep kernel (next launch) takes it
+      if (lane == 0) {
+        P.gen_list[atomicAdd(P.gen_count, 1ull)] = inst;
+        meta[WS_FLAG] = 1;
+      }
+      return;
+    }
+    prep_rest<NC, true>(P, inst, wsm, L, lane, tstar, W, c0);
+  } else {
+    prep_rest<NC, false>(P, inst, wsm, L, lane, tstar, W, c0);
+  }
+}
+
+// MONO = true: every instance (the monotone merge form of H2); instances with a chain along which
+// t increases are appended to P.gen_list.  MONO = false: the instances of P.gen_list, with the
+// step-by-step H2 (a separate, normally empty launch keeps that code out of the hot kernel's
+// instruction-cache footprint).
+template <int NC, bool MONO>
 __global__ void __launch_bounds__(128, 8) far_prep_kernel(KParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const PLayout L = make_playout(P.n, NC, P.kcap);
   unsigned char* wsm = smem + (size_t)warp * L.bytes;
+  const int64_t total = MONO ? P.I : (int64_t)*(volatile unsigned long long*)P.gen_count;
   // dynamic instance scheduler, next index claimed one instance ahead
   unsigned long long nxt = 0;
   if (lane == 0) nxt = atomicAdd(P.counter, 1ull);
   for (;;) {
-    const unsigned long long inst = __shfl_sync(FULL, nxt, 0);
-    if ((int64_t)inst >= P.I) break;
+    const unsigned long long it = __shfl_sync(FULL, nxt, 0);
+    if ((int64_t)it >= total) break;
     if (lane == 0) nxt = atomicAdd(P.counter, 1ull);
-    prep_instance<NC>(P, (int64_t)inst, wsm, L, lane);
+    prep_instance<NC, MONO>(P, MONO ? (int64_t)it : P.gen_list[it], wsm, L, lane);
     __syncwarp();
   }
 }
