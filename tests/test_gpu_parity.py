@@ -540,3 +540,18 @@ def test_sync_calls_keep_the_async_error_flag(torch_dev):
         F.solve_many_host(np.ascontiguousarray(bad))
     assert e.value.status == 3
     F.sync()                                              # ... and leaves no flag behind
+
+
+@pytest.mark.parametrize("profile,n", [("A100", 128), ("A100", 37), ("A30", 64), ("H100", 100)])
+def test_general_prep_mixed_batches(O, torch_dev, profile, n):
+    """Batches mixing monotone instances (far_prep_kernel<NC, true>, the merge form of phase 1) and
+    non-monotone ones (listed by it and prepared by far_prep_kernel<NC, false>, the step-by-step
+    growth of P:343-352) in one far_solve_many call: every instance, field and slot bit-exact, with
+    and without the lower-bound pruning."""
+    costs = inputs.reconfig_costs(profile)
+    mono = inputs.synthetic(profile, n, 300, 41 + n)
+    rnd = inputs.uniform_random(profile, n, 300, 43 + n)
+    tab = np.ascontiguousarray(np.concatenate([mono, rnd])[np.random.default_rng(n).permutation(600)])
+    for flags in (0, far.EXHAUSTIVE):
+        ms, slots, res = run_gpu(torch_dev, profile, costs, tab, flags=flags)
+        check_against_oracle(O, profile, costs, tab, ms, slots, res, flags=flags, full=True)
