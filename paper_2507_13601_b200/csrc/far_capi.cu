@@ -444,10 +444,8 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     else far_members_kernel<5><<<g_items, tb, psm, stream>>>(Q);
     CK(cudaGetLastError());
     if ((st = t_mark(ctx, tset, stream, FAR_STAGE_MEMBERS))) return st;
-    int g_win = g_inst;
-    if (const char* e = getenv("FAR_DEBUG_WINNER_BPS")) g_win = (int)std::min<int64_t>(g_inst, (int64_t)ctx->sms * atoi(e));
-    if (a30) far_winner_kernel<3><<<g_win, tb, psm, stream>>>(Q);
-    else far_winner_kernel<5><<<g_win, tb, psm, stream>>>(Q);
+    if (a30) far_winner_kernel<3><<<g_inst, tb, psm, stream>>>(Q);
+    else far_winner_kernel<5><<<g_inst, tb, psm, stream>>>(Q);
     CK(cudaGetLastError());
     ctx->launches += 3;
     if ((st = t_mark(ctx, tset, stream, FAR_STAGE_WINNER))) return st;
