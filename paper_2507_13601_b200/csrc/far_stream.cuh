@@ -101,7 +101,7 @@ struct SeamRes {
 
 // Timeline of the batch described by (nl, ncnt) + its seam against the stream state.
 template <int NC>
-__device__ SeamRes eval_seam(int n, const int32_t* T, const uint8_t* su, const int* D, const uint16_t* nl,
+__device__ __noinline__ SeamRes eval_seam(int n, const int32_t* T, const uint8_t* su, const int* D, const uint16_t* nl,
                              const int* ncnt, int* nsum, uint8_t* onode, int* start, int* life, const uint32_t* ninfo,
                              const int* cr, const int* de, bool rev, const StreamSt* st, const WinEv* win, int lane) {
   constexpr int S = Tree<NC>::S, NN = Tree<NC>::NN;
@@ -296,17 +296,38 @@ __global__ void __launch_bounds__(128) far_stream_kernel(SParams P) {
       D[j] = T[j * NC + su[j]];
     }
     __syncwarp();
-    for (int j = lane; j < n; j += 32) {
-      const int v = start[j], sj = fstart[j];
-      int pos = 0;
-      for (int q = 0; q < n; ++q) pos += (start[q] == v) && (fstart[q] < sj || (fstart[q] == sj && q < j));
-      nl[v * n + pos] = (uint16_t)j;
-    }
-    for (int v = 0; v < NN; ++v) {
-      int c = 0;
-      for (int j = lane; j < n; j += 32) c += (start[j] == v);
-      c = __reduce_add_sync(FULL, c);
-      if (lane == 0) ncnt[v] = c;
+    // node lists ordered by (start, task): the tasks grouped by node with ballots (into nl2, free
+    // until the seam refinement; group offsets in nsum, rewritten by the replay), then each task
+    // ranked among its node's few tasks
+    {
+      const unsigned lt = (1u << lane) - 1u;
+      int goff = 0;
+      for (int v = 0; v < NN; ++v) {
+        int c = 0;
+        for (int j0 = 0; j0 < n; j0 += 32) {
+          const int j = j0 + lane;
+          const bool in = j < n && start[j] == v;
+          const unsigned b = __ballot_sync(FULL, in);
+          if (in) nl2[goff + c + __popc(b & lt)] = (uint16_t)j;
+          c += __popc(b);
+        }
+        if (lane == 0) {
+          ncnt[v] = c;
+          nsum[v] = goff;
+        }
+        goff += c;
+      }
+      __syncwarp();
+      for (int j = lane; j < n; j += 32) {
+        const int v = start[j], sj = fstart[j];
+        const int b = nsum[v], c = ncnt[v];
+        int pos = 0;
+        for (int q = 0; q < c; ++q) {
+          const int x = nl2[b + q];
+          pos += fstart[x] < sj || (fstart[x] == sj && x < j);
+        }
+        nl[v * n + pos] = (uint16_t)j;
+      }
     }
     __syncwarp();
     // ---- trivial concatenation: forward timeline, right after all previous activity
