@@ -53,7 +53,7 @@ __host__ __device__ inline SLayout make_slayout(int n, int NC, int NN) {
   L.start = o;  o = al16(o + 4 * n);
   L.fstart = o; o = al16(o + 4 * n);
   L.dur = o;    o = al16(o + 4 * n);
-  L.life = o;   o = al16(o + 4 * 16 * 6);
+  L.life = o;   o = al16(o + 4 * 16 * 6 + 32 + 64);  // + eval_seam's per-slice scratch
   L.win = o;    o = al16(o + WCAP * 24);
   L.misc = o;   o = al16(o + 8 * 64);
   L.bytes = o;
@@ -140,79 +140,147 @@ __device__ __noinline__ SeamRes eval_seam(int n, const int32_t* T, const uint8_t
   SeamRes R;
   R.E = E;
   R.task_end = tend;
-  // first lifecycle on each slice; reuse (R23 ii)
-  int first[S];
-  unsigned touched = 0;
+  if (NC == 3) {  // the A30 tree (4 slices, 7 nodes): per-slice registers are cheaper
+    // first lifecycle on each slice; reuse (R23 ii)
+    int first[S];
+    unsigned touched = 0;
 #pragma unroll
-  for (int s = 0; s < S; ++s) first[s] = -1;
-  for (int v = 0; v < NN; ++v) {
-    if (ncnt[v] == 0) continue;
-    const uint32_t w = ninfo[v];
+    for (int s = 0; s < S; ++s) first[s] = -1;
+    for (int v = 0; v < NN; ++v) {
+      if (ncnt[v] == 0) continue;
+      const uint32_t w = ninfo[v];
 #pragma unroll
-    for (int s = 0; s < S; ++s)
-      if (s >= nd_lo(w) && s < nd_lo(w) + nd_sz(w)) {
-        touched |= 1u << s;
-        if (first[s] < 0 || life[v * 6] < life[first[s] * 6]) first[s] = v;
-      }
-  }
-  unsigned reuse = 0;
-  for (int v = 0; v < NN; ++v) {
-    if (ncnt[v] == 0) continue;
-    const uint32_t w = ninfo[v];
-    bool ok = true;
-#pragma unroll
-    for (int s = 0; s < S; ++s)
-      if (s >= nd_lo(w) && s < nd_lo(w) + nd_sz(w)) ok = ok && first[s] == v && st->tail_node[s] == v;
-    if (ok) reuse |= 1u << v;
-  }
-  long long bound[S];
-  long long O = max(st->last_off, 0LL);
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    bound[s] = 0;
-    if (first[s] >= 0) {
-      const int v = first[s];
-      bound[s] = ((reuse >> v) & 1) ? st->tail_lt[s] - life[v * 6 + 4] : st->tail[s] - life[v * 6 + 0];
-      O = max(O, bound[s]);
+      for (int s = 0; s < S; ++s)
+        if (s >= nd_lo(w) && s < nd_lo(w) + nd_sz(w)) {
+          touched |= 1u << s;
+          if (first[s] < 0 || life[v * 6] < life[first[s] * 6]) first[s] = v;
+        }
     }
-  }
-  // (iii) sequential reconfiguration against the placed window
-  unsigned skipmask_dev[8];
+    unsigned reuse = 0;
+    for (int v = 0; v < NN; ++v) {
+      if (ncnt[v] == 0) continue;
+      const uint32_t w = ninfo[v];
+      bool ok = true;
 #pragma unroll
-  for (int s = 0; s < S; ++s) skipmask_dev[s] = (first[s] >= 0 && ((reuse >> first[s]) & 1)) ? 1u : 0u;
-  for (;;) {
-    long long push = O;
-    for (int p = lane; p < st->nwin; p += 32) {
-      const WinEv ev = win[p];
-      if (!ev.alive) continue;
-      bool skip = false;
+      for (int s = 0; s < S; ++s)
+        if (s >= nd_lo(w) && s < nd_lo(w) + nd_sz(w)) ok = ok && first[s] == v && st->tail_node[s] == v;
+      if (ok) reuse |= 1u << v;
+    }
+    long long bound[S];
+    long long O = max(st->last_off, 0LL);
 #pragma unroll
-      for (int s = 0; s < S; ++s) skip = skip || (skipmask_dev[s] && st->tail_dev[s] == ev.id);
-      if (skip) continue;
-      for (int v = 0; v < NN; ++v) {
-        if (ncnt[v] == 0) continue;
-        if (!((reuse >> v) & 1)) {
-          const long long a = life[v * 6 + 0], b = life[v * 6 + 1];
+    for (int s = 0; s < S; ++s) {
+      bound[s] = 0;
+      if (first[s] >= 0) {
+        const int v = first[s];
+        bound[s] = ((reuse >> v) & 1) ? st->tail_lt[s] - life[v * 6 + 4] : st->tail[s] - life[v * 6 + 0];
+        O = max(O, bound[s]);
+      }
+    }
+    // (iii) sequential reconfiguration against the placed window
+    unsigned skipmask_dev[8];
+#pragma unroll
+    for (int s = 0; s < S; ++s) skipmask_dev[s] = (first[s] >= 0 && ((reuse >> first[s]) & 1)) ? 1u : 0u;
+    for (;;) {
+      long long push = O;
+      for (int p = lane; p < st->nwin; p += 32) {
+        const WinEv ev = win[p];
+        if (!ev.alive) continue;
+        bool skip = false;
+#pragma unroll
+        for (int s = 0; s < S; ++s) skip = skip || (skipmask_dev[s] && st->tail_dev[s] == ev.id);
+        if (skip) continue;
+        for (int v = 0; v < NN; ++v) {
+          if (ncnt[v] == 0) continue;
+          if (!((reuse >> v) & 1)) {
+            const long long a = life[v * 6 + 0], b = life[v * 6 + 1];
+            if (a + O < ev.e && ev.s < b + O) push = max(push, ev.e - a);
+          }
+          const long long a = life[v * 6 + 2], b = life[v * 6 + 3];
           if (a + O < ev.e && ev.s < b + O) push = max(push, ev.e - a);
         }
-        const long long a = life[v * 6 + 2], b = life[v * 6 + 3];
-        if (a + O < ev.e && ev.s < b + O) push = max(push, ev.e - a);
       }
+      push = warp_max_ll(push);
+      if (push == O) break;
+      O = push;
     }
-    push = warp_max_ll(push);
-    if (push == O) break;
-    O = push;
-  }
-  R.O = O;
-  R.end = O + E;
-  R.reuse = reuse;
-  R.touched = touched;
+    R.O = O;
+    R.end = O + E;
+    R.reuse = reuse;
+    R.touched = touched;
 #pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const long long g = first[s] >= 0 ? O - bound[s] : O + E - st->tail[s];
-    R.gap[s] = max(g, 0LL);
+    for (int s = 0; s < S; ++s) {
+      const long long g = first[s] >= 0 ? O - bound[s] : O + E - st->tail[s];
+      R.gap[s] = max(g, 0LL);
+    }
+    return R;
+  } else {
+    // first lifecycle on each slice (lane s < S), reuse (R23 ii; lane v < NN), offset bound per slice
+    //   -- lane-parallel instead of per-slice register arrays: a much smaller kernel body
+    int* firsts = life + 16 * 6;  // scratch after the lifecycle table (make_slayout reserves it)
+    long long* skipid = (long long*)(firsts + 8);
+    int fs = -1;
+    if (lane < S) {
+      for (int v = 0; v < NN; ++v) {
+        const uint32_t w = ninfo[v];
+        if (ncnt[v] > 0 && lane >= nd_lo(w) && lane < nd_lo(w) + nd_sz(w) && (fs < 0 || life[v * 6] < life[fs * 6]))
+          fs = v;
+      }
+      firsts[lane] = fs;
+    }
+    const unsigned touched = __ballot_sync(FULL, lane < S && fs >= 0);
+    __syncwarp();
+    bool ok = lane < NN && ncnt[lane] > 0;
+    if (ok) {
+      const uint32_t w = ninfo[lane];
+      for (int q = nd_lo(w); q < nd_lo(w) + nd_sz(w); ++q) ok = ok && firsts[q] == lane && st->tail_node[q] == lane;
+    }
+    const unsigned reuse = __ballot_sync(FULL, ok);
+    long long bnd = 0;
+    long long O = max(st->last_off, 0LL);
+    if (lane < S) {
+      if (fs >= 0) {
+        bnd = ((reuse >> fs) & 1) ? st->tail_lt[lane] - life[fs * 6 + 4] : st->tail[lane] - life[fs * 6 + 0];
+        O = max(O, bnd);
+      }
+      // (iii) the destroy event of a reused boundary instance is elided: skip it below
+      skipid[lane] = (fs >= 0 && ((reuse >> fs) & 1)) ? (long long)st->tail_dev[lane] : -2;
+    }
+    O = warp_max_ll(O);
+    __syncwarp();
+    // (iii) sequential reconfiguration against the placed window
+    for (;;) {
+      long long push = O;
+      for (int p = lane; p < st->nwin; p += 32) {
+        const WinEv ev = win[p];
+        if (!ev.alive) continue;
+        bool skip = false;
+#pragma unroll
+        for (int q = 0; q < S; ++q) skip = skip || skipid[q] == (long long)ev.id;
+        if (skip) continue;
+        for (int v = 0; v < NN; ++v) {
+          if (ncnt[v] == 0) continue;
+          if (!((reuse >> v) & 1)) {
+            const long long a = life[v * 6 + 0], b = life[v * 6 + 1];
+            if (a + O < ev.e && ev.s < b + O) push = max(push, ev.e - a);
+          }
+          const long long a = life[v * 6 + 2], b = life[v * 6 + 3];
+          if (a + O < ev.e && ev.s < b + O) push = max(push, ev.e - a);
+        }
+      }
+      push = warp_max_ll(push);
+      if (push == O) break;
+      O = push;
+    }
+    const long long gl = lane < S ? max(fs >= 0 ? O - bnd : O + E - st->tail[lane], 0LL) : 0LL;
+#pragma unroll
+    for (int q = 0; q < S; ++q) R.gap[q] = __shfl_sync(FULL, gl, q);
+    R.O = O;
+    R.end = O + E;
+    R.reuse = reuse;
+    R.touched = touched;
+    return R;
   }
-  return R;
 }
 
 // Move task k from node I to node A and (swap) task j from A to I, keeping lists ordered.
