@@ -13,8 +13,9 @@
 //                 (D = duration at the task's size, < 2^22 on this path), so "ordered by
 //                 T.time, ties -> lower index" is the descending order of entries
 //   off[NN+1] u16 segment offsets of the node lists inside ent
-//   alt[n/32] u32 bit per task: the task runs at the second size its node hosts (A100 {S0..S3}
-//                 running a 3-slice task); such tasks never change node (no other 4-slice node)
+//   bit 9 of an entry is CLEARED for a task that runs at the second size its node hosts (A100
+//                 {S0..S3} running a 3-slice task; for n <= 256 the bit is 1 in every 1023 - task, and
+//                 such tasks never change node or get compared: that node has no same-size alternative)
 // Slice ends live in registers (7 slots, compile-time indexed).
 #pragma once
 #include "far_pipeline.cuh"
@@ -22,18 +23,23 @@
 namespace farb {
 
 struct LRow {
-  int ent, off, alt, bytes;  // byte offsets inside one thread's row
+  int ent, off, bytes;  // byte offsets inside one thread's row
 };
 __host__ __device__ inline LRow make_lrow(int n, int NN) {
   LRow r;
   int o = 0;
   r.ent = o; o += 4 * ((n + 3) & ~3);
-  r.alt = o; o += 4 * ((n + 31) / 32);
   r.off = o; o += 2 * (NN + 1);
   o = (o + 15) & ~15;
   r.bytes = o + 4;  // odd word stride: the 32 rows of a warp start in 32 different banks
   return r;
 }
+
+// entry word of task j with duration d; `second`: the task runs at its node's second size
+__device__ __forceinline__ uint32_t lane_entry(int d, int j, bool second) {
+  return ((uint32_t)d << 10) | ((uint32_t)(1023 - j) & (second ? ~512u : ~0u));
+}
+__device__ __forceinline__ int entry_task(uint32_t x) { return 1023 - (int)((x & 1023u) | 512u); }
 
 template <int NC>
 __device__ __forceinline__ uint32_t cnode(int u) {
@@ -275,12 +281,11 @@ __device__ void refine_lane(uint32_t* ent, uint16_t* off, int (&send)[Tree<NC>::
 }
 
 // Node lists of k* from the phase-2 record (node | size index << 4 | position << 7 per task,
-// node list lengths in ncnt); fills ent/off/alt.
+// node list lengths in ncnt); fills ent/off.
 template <int NC>
 __device__ void lane_lists(int n, const uint32_t* __restrict__ rec, const uint16_t* __restrict__ ncnt,
-                           const int32_t* __restrict__ t, uint32_t* ent, uint16_t* off, uint32_t* alt) {
+                           const int32_t* __restrict__ t, uint32_t* ent, uint16_t* off) {
   constexpr int NN = Tree<NC>::NN;
-  for (int w = 0; w < (n + 31) / 32; ++w) alt[w] = 0;
   int acc = 0;
 #pragma unroll
   for (int v = 0; v < NN; ++v) {
@@ -292,9 +297,7 @@ __device__ void lane_lists(int n, const uint32_t* __restrict__ rec, const uint16
   for (int j = 0; j < n; ++j) {
     const uint32_t r = __ldg(rec + j);
     const int v = (int)(r & 15u), c = (int)((r >> 4) & 7u), pos = (int)(r >> 7);
-    const int d = __ldg(t + j * NC + c);
-    ent[off[v] + pos] = ((uint32_t)d << 10) | (uint32_t)(1023 - j);
-    if (c != nd_c0(cnode<NC>(v))) alt[j >> 5] |= 1u << (j & 31);
+    ent[off[v] + pos] = lane_entry(__ldg(t + j * NC + c), j, c != nd_c0(cnode<NC>(v)));
   }
 }
 
@@ -303,15 +306,14 @@ __device__ void lane_lists(int n, const uint32_t* __restrict__ rec, const uint16
 // 512 B with dependent loads) and its entries are written into lane i's row; the loads of four
 // instances are in flight together.  k0: bit i set if instance i's winner is member 0 (then the
 // durations prep wrote are read coalesced instead of gathered from the runtime table).  The rows'
-// off[] must already hold the node offsets and alt[] be zero.
+// off[] must already hold the node offsets.
 template <int NC>
 __device__ void lane_lists_coop(int n, int64_t base, unsigned am, unsigned k0, const KParams& P, unsigned char* wrows,
                                 int rbytes, const LRow& L, int lane) {
-  auto put = [&](uint32_t* ent, const uint16_t* off, uint32_t* alt, const int32_t* t, int j, uint32_t r, int d) {
+  auto put = [&](uint32_t* ent, const uint16_t* off, const int32_t* t, int j, uint32_t r, int d) {
     const int v = (int)(r & 15u), c = (int)((r >> 4) & 7u), pos = (int)(r >> 7);
     if (d < 0) d = __ldg(t + j * NC + c);
-    ent[off[v] + pos] = ((uint32_t)d << 10) | (uint32_t)(1023 - j);
-    if (c != nd_c0(cnode<NC>(v))) atomicOr(&alt[j >> 5], 1u << (j & 31));
+    ent[off[v] + pos] = lane_entry(d, j, c != nd_c0(cnode<NC>(v)));
   };
   if ((n & 3) == 0) {
     const int n4 = n >> 2;
@@ -345,12 +347,11 @@ __device__ void lane_lists_coop(int n, int64_t base, unsigned am, unsigned k0, c
           unsigned char* row = wrows + (size_t)ids[u] * rbytes;
           uint32_t* ent = (uint32_t*)(row + L.ent);
           const uint16_t* off = (const uint16_t*)(row + L.off);
-          uint32_t* alt = (uint32_t*)(row + L.alt);
           const int32_t* t = P.times + inst * (int64_t)n * NC;
-          put(ent, off, alt, t, 4 * q, x[u].x, (int)dd[u].x);
-          put(ent, off, alt, t, 4 * q + 1, x[u].y, (int)dd[u].y);
-          put(ent, off, alt, t, 4 * q + 2, x[u].z, (int)dd[u].z);
-          put(ent, off, alt, t, 4 * q + 3, x[u].w, (int)dd[u].w);
+          put(ent, off, t, 4 * q, x[u].x, (int)dd[u].x);
+          put(ent, off, t, 4 * q + 1, x[u].y, (int)dd[u].y);
+          put(ent, off, t, 4 * q + 2, x[u].z, (int)dd[u].z);
+          put(ent, off, t, 4 * q + 3, x[u].w, (int)dd[u].w);
         }
       }
     }
@@ -362,8 +363,7 @@ __device__ void lane_lists_coop(int n, int64_t base, unsigned am, unsigned k0, c
       const uint32_t* rec = P.ws_rec + inst * (int64_t)n;
       const int32_t* t = P.times + inst * (int64_t)n * NC;
       for (int j = lane; j < n; j += 32)
-        put((uint32_t*)(row + L.ent), (const uint16_t*)(row + L.off), (uint32_t*)(row + L.alt), t, j, __ldcs(rec + j),
-            -1);
+        put((uint32_t*)(row + L.ent), (const uint16_t*)(row + L.off), t, j, __ldcs(rec + j), -1);
     }
   }
   __syncwarp();
@@ -372,7 +372,7 @@ __device__ void lane_lists_coop(int n, int64_t base, unsigned am, unsigned k0, c
 // Node-level replay (the frontier in registers of this thread); writes the schedule when
 // `out` is not null; returns the makespan.
 template <int NC>
-__device__ int lane_replay(const uint32_t* ent, const uint16_t* off, const uint32_t* alt, const int* cr,
+__device__ int lane_replay(const uint32_t* ent, const uint16_t* off, const int* cr,
                            const int* de, far_task_slot* out) {
   constexpr int S = Tree<NC>::S;
   Frontier<S> F;
@@ -388,14 +388,14 @@ __device__ int lane_replay(const uint32_t* ent, const uint16_t* off, const uint3
       rec = max(rec, be) + cr[nd_szi(w)];
       int acc = rec;
       if (out) {
-        // slot word node | size << 8 | start << 32; only the two-size node reads the alt bits
+        // slot word node | size << 8 | start << 32; only the two-size node has second-size entries
         const unsigned lo0 = (unsigned)v | ((unsigned)size_of<NC>(nd_c0(w)) << 8);
         const bool two = nd_c1(w) != NONE;
         const unsigned lo1 = two ? (unsigned)v | ((unsigned)size_of<NC>(nd_c1(w)) << 8) : lo0;
         for (int q = b; q < e; ++q) {
           const uint32_t x = ent[q];
-          const int j = 1023 - (int)(x & 1023u);
-          const unsigned lo = (two && ((alt[j >> 5] >> (j & 31)) & 1)) ? lo1 : lo0;
+          const int j = entry_task(x);
+          const unsigned lo = (two && !(x & 512u)) ? lo1 : lo0;
           *(unsigned long long*)(out + j) = (unsigned long long)lo | ((unsigned long long)(unsigned)acc << 32);
           acc += (int)(x >> 10);
         }
@@ -428,7 +428,6 @@ __global__ void __launch_bounds__(128, 3) far_finish_lane_kernel(KParams P) {
   unsigned char* row = dsm + (size_t)threadIdx.x * L.bytes;
   uint32_t* ent = (uint32_t*)(row + L.ent);
   uint16_t* off = (uint16_t*)(row + L.off);
-  uint32_t* alt = (uint32_t*)(row + L.alt);
   const bool want_sched = P.sched != nullptr && !(P.flags & FAR_NO_SCHEDULE);
   const bool refine = !(P.flags & FAR_NO_REFINE);
   const bool need_replay = refine || want_sched;
@@ -441,7 +440,6 @@ __global__ void __launch_bounds__(128, 3) far_finish_lane_kernel(KParams P) {
     // error / empty (K1 wrote the outputs) / deferred to the overflow pass: nothing to finish
     const bool active = inst < P.I && !P.ws_meta[inst * 16 + WS_FLAG];
     if (active) {
-      for (int w = 0; w < (n + 31) / 32; ++w) alt[w] = 0;
       int acc = 0;
       const uint16_t* nc = P.ws_ncnt + inst * 16;
 #pragma unroll
@@ -467,7 +465,7 @@ __global__ void __launch_bounds__(128, 3) far_finish_lane_kernel(KParams P) {
     far_task_slot* out = want_sched ? P.sched + inst * (int64_t)n : nullptr;
     int msF = ms2;
     for (int pass = 0; pass < 2; ++pass) {
-      if (pass) lane_lists<NC>(n, rec, P.ws_ncnt + inst * 16, t, ent, off, alt);
+      if (pass) lane_lists<NC>(n, rec, P.ws_ncnt + inst * 16, t, ent, off);
       const bool ref = refine && pass == 0;
       if (ref) {
         int send[S];
@@ -479,7 +477,7 @@ __global__ void __launch_bounds__(128, 3) far_finish_lane_kernel(KParams P) {
         R.moves = mv; R.swaps = sw; R.iterations = it; R.evals = ev;
       }
       if (!need_replay) break;
-      const int msR = lane_replay<NC>(ent, off, alt, s_cr, s_de, out);
+      const int msR = lane_replay<NC>(ent, off, s_cr, s_de, out);
       if (ref && !(P.flags & FAR_NO_GUARD) && msR > ms2) {
         R.reverted = 1;  // keep-best guard: return the phase-2 schedule (replayed in pass 1)
         if (!want_sched) break;
