@@ -9,6 +9,6 @@ python bench.py > $out/bench.log 2>&1
 grep '^{' $out/bench.log | tail -1 > $out/bench.json
 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $out/launches.csv \
   python bench.py --steps 2 --warmup 1 --profile-run --no-secondary > $out/launches.log 2>&1
-ncu --set full --clock-control none --import-source on -s 6 -c 6 -o $out/chain \
+ncu --set full --clock-control none --import-source on -s 7 -c 7 -o $out/chain \
   python bench.py --instances 200000 --steps 1 --warmup 1 --profile-run --no-secondary > $out/chain.log 2>&1
 ls -la $out

@@ -24,10 +24,14 @@ tj["source"] = (f"ncu --set full capture of one far_solve_many chain, 200k M5 in
 json.dump(tj, open(os.path.join(P, "ncu_traffic_M5.json"), "w"), indent=1)
 # hardware view for bench.py's roofline.stages_hw: issued lane-ops (warp instructions x active lanes
 # per instruction) per instance of each kernel
-issue = {"workload": tj["workload"], "source": tj["source"],
-         "lane_ops_per_instance": {k["stage"]: k["warp_inst_per_instance"] * k["thread_inst_per_inst"]
-                                   for k in tj["kernels"]},
-         "warp_inst_per_instance": {k["stage"]: k["warp_inst_per_instance"] for k in tj["kernels"]}}
+# (the bench's "prep" stage spans both prep launches: the monotone pass and the general pass)
+lane_ops, warp_inst = {}, {}
+for k in tj["kernels"]:
+    st = "prep" if k["stage"] == "prep_general" else k["stage"]
+    lane_ops[st] = lane_ops.get(st, 0.0) + k["warp_inst_per_instance"] * k["thread_inst_per_inst"]
+    warp_inst[st] = warp_inst.get(st, 0.0) + k["warp_inst_per_instance"]
+issue = {"workload": tj["workload"], "source": tj["source"], "lane_ops_per_instance": lane_ops,
+         "warp_inst_per_instance": warp_inst}
 json.dump(issue, open(os.path.join(P, "ncu_issue_M5.json"), "w"), indent=1)
 
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -48,7 +52,7 @@ keys = ["Kernel Name", "Grid Size", "Block Size", "gpu__time_duration.sum", "lau
         "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_branch_resolving_per_issue_active.ratio"]
 out = ["# ncu --set full --clock-control none, one far_solve_many chain on 200k M5 instances (A100, n=128, seed 5)",
-       "# columns: one per kernel in launch order (prep, member0, members, winner, finish, overflow)"]
+       "# columns: one per kernel in launch order (prep, prep_general, member0, members, winner, finish, overflow)"]
 for k in keys:
     if k in hdr:
         i = hdr.index(k)
@@ -56,8 +60,8 @@ for k in keys:
 open(os.path.join(P, f"{rnd}_ncu_final_raw.txt"), "w").write("\n".join(out) + "\n")
 
 top = []
-for skip, name in ((0, "far_prep_kernel<5> (prep)"), (1, "far_member0_kernel<5> (member0)"),
-                   (2, "far_members_kernel<5> (members)"), (4, "far_finish_lane_kernel<5> (finish)")):
+for skip, name in ((0, "far_prep_kernel<5, true> (prep)"), (2, "far_member0_kernel<5> (member0)"),
+                   (3, "far_members_kernel<5> (members)"), (5, "far_finish_lane_kernel<5> (finish)")):
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
                           "--launch-skip", str(skip), "--launch-count", "1"], capture_output=True, text=True).stdout
     tmp = os.path.join("/tmp", f"src_{skip}.csv")
@@ -73,7 +77,7 @@ b = json.load(open(bench))
 st = b["roofline"]["stages_ms_per_step"]
 for k in tj["kernels"]:
     nm = k["name"].replace("void ", "").replace("(KParams)", "").replace("(PParams)", "")
-    print(f"| {k['stage']} | `{nm}` | {st.get(k['stage'], 0):.2f} | {k['ms_cold_serialised']:.3f} | {k['registers']} | "
+    print(f"| {k['stage']} | `{nm}` | {st.get(k['stage'], 0) if k['stage'] != 'prep_general' else 0:.2f} | {k['ms_cold_serialised']:.3f} | {k['registers']} | "
           f"{k['warps_active_pct']:.0f} % | {k['issue_active_pct']:.0f} % | {k['thread_inst_per_inst']:.1f} | "
           f"{k['dram_read_bytes_per_instance']:.0f} / {k['dram_write_bytes_per_instance']:.0f} |")
 print(f"total DRAM per instance: {tj['dram_read_bytes_per_instance']:.0f} + {tj['dram_write_bytes_per_instance']:.0f} B;"

@@ -12,7 +12,7 @@ raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_outpu
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units = rows[0], rows[1]
 col = {h: i for i, h in enumerate(hdr)}
-stages = ["prep", "member0", "members", "winner", "finish", "overflow"]
+stages = ["prep", "prep_general", "member0", "members", "winner", "finish", "overflow"]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 out = {"workload": workload, "source": rep, "instances_per_launch": inst, "kernels": []}
 tot_r = tot_w = tot_t = 0.0
