@@ -49,42 +49,44 @@ __host__ __device__ inline PLayout make_playout(int n, int NC, int kcap) {
   return L;
 }
 
-// Ascending bitonic sort of 256 keys, 8 per lane, element i = q * 32 + lane in v[q].  Every
+// Ascending bitonic sort of 256 keys, 8 per lane, element i = lane * 8 + q in v[q] (blocked: the
+// 21 stages whose partners differ only in q are register pairs, the other 15 shuffles).  Every
 // comparator keeps the minimum at the lower index (block step: i <-> i ^ (k - 1), then
-// half-cleaners i <-> i ^ j); partners within a register column are shuffles, across columns
-// register pairs.
+// half-cleaners i <-> i ^ j), so no stage needs a direction.
 __device__ __forceinline__ void warp_sort256(unsigned (&v)[8], int lane) {
 #pragma unroll
   for (int k = 2; k <= 256; k <<= 1) {
-    if (k <= 32) {
-      const bool lower = (lane & (k >> 1)) == 0;
+    if (k <= 8) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const unsigned o = __shfl_xor_sync(FULL, v[q], k - 1);
-        v[q] = lower ? min(v[q], o) : max(v[q], o);
-      }
+      for (int q = 0; q < 8; ++q)
+        if (q < (q ^ (k - 1))) {
+          const unsigned x = v[q], y = v[q ^ (k - 1)];
+          v[q] = min(x, y);
+          v[q ^ (k - 1)] = max(x, y);
+        }
     } else {
+      const bool lower = (lane & (k >> 4)) == 0;
       unsigned o[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) o[q] = __shfl_xor_sync(FULL, v[q ^ ((k - 1) >> 5)], 31);
+      for (int q = 0; q < 8; ++q) o[q] = __shfl_xor_sync(FULL, v[q ^ 7], (k - 1) >> 3);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = (q & (k >> 6)) == 0 ? min(v[q], o[q]) : max(v[q], o[q]);
+      for (int q = 0; q < 8; ++q) v[q] = lower ? min(v[q], o[q]) : max(v[q], o[q]);
     }
 #pragma unroll
     for (int j = k >> 2; j > 0; j >>= 1) {
-      if (j >= 32) {
+      if (j < 8) {
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          if ((q & (j >> 5)) == 0) {
-            const unsigned x = v[q], y = v[q | (j >> 5)];
+          if ((q & j) == 0) {
+            const unsigned x = v[q], y = v[q | j];
             v[q] = min(x, y);
-            v[q | (j >> 5)] = max(x, y);
+            v[q | j] = max(x, y);
           }
       } else {
-        const bool lower = (lane & j) == 0;
+        const bool lower = (lane & (j >> 3)) == 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const unsigned o = __shfl_xor_sync(FULL, v[q], j);
+          const unsigned o = __shfl_xor_sync(FULL, v[q], j >> 3);
           v[q] = lower ? min(v[q], o) : max(v[q], o);
         }
       }
@@ -366,8 +368,8 @@ __device__ __forceinline__ void prep_rest(const KParams& P, int64_t inst, unsign
       }
     }
     warp_sort256(v, lane);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) kk[q * 32 + lane] = v[q];
+    *(uint4*)(kk + lane * 8) = make_uint4(v[0], v[1], v[2], v[3]);  // sorted order, blocked
+    *(uint4*)(kk + lane * 8 + 4) = make_uint4(v[4], v[5], v[6], v[7]);
   }
   __syncwarp();
   // ---- outputs: ws_ent[i] = {t | task << 22, lo | hi << 16} (member interval of the entry), the a^1
