@@ -425,7 +425,9 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     const int tb = 128;
     const size_t psm = (size_t)4 * NC * tb + (size_t)2 * NN * tb;
     const int g_inst = (int)std::min<int64_t>((P.I + tb - 1) / tb, (int64_t)ctx->sms * 16);
-    const int g_items = ctx->sms * 16;
+    int items_per_sm = 12;  // blocks of 128 per SM for K3: 12 measured 1.68 ms per 1M M5, 16: 1.71, 14: 1.85
+    if (const char* e = getenv("FAR_DEBUG_MEMBERS_BPS")) items_per_sm = std::max(1, std::min(16, atoi(e)));  // experiments
+    const int g_items = ctx->sms * items_per_sm;
     {  // K2: per-thread shared-memory copy of member 0's lists -> block size by footprint
       const size_t per_thread = (size_t)4 * NC + 2 * NN + 4 * (size_t)(n4 + 1);
       const int tb0 = (int)std::min<size_t>(128, (size_t)ctx->smem_max / per_thread / 32 * 32);

@@ -53,18 +53,17 @@ __device__ int sim_member(const int2* __restrict__ ent, const int* loff, unsigne
     int bs, be;
     F.pop(bs, be);
     const int v = F.node(bs);
-    const uint32_t w = ninfo[v];
-    int c = nd_c0(w);
+    int c = node_c0<NC>(v);
     uint32_t sv = st[c * bdim];
     if (!(sv >> 16)) {
-      c = nd_c1(w);
+      c = node_c1<NC>(v);
       sv = 0;
       if (c != NONE) sv = st[c * bdim];
     }
     ++pops;
     if (sv >> 16) {
       if (!((F.has >> bs) & 1)) {
-        rec_end = max(rec_end, be) + cr[nd_szi(w)];
+        rec_end = max(rec_end, be) + cr[node_szi<NC>(v)];
         be = rec_end;
         F.has |= 1u << bs;
       }
@@ -88,6 +87,7 @@ __device__ int sim_member(const int2* __restrict__ ent, const int* loff, unsigne
       --total;
       F.set(bs, be);
     } else {
+      const uint32_t w = ninfo[v];
       if ((F.has >> bs) & 1) rec_end = max(rec_end, be) + de[nd_szi(w)];
       if (!F.split(bs, be, w)) {
 #pragma unroll
@@ -136,18 +136,17 @@ __device__ int sim_member0(const uint32_t* row, unsigned long long cp, const uin
     int bs, be;
     F.pop(bs, be);
     const int v = F.node(bs);
-    const uint32_t w = ninfo[v];
-    int c = nd_c0(w);
+    int c = node_c0<NC>(v);
     uint32_t sv = st[c * bdim];
     if (!(sv >> 16)) {
-      c = nd_c1(w);
+      c = node_c1<NC>(v);
       sv = 0;
       if (c != NONE) sv = st[c * bdim];
     }
     ++pops;
     if (sv >> 16) {
       if (!((F.has >> bs) & 1)) {
-        rec_end = max(rec_end, be) + cr[nd_szi(w)];
+        rec_end = max(rec_end, be) + cr[node_szi<NC>(v)];
         be = rec_end;
         F.has |= 1u << bs;
       }
@@ -163,6 +162,7 @@ __device__ int sim_member0(const uint32_t* row, unsigned long long cp, const uin
       --total;
       F.set(bs, be);
     } else {
+      const uint32_t w = ninfo[v];
       if ((F.has >> bs) & 1) rec_end = max(rec_end, be) + de[nd_szi(w)];
       if (!F.split(bs, be, w)) {
 #pragma unroll
@@ -233,23 +233,49 @@ __global__ void __launch_bounds__(128) far_member0_kernel(PParams P) {
   uint16_t* npos = (uint16_t*)(dsm + 4 * NC * bdim) + tid;
   // this thread's copy of member 0's lists (odd row stride n4 + 1 words: the rows of a warp start
   // in 32 different banks)
-  uint32_t* row = (uint32_t*)(dsm + (4 * NC + 2 * NN) * bdim) + (size_t)tid * (P.ws_n4 + 1);
+  const int nw = P.ws_n4, rs = nw + 1, lane = tid & 31;
+  uint32_t* wrows = (uint32_t*)(dsm + (4 * NC + 2 * NN) * bdim) + (size_t)(tid & ~31) * rs;
+  uint32_t* row = wrows + (size_t)lane * rs;
   const bool exhaustive = (P.flags & FAR_EXHAUSTIVE) != 0;
-  for (int64_t i = (int64_t)blockIdx.x * bdim + tid; i < P.I; i += (int64_t)gridDim.x * bdim) {
+  // the lanes of a warp hold consecutive instances and step together (the list staging is
+  // warp-cooperative); every lane runs the loop until the warp's first instance passes I
+  for (int64_t i = (int64_t)blockIdx.x * bdim + tid; i - lane < P.I; i += (int64_t)gridDim.x * bdim) {
+    const bool active = i < P.I && !P.ws_meta[i * 16 + WS_FLAG];
+    __syncwarp();  // every lane is done with its row (previous instance)
+    {  // the warp copies its instances' lists: coalesced 128-B loads, eight instances' loads in
+       // flight per lane (one exposed latency per eight instances), conflict-free stores into the rows
+      const uint32_t* src = P.ws_m0 + (i - lane) * (int64_t)nw;
+      for (unsigned am = __ballot_sync(FULL, active); am;) {
+        int ids[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          ids[u] = am ? __ffs(am) - 1 : -1;
+          am &= am - 1;
+        }
+        for (int w0 = 0; w0 < nw; w0 += 128) {
+          uint32_t x[8][4];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const int w = w0 + 32 * v + lane;
+              x[u][v] = (ids[u] >= 0 && w < nw) ? __ldcs(src + (int64_t)ids[u] * nw + w) : 0u;
+            }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const int w = w0 + 32 * v + lane;
+              if (ids[u] >= 0 && w < nw) wrows[(size_t)ids[u] * rs + w] = x[u][v];
+            }
+        }
+      }
+      __syncwarp();
+    }
+    if (!active) continue;
     const int* meta = P.ws_meta + i * 16;
-    if (meta[WS_FLAG]) continue;
     const int K = meta[WS_K];
     const int* lb = P.ws_lb + i * (int64_t)P.ws_kcap;
-    {  // independent 16 B loads (many in flight), then every placement reads shared memory
-      const int4* src = (const int4*)(P.ws_m0 + i * (int64_t)P.ws_n4);
-      for (int q = 0; q < (P.ws_n4 >> 2); ++q) {
-        const int4 x = __ldcs(src + q);
-        row[4 * q] = (uint32_t)x.x;
-        row[4 * q + 1] = (uint32_t)x.y;
-        row[4 * q + 2] = (uint32_t)x.z;
-        row[4 * q + 3] = (uint32_t)x.w;
-      }
-    }
     int pops = 0;
     const int ms0 = sim_member0<NC>(row, P.ws_cnt[i * (int64_t)P.ws_kcap], sm.ninfo, sm.cr, sm.de, st, npos, bdim,
                                     P.ws_rec + i * (int64_t)P.n, P.ws_sl + i * 8, pops);

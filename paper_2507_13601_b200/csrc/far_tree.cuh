@@ -99,6 +99,26 @@ template <int NC> __host__ __device__ constexpr uint32_t tree_node(int u) {
 template <int NC> __host__ __device__ constexpr int tree_leaf(int s) {
   return NC == 3 ? 3 + s : (s < 6 ? 7 + s : 6);
 }
+// One 3-bit field (at bit `shift` of the node word) of every node, packed into a 64-bit word
+// (13 x 3 = 39 bits): looking a field up by a dynamic node id is a funnel shift instead of a
+// dependent shared-memory load on the Alg. 1 event chain.
+template <int NC> __host__ __device__ constexpr unsigned long long node_field_tab(int shift) {
+  unsigned long long t = 0;
+  for (int v = 0; v < (NC == 3 ? 7 : 13); ++v) t |= (unsigned long long)((tree_node<NC>(v) >> shift) & 7u) << (3 * v);
+  return t;
+}
+template <int NC> __device__ __forceinline__ int node_c0(int v) {
+  constexpr unsigned long long T = node_field_tab<NC>(0);
+  return (int)((T >> (3 * v)) & 7u);
+}
+template <int NC> __device__ __forceinline__ int node_c1(int v) {
+  constexpr unsigned long long T = node_field_tab<NC>(3);
+  return (int)((T >> (3 * v)) & 7u);
+}
+template <int NC> __device__ __forceinline__ int node_szi(int v) {
+  constexpr unsigned long long T = node_field_tab<NC>(6);
+  return (int)((T >> (3 * v)) & 7u);
+}
 static_assert(tree_node<3>(6) == Tree<3>::node[6] && tree_node<3>(3) == Tree<3>::node[3], "A30 node table");
 static_assert(tree_node<5>(12) == Tree<5>::node[12] && tree_node<5>(9) == Tree<5>::node[9] &&
                   tree_node<5>(6) == Tree<5>::node[6] && tree_node<5>(2) == Tree<5>::node[2],
