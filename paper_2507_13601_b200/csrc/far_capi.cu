@@ -278,6 +278,7 @@ static far_status launch_prep(far_ctx* ctx, KParams& P, cudaStream_t stream, uns
     far_status st = pick_shape(ctx, fn, L.bytes, warps, per_sm);
     if (st) return st;
     const size_t smem = (size_t)warps * L.bytes;
+    if (const char* e = getenv("FAR_DEBUG_PREP_BPS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));  // experiments
     int64_t units = pass == 0 ? P.I : std::min<int64_t>(P.I, (int64_t)ctx->sms * per_sm * warps);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((units + warps - 1) / warps, (int64_t)ctx->sms * per_sm));
     KParams Q = P;
@@ -430,12 +431,19 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     const int g_items = ctx->sms * items_per_sm;
     {  // K2: per-thread shared-memory copy of member 0's lists -> block size by footprint
       const size_t per_thread = (size_t)4 * NC + 2 * NN + 4 * (size_t)(n4 + 1);
-      const int tb0 = (int)std::min<size_t>(128, (size_t)ctx->smem_max / per_thread / 32 * 32);
+      int tbmax = 128;
+      if (const char* e = getenv("FAR_DEBUG_M0_TB")) tbmax = std::max(32, std::min(128, atoi(e)));  // experiments
+      const int tb0 = (int)std::min<size_t>(tbmax, (size_t)ctx->smem_max / per_thread / 32 * 32);
       if (tb0 < 32) return fail(ctx, FAR_E_TOO_LARGE, "member-0 lists do not fit in shared memory");
       const size_t sm0 = per_thread * tb0;
       const void* f0 = a30 ? (const void*)far_member0_kernel<3> : (const void*)far_member0_kernel<5>;
       int per_sm = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, tb0, sm0));
+      // n > 64: at most 8 warps per SM -- measured on M5 (1M x n = 128) 1.33 ms at 8 warps (2 x 128,
+      // 4 x 64 or 8 x 32 threads) against 1.48 at the 12 the shared memory allows, 1.48-1.51 at 9-10,
+      // 1.53 at 6; M3 (100k x n = 32, short rows, one pass over the instances) keeps full occupancy
+      if (P.n > 64) per_sm = std::min(per_sm, std::max(1, 256 / tb0));
+      if (const char* e = getenv("FAR_DEBUG_M0_BPS")) per_sm = std::min(per_sm, atoi(e));  // experiments
       const int g0 = (int)std::max<int64_t>(1, std::min<int64_t>((P.I + tb0 - 1) / tb0, (int64_t)ctx->sms * std::max(1, per_sm)));
       if (a30) far_member0_kernel<3><<<g0, tb0, sm0, stream>>>(Q);
       else far_member0_kernel<5><<<g0, tb0, sm0, stream>>>(Q);
@@ -455,12 +463,15 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     //      per instance
     P.counter = ctx->d_counter + slot + 5;
     const LRow LR = make_lrow(P.n, NN);
-    const int tbl = (int)std::min<int64_t>(128, (int64_t)ctx->smem_max / LR.bytes / 32 * 32);
+    int tblmax = 128;
+    if (const char* e = getenv("FAR_DEBUG_FIN_TB")) tblmax = std::max(32, std::min(128, atoi(e)));  // experiments
+    const int tbl = (int)std::min<int64_t>(tblmax, (int64_t)ctx->smem_max / LR.bytes / 32 * 32);
     if (P.n <= 256 && tbl >= 32 && !(P.flags & FAR_BEST_IMPROVEMENT) && !getenv("FAR_DEBUG_WARP_FINISH")) {
       const void* lfn = a30 ? (const void*)far_finish_lane_kernel<3> : (const void*)far_finish_lane_kernel<5>;
       const size_t lsm = (size_t)tbl * LR.bytes;
       int per_sm = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lfn, tbl, lsm));
+      if (const char* e = getenv("FAR_DEBUG_FIN_BPS")) per_sm = std::min(per_sm, atoi(e));  // experiments
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((P.I + tbl - 1) / tbl, (int64_t)ctx->sms * std::max(1, per_sm)));
       if (a30) far_finish_lane_kernel<3><<<grid, tbl, lsm, stream>>>(P);
       else far_finish_lane_kernel<5><<<grid, tbl, lsm, stream>>>(P);
