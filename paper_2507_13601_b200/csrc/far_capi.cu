@@ -425,7 +425,9 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     Q.counter = ctx->d_counter + slot + 4;
     const int tb = 128;
     const size_t psm = (size_t)4 * NC * tb + (size_t)2 * NN * tb;
-    const int g_inst = (int)std::min<int64_t>((P.I + tb - 1) / tb, (int64_t)ctx->sms * 16);
+    int winner_per_sm = 16;
+    if (const char* e = getenv("FAR_DEBUG_WINNER_BPS")) winner_per_sm = std::max(1, atoi(e));  // experiments
+    const int g_inst = (int)std::min<int64_t>((P.I + tb - 1) / tb, (int64_t)ctx->sms * winner_per_sm);
     int items_per_sm = 12;  // blocks of 128 per SM for K3: 12 measured 1.68 ms per 1M M5, 16: 1.71, 14: 1.85
     if (const char* e = getenv("FAR_DEBUG_MEMBERS_BPS")) items_per_sm = std::max(1, std::min(16, atoi(e)));  // experiments
     const int g_items = ctx->sms * items_per_sm;

@@ -433,10 +433,19 @@ __global__ void __launch_bounds__(128, 3) far_finish_lane_kernel(KParams P) {
   const bool need_replay = refine || want_sched;
   const int lane = threadIdx.x & 31;
   unsigned char* wrows = dsm + (size_t)(threadIdx.x & ~31) * L.bytes;
-  // the lanes of a warp hold consecutive instances and step together (the list staging is
-  // warp-cooperative); every lane runs the loop until the warp's first instance passes I
-  for (int64_t inst = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; inst - lane < P.I;
-       inst += (int64_t)gridDim.x * blockDim.x) {
+  // the lanes of a warp hold 32 consecutive instances and step together (the list staging is
+  // warp-cooperative); batches of 32 are claimed from a counter, one ahead, so that the warps
+  // finish together although their batches' refine work differs
+  // (a grid that covers every instance in one pass takes its batch by position: no atomics)
+  const bool one_pass = (int64_t)gridDim.x * blockDim.x >= P.I;
+  unsigned long long nb = (unsigned long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+  if (!one_pass && lane == 0) nb = atomicAdd(P.counter, 32ull);
+  for (;;) {
+    const int64_t base = (int64_t)__shfl_sync(FULL, nb, 0);
+    if (base >= P.I) break;
+    if (one_pass) nb = (unsigned long long)P.I;
+    else if (lane == 0) nb = atomicAdd(P.counter, 32ull);
+    const int64_t inst = base + lane;
     // error / empty (K1 wrote the outputs) / deferred to the overflow pass: nothing to finish
     const bool active = inst < P.I && !P.ws_meta[inst * 16 + WS_FLAG];
     if (active) {

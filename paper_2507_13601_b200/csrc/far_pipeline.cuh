@@ -202,7 +202,7 @@ struct PParams {
   uint16_t* ws_ncnt;            // [I][16] node list lengths of the recorded member
   int2* items;                  // (instance, member) work items of K3
   unsigned long long* nitems;   // item counter
-  unsigned long long* counter;  // K3 item scheduler
+  unsigned long long* counter;  // K2 batch counter
 };
 
 template <int NC> struct PipeSmem {
@@ -237,9 +237,18 @@ __global__ void __launch_bounds__(128) far_member0_kernel(PParams P) {
   uint32_t* wrows = (uint32_t*)(dsm + (4 * NC + 2 * NN) * bdim) + (size_t)(tid & ~31) * rs;
   uint32_t* row = wrows + (size_t)lane * rs;
   const bool exhaustive = (P.flags & FAR_EXHAUSTIVE) != 0;
-  // the lanes of a warp hold consecutive instances and step together (the list staging is
-  // warp-cooperative); every lane runs the loop until the warp's first instance passes I
-  for (int64_t i = (int64_t)blockIdx.x * bdim + tid; i - lane < P.I; i += (int64_t)gridDim.x * bdim) {
+  // the lanes of a warp hold 32 consecutive instances and step together (the list staging is
+  // warp-cooperative); batches of 32 are claimed from a counter, one ahead
+  // (a grid that covers every instance in one pass takes its batch by position: no atomics)
+  const bool one_pass = (int64_t)gridDim.x * blockDim.x >= P.I;
+  unsigned long long nb = (unsigned long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+  if (!one_pass && lane == 0) nb = atomicAdd(P.counter, 32ull);
+  for (;;) {
+    const int64_t base = (int64_t)__shfl_sync(FULL, nb, 0);
+    if (base >= P.I) break;
+    if (one_pass) nb = (unsigned long long)P.I;
+    else if (lane == 0) nb = atomicAdd(P.counter, 32ull);
+    const int64_t i = base + lane;
     const bool active = i < P.I && !P.ws_meta[i * 16 + WS_FLAG];
     __syncwarp();  // every lane is done with its row (previous instance)
     {  // the warp copies its instances' lists: coalesced 128-B loads, eight instances' loads in
