@@ -21,7 +21,7 @@
 using namespace farb;
 
 namespace {
-constexpr int RING = 256;
+constexpr int NREC = 32, CPL = 16, RING = NREC * CPL;  // launch records; counters per launch
 }  // namespace
 
 struct far_ctx {
@@ -42,7 +42,7 @@ struct far_ctx {
   // cross-stream ordering of the context's device workspaces: every launch records an event on
   // its stream; a launch that reuses a workspace last used on ANOTHER stream waits on that event
   struct LaunchRec { cudaEvent_t ev; cudaStream_t stream; bool valid; };
-  LaunchRec recs[RING / 8] = {};
+  LaunchRec recs[NREC] = {};
   int64_t pws_last[2] = {-1, -1}, ovf_last[4] = {-1, -1, -1, -1}, cbuf_last = -1;
   // staging for host-memory calls
   char* d_buf = nullptr;   // staging of the synchronous host-memory calls (ctx streams)
@@ -163,12 +163,12 @@ static far_status ensure_buf(far_ctx* ctx, size_t bytes) { return grow(ctx, &ctx
 // q's counter slot), so waiting on the newer event is still sufficient.
 static far_status order_after(far_ctx* ctx, int64_t q, cudaStream_t stream) {
   if (q < 0) return FAR_OK;
-  far_ctx::LaunchRec& r = ctx->recs[q % (RING / 8)];
+  far_ctx::LaunchRec& r = ctx->recs[q % NREC];
   if (r.valid && r.stream != stream) CK(cudaStreamWaitEvent(stream, r.ev, 0));
   return FAR_OK;
 }
 static far_status record_launch(far_ctx* ctx, int64_t id, cudaStream_t stream) {
-  far_ctx::LaunchRec& r = ctx->recs[id % (RING / 8)];
+  far_ctx::LaunchRec& r = ctx->recs[id % NREC];
   CK(cudaEventRecord(r.ev, stream));
   r.stream = stream;
   r.valid = true;
@@ -333,15 +333,15 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
                     !(P.flags & FAR_SWITCH_COST) && (P.I >= 256 || getenv("FAR_PIPELINE_ALWAYS"));
   const bool need_ovf = P.mode == MODE_SOLVE && (kfast < kmax || pipe);
   const int64_t lid = ctx->launch_id++;
-  const int slot = (int)(lid % (RING / 8)) * 8;
+  const int slot = (int)(lid % NREC) * CPL;
   far_status st;
-  if ((st = order_after(ctx, lid - RING / 8, stream))) return st;  // previous user of the counter slot
-  CK(cudaMemsetAsync(ctx->d_counter + slot, 0, 8 * sizeof(unsigned long long), stream));
+  if ((st = order_after(ctx, lid - NREC, stream))) return st;  // previous user of the counter slot
+  CK(cudaMemsetAsync(ctx->d_counter + slot, 0, CPL * sizeof(unsigned long long), stream));
   if (!P.errflag) P.errflag = ctx->d_errflag;
   P.ovf_count = ctx->d_counter + slot + 2;
   P.ovf = nullptr;
   if (need_ovf) {
-    const int r = (slot / 8) & 3;
+    const int r = (slot / CPL) & 3;
     if ((st = order_after(ctx, ctx->ovf_last[r], stream))) return st;
     ctx->ovf_last[r] = lid;
     const size_t words = (size_t)((P.I + 31) / 32);
@@ -423,6 +423,7 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     Q.items = (int2*)(w + o_items);
     Q.nitems = ctx->d_counter + slot + 3;
     Q.counter = ctx->d_counter + slot + 4;
+    Q.counter2 = ctx->d_counter + slot + 8;
     const int tb = 128;
     const size_t psm = (size_t)4 * NC * tb + (size_t)2 * NN * tb;
     int winner_per_sm = 16;
@@ -918,7 +919,7 @@ extern "C" far_status far_concat_streams(far_ctx* ctx, const int32_t* d_times, i
   if ((st = t_mark(ctx, tset, stream, FAR_STAGE_STREAM))) return st;
   // the fold is the last user of d_cbuf: order the next concat after it (same event ring)
   ctx->cbuf_last = ctx->launch_id++;
-  if ((st = order_after(ctx, ctx->cbuf_last - RING / 8, stream))) return st;
+  if ((st = order_after(ctx, ctx->cbuf_last - NREC, stream))) return st;
   return record_launch(ctx, ctx->cbuf_last, stream);
 }
 
@@ -932,8 +933,8 @@ static far_status launch_check(far_ctx* ctx, CParams& Q, int64_t I, int n, bool 
   far_status st = pick_shape(ctx, fn, bytes, warps, per_sm);
   if (st) return st;
   const int64_t lid = ctx->launch_id++;
-  const int slot = (int)(lid % (RING / 8)) * 8;
-  if ((st = order_after(ctx, lid - RING / 8, stream))) return st;
+  const int slot = (int)(lid % NREC) * CPL;
+  if ((st = order_after(ctx, lid - NREC, stream))) return st;
   CK(cudaMemsetAsync(ctx->d_counter + slot, 0, sizeof(unsigned long long), stream));
   Q.counter = ctx->d_counter + slot;
   far_ctx::EvSet* tset = nullptr;

@@ -203,6 +203,7 @@ struct PParams {
   int2* items;                  // (instance, member) work items of K3
   unsigned long long* nitems;   // item counter
   unsigned long long* counter;  // K2 batch counter
+  unsigned long long* counter2; // K3 item batch counter
 };
 
 template <int NC> struct PipeSmem {
@@ -328,8 +329,17 @@ __global__ void __launch_bounds__(128) far_members_kernel(PParams P) {
   uint32_t* st = (uint32_t*)dsm + tid;
   const bool exhaustive = (P.flags & FAR_EXHAUSTIVE) != 0;
   const unsigned long long nit = *(volatile unsigned long long*)P.nitems;
-  for (unsigned long long it = (unsigned long long)blockIdx.x * bdim + tid; it < nit;
-       it += (unsigned long long)gridDim.x * bdim) {
+  // batches of 32 consecutive items claimed per warp from a counter, one ahead (the items' costs
+  // differ: a pruned item is a few loads, a simulated one ~n + #nodes events)
+  const int lane = tid & 31;
+  unsigned long long nb = 0;
+  if (lane == 0) nb = atomicAdd(P.counter2, 32ull);
+  for (;;) {
+    const unsigned long long b0 = __shfl_sync(FULL, nb, 0);
+    if (b0 >= nit) break;
+    if (lane == 0) nb = atomicAdd(P.counter2, 32ull);
+    const unsigned long long it = b0 + lane;
+    if (it >= nit) continue;
     const int2 item = P.items[it];
     const int64_t i = item.x;
     const int k = item.y;
