@@ -377,30 +377,27 @@ __device__ __forceinline__ void prep_rest(const KParams& P, int64_t inst, unsign
   const int E = n + Gn;
   int2* ge = P.ws_ent + inst * (int64_t)P.ws_ecap1;
   uint32_t* gm = P.ws_m0 + inst * (int64_t)P.ws_n4;
-  int m0 = 0;
+  // entry i (lane-strided): chain position p of its size in its task's chain (0 for the a^1
+  // entry), member interval [lo, hi) = [p ? rank of step p-1 + 1 : 0, p < g ? rank of step p + 1 : K),
+  // computed branch-free (both rank loads issued), stores through running pointers
+  int2* gep = ge + lane;
+  uint32_t* gmp = gm;
 #pragma unroll 1
-  for (int i = lane; i - lane < E; i += 32) {
-    const unsigned key = i < E ? kk[i] : 0xFFFFFFFFu;
+  for (int i = lane; i - lane < E; i += 32, gep += 32) {
+    const bool valid = i < E;
+    const unsigned key = valid ? kk[i] : 0u;
     const int c = (int)(key >> 29), j = (int)(key & 127u);
-    const int t = 0x3FFFFF - (int)((key >> 7) & 0x3FFFFFu);
-    bool a1 = false;
-    if (i < E) {
-      const uint32_t w = info[j];
-      const int g = (int)((w >> 8) & 7u), first = (int)(w >> 11);
-      a1 = c == (int)(w & 7u);
-      int lo = 0, hi;
-      if (a1) {
-        hi = g ? rnk[first] + 1 : K;
-      } else {  // growth entry: the p-th chain element, entered by step first + p - 1
-        const int p = __popc(((w >> 3) & 31u) & ((1u << c) - 1u));
-        lo = rnk[first + p - 1] + 1;
-        hi = p < g ? rnk[first + p] + 1 : K;
-      }
-      ge[i] = make_int2((int)((unsigned)t | ((unsigned)j << 22)), lo | (hi << 16));
-    }
+    const unsigned tj = ((0x3FFFFFu - ((key >> 7) & 0x3FFFFFu)) | ((unsigned)j << 22));
+    const uint32_t w = info[j];
+    const int g = (int)((w >> 8) & 7u), first = (int)(w >> 11);
+    const bool a1 = valid && c == (int)(w & 7u);
+    const int p = a1 ? 0 : __popc(((w >> 3) & 31u) & ((1u << c) - 1u));
+    const int rlo = rnk[max(first + p - 1, 0)], rhi = rnk[first + p];
+    const int lo = p ? rlo + 1 : 0, hi = p < g ? rhi + 1 : K;
+    if (valid) *gep = make_int2((int)tj, lo | (hi << 16));
     const unsigned b = __ballot_sync(FULL, a1);
-    if (a1) gm[m0 + __popc(b & lt)] = (unsigned)t | ((unsigned)j << 22);
-    m0 += __popc(b);
+    if (a1) gmp[__popc(b & lt)] = tj;
+    gmp += __popc(b);
   }
   // list offsets per size (meta[0..NC]) from the member-0 and growth counts
   {
