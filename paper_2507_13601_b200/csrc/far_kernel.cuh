@@ -204,6 +204,73 @@ template <int S> struct Frontier {
   }
 };
 
+// The same frontier kept SORTED by key (end << 3 | slot), for the hot Alg. 1 simulations of the
+// member kernels: the pop is k[0] (no min tree); a placement replaces the popped key by a larger one
+// (remove the front, sorted insert: one min and one max per position), a split inserts the second
+// child's key (the first child keeps slot bs and the popped key), a dropped leaf shifts the keys
+// down.  The keys are unique (slot bits), so the order -- and every pop -- is Frontier's.
+template <int S> struct SFrontier {
+  unsigned k[S];  // ascending; 0xFFFFFFFF = empty
+  uint32_t slotnode = 0, live = 1, has = 0;
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int s = 0; s < S; ++s) k[s] = 0xFFFFFFFFu;
+    k[0] = 0;  // root (node 0) in slot 0 at time 0
+    slotnode = 0;
+    live = 1;
+    has = 0;
+  }
+  __device__ __forceinline__ void pop(int& bs, int& be) const {
+    bs = (int)(k[0] & 7u);
+    be = (int)(k[0] >> 3);
+  }
+  __device__ __forceinline__ int node(int s) const { return (slotnode >> (4 * s)) & 15; }
+  // the popped slot bs gets end v (>= its old end): remove the front, insert the new key
+  __device__ __forceinline__ void set_front(int bs, int v) {
+    const unsigned key = ((unsigned)v << 3) | (unsigned)bs;
+    unsigned f[S];
+    f[0] = min(k[1], key);
+#pragma unroll
+    for (int s = 1; s < S - 1; ++s) f[s] = min(k[s + 1], max(k[s], key));
+    f[S - 1] = max(k[S - 1], key);
+#pragma unroll
+    for (int s = 0; s < S; ++s) k[s] = f[s];
+  }
+  __device__ __forceinline__ void insert(unsigned key) {  // k[S - 1] is empty
+    unsigned f[S];
+    f[0] = min(k[0], key);
+#pragma unroll
+    for (int s = 1; s < S; ++s) f[s] = min(k[s], max(k[s - 1], key));
+#pragma unroll
+    for (int s = 0; s < S; ++s) k[s] = f[s];
+  }
+  __device__ __forceinline__ int endv(int s) const {
+    int e = 0;
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+      if (k[q] != 0xFFFFFFFFu && (int)(k[q] & 7u) == s) e = (int)(k[q] >> 3);
+    return e;
+  }
+  // Alg. 1 lines 17-24 (repartitioning) after the optional destroy; returns false if v was a leaf.
+  __device__ __forceinline__ bool split(int bs, int be, uint32_t w) {
+    has &= ~(1u << bs);
+    const int ch1 = nd_ch1(w);
+    if (ch1 != LEAF) {
+      const int s2 = nd_ch2lo(w);
+      slotnode = (slotnode & ~(15u << (4 * bs))) | ((uint32_t)ch1 << (4 * bs));
+      slotnode = (slotnode & ~(15u << (4 * s2))) | ((uint32_t)nd_ch2(w) << (4 * s2));
+      live |= 1u << s2;
+      insert(((unsigned)be << 3) | (unsigned)s2);  // C.end := I.end for both children
+      return true;
+    }
+    live &= ~(1u << bs);
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) k[s] = k[s + 1];
+    k[S - 1] = 0xFFFFFFFFu;
+    return false;
+  }
+};
+
 // ---------------------------------------------------------------------------
 // Node-level replay (Alg. 2 line 26, O7).  Between two reconfiguration events of the
 // Alg. 1 event loop only task placements happen, and a node's tasks run back to back, so

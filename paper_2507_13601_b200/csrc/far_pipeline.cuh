@@ -43,7 +43,7 @@ __device__ int sim_member(const int2* __restrict__ ent, const int* loff, unsigne
   }
   if (REC)
     for (int v = 0; v < NN; ++v) npos[v * bdim] = 0;
-  Frontier<S> F;
+  SFrontier<S> F;
   F.init();
   int rec_end = 0, ms = 0;
   int sl[S];
@@ -85,7 +85,7 @@ __device__ int sim_member(const int2* __restrict__ ent, const int* loff, unsigne
       be += e.x & 0x3FFFFF;
       ms = max(ms, be);
       --total;
-      F.set(bs, be);
+      F.set_front(bs, be);
     } else {
       const uint32_t w = ninfo[v];
       if ((F.has >> bs) & 1) rec_end = max(rec_end, be) + de[nd_szi(w)];
@@ -126,7 +126,7 @@ __device__ int sim_member0(const uint32_t* row, unsigned long long cp, const uin
     total += r;
   }
   for (int v = 0; v < NN; ++v) npos[v * bdim] = 0;
-  Frontier<S> F;
+  SFrontier<S> F;
   F.init();
   int rec_end = 0, ms = 0;
   int sl[S];
@@ -160,7 +160,7 @@ __device__ int sim_member0(const uint32_t* row, unsigned long long cp, const uin
       be += (int)(x & 0x3FFFFFu);
       ms = max(ms, be);
       --total;
-      F.set(bs, be);
+      F.set_front(bs, be);
     } else {
       const uint32_t w = ninfo[v];
       if ((F.has >> bs) & 1) rec_end = max(rec_end, be) + de[nd_szi(w)];
