@@ -230,7 +230,9 @@ typedef struct {
  * replay's makespan.  For a schedule returned by far_solve_many the replay reproduces its
  * starts (fixpoint), so these are exactly the schedule's reconfigurations.  An instance whose
  * slot names a node that does not host its size gets d_nev = -1.  Costs: the ctx's, or zero
- * with FAR_ZERO_RECONFIG in opts->flags. */
+ * with FAR_ZERO_RECONFIG in opts->flags.  Multi-target contexts (far_create_multi): the
+ * replay runs over the forest (one heap, one reconfiguration sequence), node ids as in
+ * far_node_table, n <= 256 (FAR_E_TOO_LARGE).  FAR_SWITCH_COST: FAR_E_INVALID_ARG. */
 far_status far_schedule_events(far_ctx *ctx, const int32_t *d_times, int64_t I, int32_t n,
                                const far_task_slot *d_sched, const far_opts *opts, far_event *d_events,
                                int32_t *d_nev, int32_t *d_makespan, void *cuda_stream);
@@ -244,7 +246,8 @@ far_status far_schedule_events(far_ctx *ctx, const int32_t *d_times, int64_t I, 
  * node with tasks is created exactly once before its first task and destroyed at most once
  * after its last, nodes without tasks have no events, and of two nodes sharing a slice the
  * earlier-created one is destroyed before the other is created.  d_events/d_nev as written
- * by far_schedule_events (nev <= 2 * far_num_nodes). */
+ * by far_schedule_events (nev <= 2 * far_num_nodes).  Multi-target contexts: the same
+ * conditions over the forest's nodes and slices (n <= 256). */
 far_status far_validate_schedules(far_ctx *ctx, const int32_t *d_times, int64_t I, int32_t n,
                                   const far_task_slot *d_sched, const far_opts *opts, const far_event *d_events,
                                   const int32_t *d_nev, int32_t *d_violations, void *cuda_stream);

@@ -16,6 +16,7 @@
 #include "far_finish_lane.cuh"
 #include "far_check.cuh"
 #include "far_forest.cuh"
+#include "far_forest_check.cuh"
 #include "far_peak.cuh"
 
 using namespace farb;
@@ -127,6 +128,11 @@ static far_status ensure_device(far_ctx* ctx) {
     for (const void* f : cf) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   }
   for (const void* f : fns) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
+  {
+    const void* ff[4] = {(const void*)far_forest_events_kernel<3>, (const void*)far_forest_events_kernel<5>,
+                         (const void*)far_forest_validate_kernel<3>, (const void*)far_forest_validate_kernel<5>};
+    for (const void* f : ff) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
+  }
   CK(cudaFuncSetAttribute((const void*)far_forest_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   CK(cudaFuncSetAttribute((const void*)far_forest_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem_max));
   {
@@ -926,9 +932,15 @@ extern "C" far_status far_concat_streams(far_ctx* ctx, const int32_t* d_times, i
 // ---- schedule events and validation (far_check.cuh), one warp per instance
 static far_status launch_check(far_ctx* ctx, CParams& Q, int64_t I, int n, bool validate, cudaStream_t stream) {
   const bool a30 = ctx->nc == 3;
-  const int bytes = validate ? make_vlayout(n, ctx->nn).bytes : make_elayout(n, ctx->nn).bytes;
-  const void* fn = validate ? (a30 ? (const void*)far_validate_kernel<3> : (const void*)far_validate_kernel<5>)
-                            : (a30 ? (const void*)far_events_kernel<3> : (const void*)far_events_kernel<5>);
+  const bool forest = ctx->gpus > 1;
+  const int NNF = ctx->nn * ctx->gpus;
+  const int bytes = forest ? (validate ? make_fvlayout(n, NNF).bytes : make_felayout(n, ctx->nc, NNF).bytes)
+                           : (validate ? make_vlayout(n, ctx->nn).bytes : make_elayout(n, ctx->nn).bytes);
+  const void* fn =
+      forest ? (validate ? (a30 ? (const void*)far_forest_validate_kernel<3> : (const void*)far_forest_validate_kernel<5>)
+                         : (a30 ? (const void*)far_forest_events_kernel<3> : (const void*)far_forest_events_kernel<5>))
+             : (validate ? (a30 ? (const void*)far_validate_kernel<3> : (const void*)far_validate_kernel<5>)
+                         : (a30 ? (const void*)far_events_kernel<3> : (const void*)far_events_kernel<5>));
   int warps = 0, per_sm = 0;
   far_status st = pick_shape(ctx, fn, bytes, warps, per_sm);
   if (st) return st;
@@ -941,7 +953,21 @@ static far_status launch_check(far_ctx* ctx, CParams& Q, int64_t I, int n, bool 
   if ((st = t_begin(ctx, stream, tset))) return st;
   const size_t smem = (size_t)warps * bytes;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((I + warps - 1) / warps, (int64_t)ctx->sms * per_sm));
-  if (validate) {
+  if (forest) {  // multi-target contexts: the generic forest kernels (far_forest_check.cuh)
+    FCParams C;
+    memset(&C, 0, sizeof(C));
+    fill_params(ctx, nullptr, C.F.P);
+    for (int c = 0; c < 8; ++c) {
+      C.F.P.cr[c] = Q.cr[c];
+      C.F.P.de[c] = Q.de[c];
+    }
+    C.F.nodes = ctx->d_fnodes;
+    C.F.NNF = NNF;
+    C.F.SF = ctx->ns * ctx->gpus;
+    C.Q = Q;
+    void* args[] = {&C};
+    CK(cudaLaunchKernel(fn, grid, warps * 32, args, smem, stream));
+  } else if (validate) {
     if (a30) far_validate_kernel<3><<<grid, warps * 32, smem, stream>>>(Q);
     else far_validate_kernel<5><<<grid, warps * 32, smem, stream>>>(Q);
   } else {
@@ -956,7 +982,7 @@ static far_status launch_check(far_ctx* ctx, CParams& Q, int64_t I, int n, bool 
 
 static far_status check_args(far_ctx* ctx, const int32_t* d_times, int64_t I, int32_t n, const far_task_slot* d_sched,
                              const far_opts* opts, CParams& Q) {
-  if (ctx->gpus > 1) return fail(ctx, FAR_E_UNSUPPORTED_PROFILE, "events / validator: single-GPU trees only");
+  if (ctx->gpus > 1 && n > FMAXN) return fail(ctx, FAR_E_TOO_LARGE, "multi-GPU forest: n > 256");
   if (opts && (opts->flags & FAR_SWITCH_COST))
     return fail(ctx, FAR_E_INVALID_ARG, "events / validator: no FAR_SWITCH_COST");
   if (I < 0 || n < 0) return fail(ctx, FAR_E_INVALID_ARG, "negative I or n");

@@ -90,8 +90,11 @@ template <int NC, bool LISTS>
 __device__ int forest_sim(const FParams& F, int n, const int32_t* T, const uint16_t* glist, const int* gcnt, int* gptr,
                           const uint16_t* L, const int* off, int* cursor, const uint8_t* su, int* rstart,
                           uint8_t* rnode, uint8_t* rpos, uint8_t* rsu, int* ncnt, long long& pops, int lane,
-                          uint8_t* isz) {
+                          uint8_t* isz, far_event* ev = nullptr, int* nevp = nullptr) {
+  // ev (optional): the reconfiguration events in the order rec issues them (creates, and the
+  // destroys of lines 18-20 while tasks remain), nevp their count
   const KParams& P = F.P;
+  int nev = 0;
   const int NNF = F.NNF;
   const bool r7 = (P.flags & FAR_SWITCH_COST) != 0;  // DESIGN.md R7 variant
   for (int v = lane; v < NNF; v += 32) {
@@ -148,6 +151,10 @@ __device__ int forest_sim(const FParams& F, int n, const int32_t* T, const uint1
       if (!has) {  // lines 8-11: give time for I's creation
         const int cs = max(rec, end);
         rec = cs + P.cr[r7 ? tc : fn_szi(w)];
+        if (ev) {
+          if (lane == 0) ev[nev] = far_event{0, v, cs, rec - cs};
+          ++nev;
+        }
         end = rec;
         has = 1;
         if (lane == 0) isz[v] = (uint8_t)tc;
@@ -172,7 +179,14 @@ __device__ int forest_sim(const FParams& F, int n, const int32_t* T, const uint1
       nslot_node = v;
       ne = end;
     } else if (unsched > 0) {  // line 17: repartition
-      if (has) rec = max(rec, end) + P.de[(r7 && fn_c1(w) != NONE) ? cur_isz : fn_szi(w)];  // lines 18-20
+      if (has) {  // lines 18-20
+        const int ds = max(rec, end);
+        rec = ds + P.de[(r7 && fn_c1(w) != NONE) ? cur_isz : fn_szi(w)];
+        if (ev) {
+          if (lane == 0) ev[nev] = far_event{1, v, ds, rec - ds};
+          ++nev;
+        }
+      }
       if (fn_ch1(w) == FNONE) {
         clear = true;
       } else {  // lines 21-24: children start at I.end
@@ -197,6 +211,7 @@ __device__ int forest_sim(const FParams& F, int n, const int32_t* T, const uint1
     }
     __syncwarp();
   }
+  if (nevp && lane == 0) *nevp = nev;
   return ms;
 }
 

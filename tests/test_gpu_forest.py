@@ -105,3 +105,56 @@ def test_forest_errors(torch_dev):
         F.concat_streams(d.reshape(1, 2, 8, 5))
     with pytest.raises(far.FarError):
         far.Far("A100x9")
+
+
+@pytest.mark.parametrize("prof,n,count", [("A30x2", 16, 100), ("A100x2", 24, 100), ("A100x4", 40, 60),
+                                          ("H100x3", 12, 100), ("A30x8", 64, 30), ("A100x8", 128, 12)])
+def test_forest_events_match_oracle(O, torch_dev, prof, n, count):
+    """far_schedule_events / far_validate_schedules on multi-target contexts (NEXT-2 x NEXT-4): the
+    forest replay's creates and the destroys issued while tasks remain equal the oracle's event list
+    of the same FAR output, the replay reproduces the makespan, and every output is feasible for both
+    validators."""
+    import test_gpu_check as TC
+    base = prof.split("x")[0]
+    costs = inputs.reconfig_costs(base)
+    tab = inputs.synthetic(base, n, count, 700 + n)
+    for flags in (0, far.NO_REFINE, far.ZERO_RECONFIG):
+        F, d, sd, ms, slots, evs, nev, ems, viol = TC.solve_and_events(torch_dev, prof, costs, tab, flags=flags)
+        assert (ems == ms).all(), "the replay of a FAR output reproduces its makespan (fixpoint)"
+        assert (viol == 0).all(), f"infeasible outputs at {np.nonzero(viol)[0][:10]}"
+        for i in range(count):
+            o = O.far(prof, costs, tab[i], flags=flags & (O.NO_REFINE | O.ZERO_RECONFIG))
+            assert TC.ordered(evs[i]) == TC.ordered(o["events"]), f"{prof} flags {flags}: events differ, instance {i}"
+            oc = inputs.reconfig_costs(base, zero=True) if flags & far.ZERO_RECONFIG else costs
+            assert O.validate(prof, oc, tab[i], TC.to_oracle_slots(slots[i]), TC.to_oracle_events(evs[i])) == 0
+
+
+@pytest.mark.parametrize("prof", ["A30x2", "A100x3"])
+def test_forest_validator_counts_match_oracle(O, torch_dev, prof):
+    """Violation counts of corrupted multi-target schedules and events equal orc_validate's."""
+    import test_gpu_check as TC
+    torch, dev = torch_dev
+    base = prof.split("x")[0]
+    costs = inputs.reconfig_costs(base)
+    tab = inputs.synthetic(base, 14, 300, 41)
+    F, d, sd, ms, slots, evs, nev, ems, viol = TC.solve_and_events(torch_dev, prof, costs, tab)
+    lo, hi, _ = F.node_table()
+    rng = np.random.default_rng(6)
+    cap = 2 * F.nnodes
+    S = np.zeros((tab.shape[0], tab.shape[1]), far.SLOT_DT)
+    E = np.zeros((tab.shape[0], cap), far.EVENT_DT)
+    NE = np.zeros(tab.shape[0], np.int32)
+    for i in range(tab.shape[0]):
+        s, e = slots[i], evs[i]
+        for _ in range(rng.integers(1, 3)):
+            s, e = TC.perturb(rng, prof, s, e, tab[i], lo, hi)
+        e = e[:cap]
+        S[i], E[i, :len(e)], NE[i] = s, e, len(e)
+    dS = torch.from_numpy(S.view(np.uint8).reshape(tab.shape[0], tab.shape[1], 8)).to(dev)
+    dE = torch.from_numpy(E.view(np.uint8).reshape(tab.shape[0], cap, 16)).to(dev)
+    dN = torch.from_numpy(NE).to(dev)
+    v = F.validate_schedules(d, dS, dE, dN).cpu().numpy()
+    want = np.array([O.validate(prof, costs, tab[i], TC.to_oracle_slots(S[i]), TC.to_oracle_events(E[i, :NE[i]]))
+                     for i in range(tab.shape[0])])
+    assert (v == want).all(), f"mismatch at {np.nonzero(v != want)[0][:10]}: gpu {v[v != want][:5]} oracle {want[v != want][:5]}"
+    assert (want > 0).mean() > 0.5
