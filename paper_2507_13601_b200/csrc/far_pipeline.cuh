@@ -285,38 +285,51 @@ __global__ void __launch_bounds__(128) far_member0_kernel(PParams P) {
       }
       __syncwarp();
     }
-    if (!active) continue;
-    const int* meta = P.ws_meta + i * 16;
-    const int K = meta[WS_K];
+    int K = 0, ms0 = 0;
     const int* lb = P.ws_lb + i * (int64_t)P.ws_kcap;
-    int pops = 0;
-    const int ms0 = sim_member0<NC>(row, P.ws_cnt[i * (int64_t)P.ws_kcap], sm.ninfo, sm.cr, sm.de, st, npos, bdim,
-                                    P.ws_rec + i * (int64_t)P.n, P.ws_sl + i * 8, pops);
-    for (int v = 0; v < NN; ++v) P.ws_ncnt[i * 16 + v] = npos[v * bdim];
-    const unsigned long long b0 = best_key(ms0, 0);
-    P.ws_best[i] = b0;
-    P.ws_evt[i] = (unsigned long long)pops;
+    if (active) {
+      K = P.ws_meta[i * 16 + WS_K];
+      int pops = 0;
+      ms0 = sim_member0<NC>(row, P.ws_cnt[i * (int64_t)P.ws_kcap], sm.ninfo, sm.cr, sm.de, st, npos, bdim,
+                            P.ws_rec + i * (int64_t)P.n, P.ws_sl + i * 8, pops);
+      for (int v = 0; v < NN; ++v) P.ws_ncnt[i * 16 + v] = npos[v * bdim];
+      P.ws_best[i] = best_key(ms0, 0);
+      P.ws_evt[i] = (unsigned long long)pops;
+    }
     // members that can still beat (ms_0, 0): (LB_k, k) < (ms_0, 0) lexicographically, i.e.
-    // LB_k < ms_0 (k >= 1).  One pass, 32 members per chunk: 16-B loads (ws_kcap is a multiple of
-    // 4), a bit per candidate, one atomic per chunk with candidates.
-    for (int k0 = 0; k0 < K; k0 += 32) {
+    // LB_k < ms_0 (k >= 1).  32 members per chunk: 16-B loads (ws_kcap is a multiple of 4), a bit
+    // per candidate; the warp's candidates of a chunk take one atomic (lane offsets by a warp scan),
+    // each lane's items stay consecutive
+    const int Kw = __reduce_max_sync(FULL, (unsigned)K);
+    for (int k0 = 0; k0 < Kw; k0 += 32) {
       unsigned mask = 0;
+      if (k0 < K) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (k0 + 4 * u < K) {
-          const int4 x = __ldg((const int4*)(lb + k0) + u);
-          mask |= (unsigned)(exhaustive || x.x < ms0) << (4 * u);
-          mask |= (unsigned)(exhaustive || x.y < ms0) << (4 * u + 1);
-          mask |= (unsigned)(exhaustive || x.z < ms0) << (4 * u + 2);
-          mask |= (unsigned)(exhaustive || x.w < ms0) << (4 * u + 3);
+        for (int u = 0; u < 8; ++u) {
+          if (k0 + 4 * u < K) {
+            const int4 x = __ldg((const int4*)(lb + k0) + u);
+            mask |= (unsigned)(exhaustive || x.x < ms0) << (4 * u);
+            mask |= (unsigned)(exhaustive || x.y < ms0) << (4 * u + 1);
+            mask |= (unsigned)(exhaustive || x.z < ms0) << (4 * u + 2);
+            mask |= (unsigned)(exhaustive || x.w < ms0) << (4 * u + 3);
+          }
         }
+        if (k0 == 0) mask &= ~1u;                                // member 0 itself
+        if (K - k0 < 32) mask &= (1u << (K - k0)) - 1u;         // past the family
       }
-      if (k0 == 0) mask &= ~1u;                                // member 0 itself
-      if (K - k0 < 32) mask &= (1u << (K - k0)) - 1u;         // past the family
-      if (mask) {
-        unsigned long long slot = atomicAdd(P.nitems, (unsigned long long)__popc(mask));
-        for (; mask; mask &= mask - 1) P.items[slot++] = make_int2((int)i, k0 + __ffs(mask) - 1);
+      const int cnt = __popc(mask);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
       }
+      const int tot = __shfl_sync(FULL, incl, 31);
+      if (tot == 0) continue;
+      unsigned long long slot = 0;
+      if (lane == 31) slot = atomicAdd(P.nitems, (unsigned long long)tot);
+      slot = __shfl_sync(FULL, slot, 31) + (unsigned long long)(incl - cnt);
+      for (; mask; mask &= mask - 1) P.items[slot++] = make_int2((int)i, k0 + __ffs(mask) - 1);
     }
   }
   (void)NN;
