@@ -471,39 +471,30 @@ __device__ __forceinline__ void prep_instance(const KParams& P, int64_t inst, un
     bad |= mn < 1;
     bsum += mx;
     tmax = max(tmax, mx);
-    // 32-bit products: meaningful once t < 2^22 is established (checked below)
-    int best = 0;
-    unsigned bw = (unsigned)tv[0];
+    // 32-bit products: meaningful once t < 2^22 is established (checked below).
+    // The growth chain a^1 -> nx(a^1) -> ... (nx(c) = argmin_{c' > c} (size(c') t(c'), c')) is the
+    // set of suffix-minimum positions of w_c = size(c) t(c): c is on it iff w_c <= w_c'' for every
+    // c'' > c (ties -> smallest index, as in nx), and a^1 (the first minimum) is its lowest element.
+    // One downward pass gives the chain mask, a^1, its work and duration, and the monotonicity of t
+    // along the chain.
+    unsigned cb = 1u << (NC - 1);
+    unsigned bw = (unsigned)size_of<NC>(NC - 1) * (unsigned)tv[NC - 1];
+    int tb = tv[NC - 1];
 #pragma unroll
-    for (int c = 1; c < NC; ++c) {
-      const unsigned w = (unsigned)size_of<NC>(c) * (unsigned)tv[c];
-      if (w < bw) { bw = w; best = c; }
-    }
-    unsigned nxp = 0;  // nx(c), 3 bits per size index
-    {
-      int above = NC - 1;
-      unsigned wa = (unsigned)size_of<NC>(NC - 1) * (unsigned)tv[NC - 1];
-#pragma unroll
-      for (int c = NC - 2; c >= 0; --c) {
-        nxp |= (unsigned)above << (3 * c);
-        const unsigned wc = (unsigned)size_of<NC>(c) * (unsigned)tv[c];
-        if (wc <= wa) { wa = wc; above = c; }
-      }
-    }
-    unsigned cb = 0;
-    int nextc = best, tprev = INT_MAX;
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-      if (c == nextc) {
+    for (int c = NC - 2; c >= 0; --c) {
+      const unsigned wc = (unsigned)size_of<NC>(c) * (unsigned)tv[c];
+      if (wc <= bw) {
+        bw = wc;
         cb |= 1u << c;
-        mono &= tv[c] <= tprev;
-        tprev = tv[c];
-        nextc = c == NC - 1 ? NC : (int)((nxp >> (3 * c)) & 7u);
+        mono &= tv[c] >= tb;
+        tb = tv[c];
       }
+    }
+    const int best = __ffs(cb) - 1;
     tstar = max(tstar, growth_key<NC>(tv[NC - 1], j, __popc(cb) - 1));
     W += bw;
     c0 += 1ull << (11 * best);
-    d0[j] = (uint32_t)tv[best];  // t_j(a^1_j): member 0's duration (finish, k* = 0)
+    d0[j] = (uint32_t)tb;  // t_j(a^1_j): member 0's duration (finish, k* = 0)
     info[j] = (uint32_t)best | (cb << 3);
   }
   bad = __any_sync(FULL, bad);
