@@ -213,13 +213,13 @@ __device__ __forceinline__ void prep_rest(const KParams& P, int64_t inst, unsign
 #pragma unroll 1
     for (int j = lane; j < n; j += 32) {
       const uint32_t w = info[j];
-      unsigned m = (w >> 3) & ((1u << (NC - 1)) - 1u);
-      int g = 0;
+      const unsigned m = (w >> 3) & ((1u << (NC - 1)) - 1u);  // non-terminal chain elements
+      int g = 0, p = 0;
 #pragma unroll
-      for (int p = 0; p < NC - 1; ++p) {
-        const int c = m ? __ffs(m) - 1 : 0;
-        g += (m != 0) & (growth_key<NC>(T[j * NC + c], j, p) > tstar);
-        m &= m - 1;
+      for (int c = 0; c < NC - 1; ++c) {  // size index c (compile-time offset), chain position p
+        const bool on = (m >> c) & 1u;
+        g += on & (growth_key<NC>(T[j * NC + c], j, p) > tstar);
+        p += on;
       }
       info[j] = w | ((uint32_t)g << 8);
       gsum += g;
