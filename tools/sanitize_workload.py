@@ -78,9 +78,14 @@ for profile in ("A30", "A100"):
     # multi-target forest
     G = far.Far(profile + "x2", costs)
     tg = inputs.synthetic(profile, 20, 40, 17)
-    G.solve_many(torch.from_numpy(tg).to(dev))
-    G.solve_many(torch.from_numpy(tg).to(dev), flags=fl.BEST_IMPROVEMENT)
+    dg = torch.from_numpy(tg).to(dev)
+    _, sg, _ = G.solve_many(dg)
+    G.solve_many(dg, flags=fl.BEST_IMPROVEMENT)
+    # events + validator on the forest (far_forest_check.cuh)
+    evg, nevg, _ = G.schedule_events(dg, sg)
+    violg = G.validate_schedules(dg, sg, evg, nevg)
     torch.cuda.synchronize()
+    assert int(violg.sum()) == 0
     G.sync()
     G.close()
 
