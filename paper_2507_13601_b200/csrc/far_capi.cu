@@ -338,6 +338,7 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
   const bool pipe = P.mode == MODE_SOLVE && P.n > 0 && P.n <= 1023 && !getenv("FAR_FUSED_PHASE2") &&
                     !(P.flags & FAR_SWITCH_COST) && (P.I >= 256 || getenv("FAR_PIPELINE_ALWAYS"));
   const bool need_ovf = P.mode == MODE_SOLVE && (kfast < kmax || pipe);
+  if (getenv("FAR_DEBUG_NO_ROUND_BALANCE")) P.flags |= FAR_I_NO_ROUND_BALANCE;  // experiments (A/B)
   const int64_t lid = ctx->launch_id++;
   const int slot = (int)(lid % NREC) * CPL;
   far_status st;

@@ -30,6 +30,8 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int MAXN = 1024;
 constexpr int BOUND = 1 << 29;
 enum { MODE_SOLVE = 0, MODE_LOCAL = 1 };
+// internal flag bits (never part of the public far_opts.flags; set by the C-ABI for experiments)
+constexpr unsigned FAR_I_NO_ROUND_BALANCE = 1u << 30;  // FAR_DEBUG_NO_ROUND_BALANCE: members keep the full grid
 
 struct KParams {
   const int32_t* times;
