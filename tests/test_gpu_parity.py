@@ -438,6 +438,29 @@ def test_full_size_m5_parity(O, torch_dev):
     assert nbad == 0, f"{nbad} schedules differ, first at instance {first}"
 
 
+@pytest.mark.parametrize("world,rank", [(8, 7), (4, 1)])
+def test_strong_scaling_shard_parity(O, torch_dev, world, rank):
+    """Config 5 under strong scaling: the shard one rank solves (dist.shard_range(1M, rank, world):
+    125k instances at N = 8 -- the members stage's one-to-two-round branch -- and 250k at N = 4),
+    generated exactly as bench.py does (counter-based table from the shard's first index), solved
+    on the GPU at the shard's size, every makespan, report field and task slot bit-exact."""
+    from paper_2507_13601_b200 import dist as fdist
+    torch, dev = torch_dev
+    w = inputs.WORKLOADS["M5"]
+    lo, hi = fdist.shard_range(1_000_000, rank, world)
+    tab = inputs.synthetic_parallel(w.profile, w.n, hi - lo, w.seed, scaling=w.scaling, times=w.times, start=lo)
+    F = far.Far(w.profile, w.costs())
+    ms, sd, rs = F.solve_many(torch.from_numpy(tab).to(dev))
+    torch.cuda.synchronize()
+    F.sync()
+    ms, res, slots = ms.cpu().numpy(), far.results_np(rs), far.slots_np(sd)
+    oms, ores, nbad, first = O.far_many_parallel_check(w.profile, w.costs(), tab, slots)
+    assert (ms == oms).all(), f"makespan mismatch at {np.nonzero(ms != oms)[0][:10]}"
+    for k in FIELDS:
+        assert (res[k] == ores[k]).all(), k
+    assert nbad == 0, f"{nbad} schedules differ, first at instance {first}"
+
+
 @pytest.mark.parametrize("profile,gen,n", [("A100", "mixed", 16), ("H100", "mixed", 40), ("A100", "ties", 24),
                                            ("A100", "monoties", 24), ("A30", "mixed", 12), ("A100", "mixed", 300)])
 def test_switch_cost_variant(O, torch_dev, profile, gen, n):
