@@ -449,10 +449,13 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
       const void* f0 = a30 ? (const void*)far_member0_kernel<3> : (const void*)far_member0_kernel<5>;
       int per_sm = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f0, tb0, sm0));
-      // n > 64: at most 8 warps per SM -- measured on M5 (1M x n = 128) 1.33 ms at 8 warps (2 x 128,
-      // 4 x 64 or 8 x 32 threads) against 1.48 at the 12 the shared memory allows, 1.48-1.51 at 9-10,
-      // 1.53 at 6; M3 (100k x n = 32, short rows, one pass over the instances) keeps full occupancy
-      if (P.n > 64) per_sm = std::min(per_sm, std::max(1, 256 / tb0));
+      // n > 64: at most 12 warps per SM -- measured on M5 (1M x n = 128): with one atomic per lane for
+      // the candidate items 8 warps were best (1.33 ms, 1.48 at 12); since the warp-aggregated item
+      // emission 12 (the shared-memory limit at n = 128) is: 1.067 ms against 1.18 at 8 and 10 (block
+      // size 64 or 128); M3 (100k x n = 32, short rows, one pass over the instances) keeps full occupancy
+      int m0_warps = 12;
+      if (const char* e = getenv("FAR_DEBUG_M0_WARPS")) m0_warps = std::max(1, atoi(e));  // experiments
+      if (P.n > 64) per_sm = std::min(per_sm, std::max(1, m0_warps * 32 / tb0));
       if (const char* e = getenv("FAR_DEBUG_M0_BPS")) per_sm = std::min(per_sm, atoi(e));  // experiments
       const int g0 = (int)std::max<int64_t>(1, std::min<int64_t>((P.I + tb0 - 1) / tb0, (int64_t)ctx->sms * std::max(1, per_sm)));
       if (a30) far_member0_kernel<3><<<g0, tb0, sm0, stream>>>(Q);
