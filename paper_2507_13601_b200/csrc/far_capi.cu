@@ -440,7 +440,7 @@ static far_status launch_solve(far_ctx* ctx, KParams& P, cudaStream_t stream) {
     if (const char* e = getenv("FAR_DEBUG_MEMBERS_BPS")) items_per_sm = std::max(1, std::min(16, atoi(e)));  // experiments
     const int g_items = ctx->sms * items_per_sm;
     {  // K2: per-thread shared-memory copy of member 0's lists -> block size by footprint
-      const size_t per_thread = (size_t)4 * NC + 2 * NN + 4 * (size_t)(n4 + 1);
+      const size_t per_thread = (size_t)4 * NC + 2 * NN + 4 * (size_t)(n4 + 4);  // row stride n4 + 4 (TMA) or n4 + 1
       int tbmax = 128;
       if (const char* e = getenv("FAR_DEBUG_M0_TB")) tbmax = std::max(32, std::min(128, atoi(e)));  // experiments
       const int tb0 = (int)std::min<size_t>(tbmax, (size_t)ctx->smem_max / per_thread / 32 * 32);

@@ -225,6 +225,10 @@ __device__ __forceinline__ void pipe_prologue(const PParams& P, PipeSmem<NC>& sm
   __syncthreads();
 }
 
+#ifndef FAR_M0_TMA
+#define FAR_M0_TMA 1  // member0 stages its lists with TMA bulk copies
+#endif
+
 // K2: member 0 of every pending instance (recorded), then the candidate members as items.
 template <int NC>
 __global__ void __launch_bounds__(128) far_member0_kernel(PParams P) {
@@ -235,9 +239,22 @@ __global__ void __launch_bounds__(128) far_member0_kernel(PParams P) {
   const int bdim = blockDim.x, tid = threadIdx.x;
   uint32_t* st = (uint32_t*)dsm + tid;
   uint16_t* npos = (uint16_t*)(dsm + 4 * NC * bdim) + tid;
-  // this thread's copy of member 0's lists (odd row stride n4 + 1 words: the rows of a warp start
-  // in 32 different banks)
+  // this thread's copy of member 0's lists.  FAR_M0_TMA: row stride n4 + 4 words (16-B aligned rows,
+  // filled by TMA bulk copies); otherwise n4 + 1 (odd: the rows of a warp start in 32 different banks)
+#if FAR_M0_TMA
+  const int nw = P.ws_n4, rs = nw + 4, lane = tid & 31;
+  __shared__ __align__(8) unsigned long long m0bar[4];  // one mbarrier per warp (blocks of <= 128)
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&m0bar[tid >> 5]);
+  unsigned phase = 0;
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncwarp();
+#else
   const int nw = P.ws_n4, rs = nw + 1, lane = tid & 31;
+#endif
   uint32_t* wrows = (uint32_t*)(dsm + (4 * NC + 2 * NN) * bdim) + (size_t)(tid & ~31) * rs;
   uint32_t* row = wrows + (size_t)lane * rs;
   const bool exhaustive = (P.flags & FAR_EXHAUSTIVE) != 0;
@@ -255,6 +272,38 @@ __global__ void __launch_bounds__(128) far_member0_kernel(PParams P) {
     const int64_t i = base + lane;
     const bool active = i < P.I && !P.ws_meta[i * 16 + WS_FLAG];
     __syncwarp();  // every lane is done with its row (previous instance)
+#if FAR_M0_TMA
+    {  // lane 0 issues one TMA bulk copy per active instance (its whole member-0 list row, global ->
+       // this warp's rows) on the warp's mbarrier; every lane waits for the transaction bytes
+      const unsigned am = __ballot_sync(FULL, active);
+      if (am) {
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the rows' generic reads first
+          const unsigned bytes = 4u * (unsigned)nw;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes * __popc(am))
+                       : "memory");
+          const uint32_t* src0 = P.ws_m0 + (i - lane) * (int64_t)nw;
+          for (unsigned m = am; m; m &= m - 1) {
+            const int u = __ffs(m) - 1;
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(wrows + (size_t)u * rs);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                "l"(src0 + (int64_t)u * nw), "r"(bytes), "r"(bar)
+                : "memory");
+          }
+        }
+        unsigned done = 0;
+        while (!done) {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+              : "=r"(done)
+              : "r"(bar), "r"(phase)
+              : "memory");
+        }
+        phase ^= 1u;
+      }
+    }
+#else
     {  // the warp copies its instances' lists: coalesced 128-B loads, eight instances' loads in
        // flight per lane (one exposed latency per eight instances), conflict-free stores into the rows
       const uint32_t* src = P.ws_m0 + (i - lane) * (int64_t)nw;
@@ -285,6 +334,7 @@ __global__ void __launch_bounds__(128) far_member0_kernel(PParams P) {
       }
       __syncwarp();
     }
+#endif
     int K = 0, ms0 = 0;
     const int* lb = P.ws_lb + i * (int64_t)P.ws_kcap;
     if (active) {
