@@ -26,6 +26,10 @@
 
 namespace farb {
 
+#ifndef FAR_PREP_TMA
+#define FAR_PREP_TMA 1  // H0 stages the runtime table with one TMA bulk copy per instance
+#endif
+
 struct PLayout {
   int T, info, gk, ginfo, rnk, cnts, lbs, lbh, kk, bytes;
 };
@@ -419,7 +423,7 @@ __device__ __forceinline__ void prep_rest(const KParams& P, int64_t inst, unsign
 
 template <int NC, bool MONO>
 __device__ __forceinline__ void prep_instance(const KParams& P, int64_t inst, unsigned char* wsm, const PLayout& L,
-                                           int lane) {
+                                           int lane, unsigned bar, unsigned& phase) {
   constexpr int S = Tree<NC>::S;
   const int n = P.n;
   int32_t* T = (int32_t*)(wsm + L.T);
@@ -438,7 +442,28 @@ __device__ __forceinline__ void prep_instance(const KParams& P, int64_t inst, un
   {
     const int cntT = n * NC;
     const int32_t* src = P.times + inst * (int64_t)cntT;
-    if ((((uintptr_t)src) & 15) == 0) {
+    if (FAR_PREP_TMA && (((uintptr_t)src) & 15) == 0 && (cntT & 3) == 0) {
+      // one TMA bulk copy of the whole table (global -> this warp's T), issued by lane 0 on the
+      // warp's mbarrier; the table's generic reads of the previous instance are ordered first
+      if (lane == 0) {
+        const unsigned bytes = 4u * (unsigned)cntT;
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(T);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                     "l"(src), "r"(bytes), "r"(bar)
+                     : "memory");
+      }
+      unsigned done = 0;
+      while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(phase)
+            : "memory");
+      }
+      phase ^= 1u;
+    } else if ((((uintptr_t)src) & 15) == 0) {
       const int n4 = cntT >> 2;
       const int4* s4 = (const int4*)src;
       int4* d4 = (int4*)T;
@@ -552,6 +577,15 @@ __global__ void __launch_bounds__(128, 8) far_prep_kernel(KParams P) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const PLayout L = make_playout(P.n, NC, P.kcap);
   unsigned char* wsm = smem + (size_t)warp * L.bytes;
+  __shared__ __align__(8) unsigned long long tbar[4];  // one mbarrier per warp (blocks of 128)
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&tbar[warp]);
+  unsigned phase = 0;
+  if (FAR_PREP_TMA && lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncwarp();
   const int64_t total = MONO ? P.I : (int64_t)*(volatile unsigned long long*)P.gen_count;
   // dynamic instance scheduler, next index claimed one instance ahead
   unsigned long long nxt = 0;
@@ -560,7 +594,7 @@ __global__ void __launch_bounds__(128, 8) far_prep_kernel(KParams P) {
     const unsigned long long it = __shfl_sync(FULL, nxt, 0);
     if ((int64_t)it >= total) break;
     if (lane == 0) nxt = atomicAdd(P.counter, 1ull);
-    prep_instance<NC, MONO>(P, MONO ? (int64_t)it : P.gen_list[it], wsm, L, lane);
+    prep_instance<NC, MONO>(P, MONO ? (int64_t)it : P.gen_list[it], wsm, L, lane, bar, phase);
     __syncwarp();
   }
 }
